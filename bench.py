@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""SRLA benchmark: packets/s scanned + end-of-slice latency (BASELINE.json).
+
+Workload (BASELINE.json configs[1], "C2" in SURVEY.md §8d): one B200 per rank,
+sketch u=4, v=2^20, g=8, g'=1024, z=4 (u8 recorders), k=10, theta=1024, seed
+0x5EA00001; synthetic trace = the reference generator's C2 spec (uniform 4M
+sources, Zipf(1.0) 4M destinations, 50 planted super points), 1e8 packets per
+slice per GPU, produced byte-identically on the device and resident in HBM
+(1.2 GB per slice, > L2, so no flush is needed between steps).
+
+A step = DetectPipeline::process_slice on one slice: scan (K1..K5) + report
+(when the window is full) + slide. N > 1: hosts are owner-partitioned
+(reduce(3, aip, N)); every rank keeps an independent sketch for its hosts and
+the per-slice report is all-gathered over NCCL (the only collective).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "packets/sec scanned (1/2/4/8 B200); end-of-slice estimation latency ms"
+ALGO_BYTES_PER_PACKET = 140  # 12 B streamed record + 4 rows x one 32-B sector update
+
+
+def plant_cards():
+    return [int(math.floor(1152.0 * math.pow(16384.0 / 1152.0, i / 49.0) + 0.5)) for i in range(50)]
+
+
+def sketch_cfg(cols):
+    return dict(rows=4, cols=cols, rough_slots=8, linear_slots=1024, recorder_bits=4, window=10, theta=1024,
+                seed=0x5EA00001)
+
+
+def trace_spec(pairs, slices=12):
+    return dict(seed=1, slices=slices, window=10, a_hosts=4194304, b_hosts=1 << 22, pairs_per_slice=pairs,
+                skew=1.0, plants=[(0x0AC80001 + i, c, 0, 0xFFFFFFFF) for i, c in enumerate(plant_cards())])
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, local_rank):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = str(local_rank)
+        if vis:
+            parts = vis.split(",")
+            if local_rank < len(parts):
+                idx = parts[local_rank].strip()
+        self.lines = []
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU reference (checker only)
+
+def cpu_reference(sample_recs, cols, threads, slice_id):
+    """Time the reference's own DetectPipeline (oracle/_ref = the unmodified
+    headers; the C restatement if _ref is absent) on a bounded sample.
+    Returns scan rate and end-of-slice ms (report_window + slide)."""
+    from oracle.pyoracle import LIBS, Checker, SeaConfig, build
+    kind = "reference"
+    if not os.path.exists(LIBS["ref"]):
+        kind = "port"
+        if not os.path.exists(LIBS["orc"]):
+            build()
+    chk = Checker("ref" if kind == "reference" else "orc")
+    pipe = chk.pipeline(SeaConfig(**sketch_cfg(cols)), workers=threads)
+    t0 = time.perf_counter()
+    pipe.process_slice(slice_id, sample_recs, True)
+    total_ms = (time.perf_counter() - t0) * 1e3
+    scan_ms = pipe.scan_ms
+    return {"kind": kind, "scan_rate": len(sample_recs) / (scan_ms / 1e3), "scan_ms": scan_ms,
+            "eos_ms": total_ms - scan_ms, "threads": threads if kind == "reference" else 1}
+
+
+def sample_records(n, device):
+    """First n background packets (plus the plants) of C2 slice 0 — an exact
+    prefix of the benchmark's own slice 0 (same generator draws)."""
+    import numpy as np
+    from paper_1803_10369_b200.srla import DeviceTraceGenerator, PlantSpec
+    gen = DeviceTraceGenerator(PlantSpec(**trace_spec(n, slices=1)), device=device)
+    return gen.slice_tensor(0).cpu().numpy().view(np.uint32).copy()
+
+
+def run_reference_arm(args):
+    rank, world, local = env_rank()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    samp_n = args.cpu_sample
+    recs = sample_records(samp_n, local)
+    full = args.packets
+    per_step = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = cpu_reference(recs, args.cols, threads, slice_id=9)
+        ms_full = full / res["scan_rate"] * 1e3 + res["eos_ms"]
+        if i >= args.warmup:
+            per_step.append((ms_full, res))
+    ms = statistics.mean(p[0] for p in per_step)
+    value = full / (ms / 1e3)
+    eos = [p[1]["eos_ms"] for p in per_step]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "packets/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "C2: u=4 v=2^20 g=8 g'=1024 z=4 k=10 theta=1024; 1e8 packets/slice",
+                   "packets_per_slice": full, "parallelism": "cpu threads"},
+        "end_of_slice_ms": {"median": statistics.median(eos), "p99": max(eos)},
+        "cpu_baseline": {"value": value, "unit": "packets/s", "cores": res["threads"], "kind": res["kind"],
+                         "sample": f"each step: DetectPipeline<u8>::process_slice (workers={res['threads']}) on the "
+                                   f"first {len(recs)} packets of C2 slice 0 at v=2^20 with a report due; "
+                                   f"value = 1e8 / (1e8 / measured scan rate + measured report+slide time)"},
+        "e2e": {"value": value, "unit": "packets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- the engine
+
+def run_engine(args):
+    import numpy as np
+    import torch
+
+    from paper_1803_10369_b200 import srla
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = srla.SeaConfig(**sketch_cfg(args.cols))
+    n_per_gpu = args.packets
+    spec = trace_spec(n_per_gpu * world)
+    gen = srla.DeviceTraceGenerator(srla.PlantSpec(**spec), device=local)
+
+    # stage the trace in HBM: one owned slice per generator slice
+    nres = min(spec["slices"], args.resident)
+    slices = []
+    for s in range(nres):
+        full = gen.slice_tensor(s)
+        if world > 1:
+            own = torch.empty_like(full)
+            m = srla.partition_records(full.data_ptr(), full.shape[0], cfg.seed, world, rank, own.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream)
+            slices.append(own[:m].clone())
+            del own
+        else:
+            slices.append(full)
+        del full
+    torch.cuda.synchronize()
+
+    eng = srla.EstimatorArray(cfg, device=local)
+    st = torch.cuda.ExternalStream(eng.stream_handle())
+    rep_cap = 1 << 22
+    rep_buf = np.empty(rep_cap, srla.ENTRY_DTYPE)
+
+    def allgather_report(entries):
+        if world == 1:
+            return entries
+        n = torch.tensor([len(entries)], device="cuda")
+        counts = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(counts, n)
+        mx = int(max(c.item() for c in counts))
+        pad = np.zeros(mx, srla.ENTRY_DTYPE)
+        pad[: len(entries)] = entries
+        t = torch.from_numpy(pad.view(np.uint8)).cuda()
+        outs = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(outs, t)
+        merged = np.concatenate([o.cpu().numpy().view(srla.ENTRY_DTYPE)[: int(c.item())] for o, c in zip(outs, counts)])
+        return merged[np.argsort(merged["host"], kind="stable")]
+
+    def step(sid, host=None):
+        recs = host[sid % len(host)] if host is not None else slices[sid % nres]
+        if host is not None:
+            eng.scan(recs)
+        else:
+            eng.scan(recs)
+        n, nr = _end_slice(eng, sid, rep_buf)
+        return allgather_report(rep_buf[:n]), n
+
+    import ctypes as C
+
+    def _end_slice(e, sid, buf):
+        n, nr = C.c_uint64(), C.c_uint64()
+        srla._check(srla._lib.srla_end_slice(e._h, sid, 1, C.c_void_p(buf.ctypes.data), len(buf), C.byref(n),
+                                             C.byref(nr)))
+        return n.value, nr.value
+
+    sid = 0
+    prefill = max(0, cfg.window - 1 - args.warmup)
+    for _ in range(prefill + args.warmup):
+        step(sid)
+        sid += 1
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    eng.synchronize()
+
+    eng.timing_reset()
+    st0 = eng.stats()
+    clocks = Clocks(local)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(st)
+    eos_dev, eos_wall, entries = [], [], []
+    for _ in range(args.steps):
+        _, n = step(sid)
+        tm = eng.timing()
+        eos_dev.append(tm["last_end_slice_device_ms"])
+        eos_wall.append(tm["last_end_slice_wall_ms"])
+        entries.append(n)
+        sid += 1
+    t_end.record(st)
+    t_end.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    tm = eng.timing()
+    st1 = eng.stats()
+    pk = torch.tensor([float(st1["packets"] - st0["packets"]), ms], dtype=torch.float64, device="cuda")
+    if dist:
+        tot = pk[:1].clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        mx = pk[1:].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        packets, ms = tot.item(), mx.item()
+    else:
+        packets = pk[0].item()
+    value = packets / (ms / 1e3)
+
+    # dominant kernel: K1 scan, CUDA events on the engine stream around each launch
+    launches = max(1, tm["scan_kernel_launches"])
+    recs_per_launch = tm["scan_kernel_records"] / launches
+    ms_per_launch = tm["scan_kernel_ms"] / launches
+    achieved = recs_per_launch * ALGO_BYTES_PER_PACKET / (ms_per_launch * 1e-3) / 1e9
+    peak, peak_src = measured_peaks()
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "scan_ncu_summary.json")
+    if os.path.exists(prof):
+        d = json.load(open(prof))
+        if d.get("dram_bytes_per_record"):
+            traffic = d["dram_bytes_per_record"] * recs_per_launch
+
+    # end to end through the public API with host buffers (pinned), H2D inside
+    e2e = None
+    if not args.no_e2e:
+        nh = min(2, nres)
+        host = [slices[i].cpu().pin_memory().numpy().view(np.uint32) for i in range(nh)]
+        h2d = sum(h.nbytes for h in host) / nh
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        d2h = 0
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            _, n = step(sid, host=host)
+            d2h += n * srla.ENTRY_DTYPE.itemsize
+            sid += 1
+        eng.synchronize()
+        if dist:
+            dist.barrier()
+        el = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = t.item()
+        e2e = {"value": packets / el, "unit": "packets/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h / args.steps)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        recs = sample_records(args.cpu_sample, local)
+        threads = os.cpu_count() or 1
+        r = cpu_reference(recs, args.cols, threads, slice_id=9)
+        ms_full = n_per_gpu / r["scan_rate"] * 1e3 + r["eos_ms"]
+        cpu = {"value": n_per_gpu / (ms_full / 1e3), "unit": "packets/s", "cores": r["threads"], "kind": r["kind"],
+               "sample": f"DetectPipeline<u8>::process_slice (workers={r['threads']}) on the first {len(recs)} "
+                         f"packets of C2 slice 0 at v=2^20 with a report due: scan {r['scan_rate']:.4g} pkt/s, "
+                         f"report+slide {r['eos_ms']:.1f} ms; value = 1e8/(1e8/scan rate + report+slide)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "packets/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference generator C2 spec, device port)",
+            "config": {"workload": "C2: u=4 v=2^20 g=8 g'=1024 z=4 k=10 theta=1024 seed=0x5EA00001; "
+                                   "trace seed 1, 4M uniform sources, Zipf(1.0) 4M destinations, 50 plants",
+                       "packets_per_slice_per_gpu": n_per_gpu, "resident_slices": nres,
+                       "l2": "inputs larger than L2 (1.2 GB per slice); no flush",
+                       "parallelism": f"owner-partitioned x{world}" if world > 1 else "1 GPU"},
+            "end_of_slice_ms": {"device_median": statistics.median(eos_dev), "device_p99": max(eos_dev),
+                                "wall_median": statistics.median(eos_wall), "report_entries_median":
+                                    statistics.median(entries)},
+            "roofline": {"bound": "hbm", "kernel": "k_scan", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_packet": ALGO_BYTES_PER_PACKET,
+                         "packets_per_launch": recs_per_launch, "ms_per_launch": ms_per_launch,
+                         "share_of_step": tm["scan_kernel_ms"] / ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
+            "library_launches": int(st1["library_launches"] - st0["library_launches"]),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--packets", type=int, default=100_000_000, help="packets per slice per GPU")
+    ap.add_argument("--cols", type=int, default=1 << 20)
+    ap.add_argument("--resident", type=int, default=12, help="distinct slices staged in HBM")
+    ap.add_argument("--cpu-sample", type=int, default=20_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_engine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,231 @@
+/*
+ * srla.h — C ABI of the B200-native SRLA engine (libsrla_b200.so).
+ *
+ * The reference (`sspread`, /root/reference/proj/include/sspread) is a
+ * header-only C++ library with no FFI; its hot path is the EstimatorArray /
+ * DetectPipeline API. Every entry point below replaces one reference call (the
+ * cite is on each declaration) and is what the drop-in headers in
+ * include/sspread/*.hpp bind. Plain pointers and sizes only; no CUDA or torch
+ * types cross this boundary. One CUDA stream per engine; an engine is not
+ * re-entrant (the drop-in wrapper serialises calls, matching the reference's
+ * "exclusive access outside the scan phase" contract, sea.hpp:108-112).
+ *
+ * Error convention: every call returns an srla_status. The message of the
+ * last failure on the calling thread is srla_last_error(). The C++ wrapper maps
+ * SRLA_E_INVALID to std::invalid_argument and SRLA_E_RANGE to
+ * std::out_of_range, as the reference throws them (sea.hpp:44-51,125-126,
+ * 249,341-346; recorders.hpp:35-53).
+ */
+#ifndef SRLA_H
+#define SRLA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum srla_status {
+    SRLA_OK = 0,
+    SRLA_E_INVALID = 1,  /* bad argument / configuration (std::invalid_argument) */
+    SRLA_E_RANGE = 2,    /* row index out of range (std::out_of_range) */
+    SRLA_E_CAPACITY = 3, /* output buffer too small; *n_out holds the size needed */
+    SRLA_E_CUDA = 4,     /* CUDA runtime / device failure */
+    SRLA_E_INTERNAL = 5
+} srla_status;
+
+/* sspread::SeaConfig (sea.hpp:33-52), field for field. */
+typedef struct srla_config {
+    uint32_t rows;          /* u: estimator rows, <= 64 (sea.hpp:125-126,349) */
+    uint32_t cols;          /* v: estimators per row */
+    uint32_t rough_slots;   /* g */
+    uint32_t linear_slots;  /* g' */
+    uint32_t recorder_bits; /* z: 1..32; storage word 1/2/4 B (recorders.hpp:64-66) */
+    uint32_t window;        /* k: 1..2^z-1 */
+    uint32_t theta;
+    uint32_t reserved;      /* must be 0 */
+    double fill_ratio;      /* kSuperTestRatio by default (estimators.hpp:19) */
+    uint64_t seed;
+} srla_config;
+
+/* sspread::TraceRecord (trace.hpp:20-26): 12 bytes, host byte order. */
+typedef struct srla_record {
+    uint32_t ts;
+    uint32_t src; /* aip: the monitored-side host */
+    uint32_t dst; /* bip: the opposite host */
+} srla_record;
+
+/* sspread::WindowEntry (sea.hpp:88-93). has_estimate == 0 is the reference's
+ * empty std::optional ("saturated"). */
+typedef struct srla_entry {
+    uint32_t host;
+    uint32_t union_weight;
+    double estimate;
+    uint8_t has_estimate;
+    uint8_t is_super;
+    uint8_t reserved[6];
+} srla_entry;
+
+/* Row kinds for export/import (the raw spans of sea.hpp:341-346). */
+enum { SRLA_INDICATOR = 0, SRLA_ROUGH = 1, SRLA_LINEAR = 2 };
+
+typedef struct srla_engine srla_engine;
+
+typedef struct srla_stats {
+    uint64_t packets;         /* records scanned since create */
+    uint64_t sampled_events;  /* rough-estimator updates (1 in 2^tau) */
+    uint64_t crossings;       /* sampled updates that passed the rho*g test */
+    uint64_t first_crossings; /* distinct hosts crossing, per chunk, summed */
+    uint64_t flagged;         /* hosts needing ordered SI resolution */
+    uint64_t pushed;          /* candidate-sink pushes */
+    uint64_t kernel_launches; /* launches of this library's own kernels */
+    uint64_t library_launches;/* CUB sort/scan/select launches (approximate) */
+    uint64_t chunks;
+    uint64_t slides;
+} srla_stats;
+
+/* Last failure message on this thread ("" if none). */
+const char* srla_last_error(void);
+/* Library version / build string ("srla_b200 <ver> sm_100a"). */
+const char* srla_version(void);
+
+/* EstimatorArray<W>::EstimatorArray (sea.hpp:116-135): validates, allocates
+ * u*v*(g+g')*W + u*v*2 bytes of HBM on `device`, all recorders expired. */
+srla_status srla_create(const srla_config* cfg, int device, srla_engine** out);
+srla_status srla_destroy(srla_engine* e);
+
+/* params().tau, weight_threshold(), storage word bytes (sea.hpp:140-141). */
+srla_status srla_params(const srla_engine* e, uint32_t* tau, uint32_t* threshold,
+                        uint32_t* word_bytes);
+/* EstimatorArray::column_of (sea.hpp:143-145); host-side hash. */
+srla_status srla_column_of(const srla_engine* e, uint32_t row, uint32_t aip, uint32_t* col);
+
+/* Scan records in order: EstimatorArray::scan_ip_pair applied to each record
+ * (sea.hpp:150-196), as DetectPipeline::scan_records does with one worker
+ * (pipeline.hpp:134-139). `recs` is host memory (on_device = 0) or device
+ * memory on the engine's GPU (on_device = 1). May be called repeatedly within
+ * a slice. Hosts the reference would push to its candidate sink are appended,
+ * in push order, to the engine's candidate list (deduplicated, like
+ * CandidateList::insert, sea.hpp:58-62) and, if `pushed` != NULL, copied out
+ * (up to `cap`; *n_pushed always receives the true count). */
+srla_status srla_scan_batch(srla_engine* e, const srla_record* recs, uint64_t n, int on_device,
+                            uint32_t* pushed, uint64_t cap, uint64_t* n_pushed);
+
+/* The engine-owned candidate list (DetectPipeline::candidates, pipeline.hpp:131),
+ * insertion order. */
+srla_status srla_candidates(srla_engine* e, uint32_t* out, uint64_t cap, uint64_t* n);
+/* Replace it (the CandidateList argument of report_window / slide);
+ * duplicates are dropped keeping first occurrences. */
+srla_status srla_set_candidates(srla_engine* e, const uint32_t* hosts, uint64_t n);
+
+/* EstimatorArray::report_window over the engine's candidate list
+ * (sea.hpp:288-309): entries sorted by host, union_linear_weight, Eq. 9
+ * estimate (host LUT of corrected_estimate_from, sea.hpp:270-279), theta cut.
+ * *fill_product receives union_fill_product() (sea.hpp:261-265). */
+srla_status srla_report(srla_engine* e, srla_entry* out, uint64_t cap, uint64_t* n_out,
+                        double* fill_product);
+
+/* EstimatorArray::slide over the engine's candidate list (sea.hpp:316-338);
+ * the list becomes the retained list. */
+srla_status srla_slide(srla_engine* e, uint64_t* n_retained);
+
+/* DetectPipeline::process_slice after the scan (pipeline.hpp:119-128): report
+ * if want_report and slice_id + 1 >= window, then slide. *n_out = 0 when no
+ * report is due. */
+srla_status srla_end_slice(srla_engine* e, uint64_t slice_id, int want_report, srla_entry* out,
+                           uint64_t cap, uint64_t* n_out, uint64_t* n_retained);
+
+/* union_rough_weight / union_linear_weight (sea.hpp:219-243) per host; either
+ * output may be NULL. */
+srla_status srla_union_weights(srla_engine* e, const uint32_t* hosts, uint64_t n,
+                               uint32_t* rough_w, uint32_t* linear_w);
+/* union_view (sea.hpp:199-217); linear may be NULL (include_linear = false).
+ * rough / linear receive g / g' words widened to uint32. */
+srla_status srla_union_view(srla_engine* e, uint32_t aip, uint16_t* indicator, uint32_t* rough,
+                            uint32_t* linear);
+/* count_active over each linear row (the numerators of row_fill_fraction,
+ * sea.hpp:248-257); `counts` has `rows` entries. */
+srla_status srla_row_active(srla_engine* e, uint64_t* counts);
+/* corrected_estimate_from (sea.hpp:270-279), host arithmetic, bit-identical. */
+srla_status srla_estimate_from(const srla_engine* e, uint32_t weight, double fill_product,
+                               double* estimate, int* has_estimate);
+
+/* Raw rows (indicator_row / rough_row / linear_row, sea.hpp:341-346) as
+ * little-endian W-byte words (u16 for the indicator). `bytes` must equal the
+ * row size. */
+srla_status srla_row_bytes(const srla_engine* e, int kind, uint64_t* bytes);
+srla_status srla_export_row(srla_engine* e, uint32_t row, int kind, void* buf, uint64_t bytes);
+srla_status srla_import_row(srla_engine* e, uint32_t row, int kind, const void* buf,
+                            uint64_t bytes);
+
+srla_status srla_stats_get(const srla_engine* e, srla_stats* out);
+
+/* Device time of the dominant kernel (K1 scan, CUDA events on the engine
+ * stream around each launch) and of end-of-slice (report + slide: device
+ * events, and host wall time including the report hand-off). */
+typedef struct srla_timing {
+    double scan_kernel_ms;
+    uint64_t scan_kernel_launches;
+    uint64_t scan_kernel_records;
+    double end_slice_device_ms;
+    double end_slice_wall_ms;
+    double last_end_slice_device_ms;
+    double last_end_slice_wall_ms;
+    uint64_t end_slices;
+} srla_timing;
+srla_status srla_timing_get(const srla_engine* e, srla_timing* out);
+srla_status srla_timing_reset(srla_engine* e);
+srla_status srla_synchronize(srla_engine* e);
+/* The engine's cudaStream_t (as void*), for callers that time on it. */
+srla_status srla_stream(srla_engine* e, void** stream);
+
+/* Synthetic trace on the device: generate_trace (generator.hpp:117-161),
+ * byte-identical to the reference, one slice at a time. `out` is device
+ * memory with room for *n_out records (query with out = NULL). Valid for
+ * slice_seconds == 1 (no in-slice reordering); other specs return
+ * SRLA_E_INVALID. */
+typedef struct srla_plant {
+    uint32_t host;
+    uint32_t cardinality;
+    uint32_t first_slice;
+    uint32_t last_slice;
+} srla_plant;
+
+typedef struct srla_trace_spec {
+    uint64_t seed;
+    uint32_t start_ts;
+    uint32_t slice_seconds;
+    uint32_t slices;
+    uint32_t window;
+    uint32_t a_base;
+    uint32_t b_base;
+    uint32_t a_hosts;
+    uint32_t b_hosts;
+    uint32_t pairs_per_slice;
+    uint32_t n_plants;
+    double skew;
+    const srla_plant* plants;
+} srla_trace_spec;
+
+typedef struct srla_generator srla_generator;
+srla_status srla_generator_create(const srla_trace_spec* spec, int device, srla_generator** out);
+srla_status srla_generator_destroy(srla_generator* g);
+/* Records in slice `slice` (0-based); out = NULL just reports the count. */
+srla_status srla_generate_slice(srla_generator* g, uint64_t slice, srla_record* out_device,
+                                uint64_t cap, uint64_t* n_out, void* stream);
+
+/* Multi-GPU ingest: keep the records (device memory) whose monitored host is
+ * owned by shard `part` of `nparts`, in their original order. Ownership is
+ * HashFamily(seed).reduce(3, src, nparts) — function index 3 is unused by the
+ * reference (hash.hpp:70-73), so shards are independent of every sketch hash.
+ * *n_out receives the kept count; d_out has room for n records. */
+srla_status srla_partition_records(const srla_record* d_in, uint64_t n, uint64_t seed, uint32_t nparts,
+                                   uint32_t part, srla_record* d_out, uint64_t* n_out, void* stream);
+/* Host-side owner of one address (same function). */
+uint32_t srla_owner_of(uint64_t seed, uint32_t aip, uint32_t nparts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRLA_H */

@@ -268,7 +268,7 @@ class Sketch:
         n = len(csip)
         out = _report_buffers(n)
         self.chk.f("report")(self.h, _ptr(csip), n, *(_ptr(out[k]) for k in _REPORT_KEYS))
-        return out
+        return {k: v[:n] for k, v in out.items()}
 
     def slide(self, csip) -> np.ndarray:
         csip = np.ascontiguousarray(csip, dtype=np.uint32)

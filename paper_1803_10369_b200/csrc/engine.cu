@@ -1,0 +1,979 @@
+// engine.cu — the SRLA engine behind the C ABI (include/srla.h).
+//
+// One engine = one EstimatorArray's state resident in HBM plus the
+// DetectPipeline's candidate list, driven on one CUDA stream. The scan is
+// processed in chunks; each chunk runs K1 scan -> K2 crossing -> K5 rough
+// commit -> K3 first crossings -> K4 ordered indicator resolution, which
+// reproduces the reference's record-order semantics exactly (kernels.cuh).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "host_math.h"
+#include "kernels.cuh"
+#include "srla.h"
+
+namespace srla {
+
+struct Error : std::runtime_error {
+    srla_status code;
+    Error(srla_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                                 \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess)                                                                \
+            throw ::srla::Error(SRLA_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        if (p) CK(cudaFree(p));
+        p = nullptr;
+        const size_t c = std::max<size_t>({n, cap + cap / 2, 256});
+        CK(cudaMalloc(&p, c * sizeof(T)));
+        cap = c;
+    }
+    // grow keeping the first `keep` elements (stream-ordered copy)
+    void ensure_keep(size_t n, size_t keep, cudaStream_t st) {
+        if (n <= cap) return;
+        const size_t c = std::max<size_t>({n, cap * 2, 256});
+        T* q = nullptr;
+        CK(cudaMalloc(&q, c * sizeof(T)));
+        if (keep) CK(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        if (p) CK(cudaFree(p));
+        p = q;
+        cap = c;
+    }
+};
+
+template <typename T>
+struct PinBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    PinBuf() = default;
+    PinBuf(const PinBuf&) = delete;
+    ~PinBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        if (p) CK(cudaFreeHost(p));
+        p = nullptr;
+        const size_t c = std::max<size_t>({n, cap + cap / 2, 256});
+        CK(cudaMallocHost(&p, c * sizeof(T)));
+        cap = c;
+    }
+};
+
+struct Engine {
+    srla_config cfg{};
+    int device = 0;
+    cudaStream_t st = nullptr;
+    DevCfg dc{};
+    uint32_t tau = 0, thr = 0, wb = 1;
+    uint64_t lin_words = 0, rough_words = 0;  // per row
+    void* d_lin = nullptr;
+    void* d_rough = nullptr;
+    uint16_t* d_si = nullptr;
+    uint32_t* d_stamp = nullptr;
+    int sms = 148;
+
+    static constexpr uint32_t kChunk = 1u << 26;      // records per ordered chunk
+    static constexpr uint32_t kHostStage = 1u << 24;  // records per host->device hop
+
+    DevBuf<uint32_t> ev;
+    uint32_t ev_cap = 0;
+    DevBuf<uint32_t> ctr;  // device counters
+    PinBuf<uint32_t> pin_ctr;
+    DevBuf<uint64_t> xkeys, xsorted, hp, hps, fmask, tkey, skey;
+    DevBuf<uint32_t> cnt, off, hosts, tval, sval, towner, posof, flagged, pushed, newhosts;
+    DevBuf<uint8_t> status, definite, fl_und, fl_ins, isnew, keep, temp;
+    DevBuf<uint32_t> csip, csip2, qhosts, sorted_hosts, weights, rweights;
+    uint64_t ncsip = 0;
+    DevBuf<unsigned long long> cset;
+    uint64_t cset_cap = 0;
+    DevBuf<unsigned long long> d_counts;
+    DevBuf<uint32_t> dstage[2];
+    PinBuf<uint32_t> pstage[2], pin_hosts, pin_w;
+    cudaStream_t cs = nullptr;  // host->device copy stream
+    cudaEvent_t ev_copied[2] = {}, ev_scanned[2] = {};
+    cudaEvent_t t_scan0 = nullptr, t_scan1 = nullptr, t_eos0 = nullptr, t_eos1 = nullptr;
+    srla_timing timing{};
+    PinBuf<unsigned long long> pin_counts;
+    std::vector<uint32_t> host_pushed;
+    bool collect_pushed = false;
+    srla_stats stats{};
+
+    // ------------------------------------------------------------ lifecycle
+    explicit Engine(const srla_config& c, int dev) : cfg(c), device(dev) {
+        validate();
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev_scanned[b], cudaEventDisableTiming));
+            CK(cudaEventRecord(ev_copied[b], cs));
+            CK(cudaEventRecord(ev_scanned[b], st));
+        }
+        CK(cudaEventCreate(&t_scan0));
+        CK(cudaEventCreate(&t_scan1));
+        CK(cudaEventCreate(&t_eos0));
+        CK(cudaEventCreate(&t_eos1));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        const uint32_t bits = cfg.recorder_bits;
+        wb = bits <= 8 ? 1 : bits <= 16 ? 2 : 4;
+        tau = srla_host::sampling_exponent(cfg.theta, cfg.rough_slots);
+        thr = srla_host::super_weight_threshold(cfg.fill_ratio, cfg.rough_slots);
+        dc.rows = cfg.rows;
+        dc.cols = cfg.cols;
+        dc.g = cfg.rough_slots;
+        dc.gl = cfg.linear_slots;
+        dc.k = cfg.window;
+        dc.expired = bits == 32 ? 0xFFFFFFFFu : (1u << bits) - 1u;
+        dc.tau_mask = tau >= 32 ? 0xFFFFFFFFu : (1u << tau) - 1u;
+        dc.thr = thr;
+        dc.gl_mask = (cfg.linear_slots & (cfg.linear_slots - 1)) == 0 ? cfg.linear_slots - 1 : 0;
+        dc.wbytes = wb;
+        dc.sub_sample = sub_key(cfg.seed, kSampleHash);
+        dc.sub_rslot = sub_key(cfg.seed, kRoughSlotHash);
+        dc.sub_ind = sub_key(cfg.seed, kIndicatorHash);
+        for (uint32_t i = 0; i < kMaxRows; ++i) dc.sub_row[i] = sub_key(cfg.seed, kRowHashBase + i);
+        lin_words = static_cast<uint64_t>(cfg.cols) * cfg.linear_slots;
+        rough_words = static_cast<uint64_t>(cfg.cols) * cfg.rough_slots;
+        const uint64_t rows = cfg.rows;
+        CK(cudaMalloc(&d_lin, rows * lin_words * wb));
+        CK(cudaMalloc(&d_rough, rows * rough_words * wb));
+        CK(cudaMalloc(&d_si, rows * cfg.cols * sizeof(uint16_t)));
+        CK(cudaMalloc(&d_stamp, rows * rough_words * sizeof(uint32_t)));
+        fill_expired(d_lin, rows * lin_words);
+        fill_expired(d_rough, rows * rough_words);
+        CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st));
+        CK(cudaMemsetAsync(d_stamp, 0xFF, rows * rough_words * sizeof(uint32_t), st));
+        ctr.ensure(16);
+        pin_ctr.ensure(16);
+        rebuild_cset(1024);
+        CK(cudaStreamSynchronize(st));
+    }
+
+    ~Engine() {
+        if (st) cudaStreamSynchronize(st);
+        if (d_lin) cudaFree(d_lin);
+        if (d_rough) cudaFree(d_rough);
+        if (d_si) cudaFree(d_si);
+        if (d_stamp) cudaFree(d_stamp);
+        if (cs) cudaStreamSynchronize(cs);
+        for (int b = 0; b < 2; ++b) {
+            if (ev_copied[b]) cudaEventDestroy(ev_copied[b]);
+            if (ev_scanned[b]) cudaEventDestroy(ev_scanned[b]);
+        }
+        for (cudaEvent_t e : {t_scan0, t_scan1, t_eos0, t_eos1})
+            if (e) cudaEventDestroy(e);
+        if (cs) cudaStreamDestroy(cs);
+        if (st) cudaStreamDestroy(st);
+    }
+
+    // SeaConfig::validate (sea.hpp:44-51), RecorderModel (recorders.hpp:33-54),
+    // EstimatorArray ctor (sea.hpp:122-126).
+    void validate() const {
+        auto bad = [](const char* m) { throw Error(SRLA_E_INVALID, m); };
+        if (cfg.rows < 1) bad("rows must be >= 1");
+        if (cfg.cols < 1) bad("cols must be >= 1");
+        if (cfg.rough_slots < 1) bad("rough_slots must be >= 1");
+        if (cfg.linear_slots < 2) bad("linear_slots must be >= 2");
+        if (cfg.theta < 1) bad("theta must be >= 1");
+        if (cfg.recorder_bits < 1 || cfg.recorder_bits > 32)
+            throw Error(SRLA_E_INVALID, "recorder width must be in [1, 32] bits, got " +
+                                            std::to_string(cfg.recorder_bits));
+        const uint32_t e = cfg.recorder_bits == 32 ? 0xFFFFFFFFu : (1u << cfg.recorder_bits) - 1u;
+        if (cfg.window < 1 || cfg.window > e)
+            throw Error(SRLA_E_INVALID, "window of " + std::to_string(cfg.window) +
+                                            " slices does not fit a " +
+                                            std::to_string(cfg.recorder_bits) +
+                                            "-bit recorder (valid range [1, " + std::to_string(e) + "])");
+        if (cfg.rows > kMaxRows) bad("at most 64 rows supported");
+        if (cfg.reserved != 0) bad("srla_config.reserved must be 0");
+    }
+
+    uint32_t blocks(uint64_t work, uint32_t per = 256, uint32_t waves = 8) const {
+        const uint64_t b = (work + per - 1) / per;
+        return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(b, uint64_t(sms) * waves)));
+    }
+
+    void launched(uint64_t n = 1) { stats.kernel_launches += n; }
+    void lib_launched(uint64_t n = 1) { stats.library_launches += n; }
+    void check_launch() { CK(cudaGetLastError()); }
+
+    template <typename Fn>
+    void with_w(Fn&& fn) {
+        switch (wb) {
+            case 1: fn(uint8_t{}); break;
+            case 2: fn(uint16_t{}); break;
+            default: fn(uint32_t{}); break;
+        }
+    }
+
+    void fill_expired(void* t, uint64_t words) {
+        with_w([&](auto w) {
+            using W = decltype(w);
+            k_fill<W><<<blocks(words, 256, 16), 256, 0, st>>>(static_cast<W*>(t), words, static_cast<W>(dc.expired));
+        });
+        check_launch();
+        launched();
+    }
+
+    uint32_t read_ctr(uint32_t idx) {
+        CK(cudaMemcpyAsync(pin_ctr.p + idx, ctr.p + idx, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return pin_ctr.p[idx];
+    }
+
+    // ------------------------------------------------------------ CUB helpers
+    template <typename Fn>
+    void cub_call(Fn&& fn) {
+        size_t bytes = 0;
+        CK(fn(static_cast<void*>(nullptr), bytes));
+        temp.ensure(bytes + 16);
+        CK(fn(static_cast<void*>(temp.p), bytes));
+        lib_launched();
+    }
+
+    static int bit_length(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 1; }
+
+    // ------------------------------------------------------------ candidate set
+    void rebuild_cset(uint64_t want) {
+        uint64_t cap = 1024;
+        while (cap < 2 * want) cap <<= 1;
+        if (cap != cset_cap) {
+            cset.ensure(cap);
+            cset_cap = cap;
+        }
+        CK(cudaMemsetAsync(cset.p, 0, cset_cap * sizeof(unsigned long long), st));
+        if (ncsip) {
+            k_cset_insert<<<blocks(ncsip), 256, 0, st>>>(csip.p, static_cast<uint32_t>(ncsip), cset.p, cset_cap - 1);
+            check_launch();
+            launched();
+        }
+    }
+
+    // Append hosts (distinct, in order) to the candidate list unless present.
+    void append_candidates(const uint32_t* d_hosts, uint32_t n) {
+        if (!n) return;
+        isnew.ensure(n);
+        newhosts.ensure(n);
+        k_cset_lookup<<<blocks(n), 256, 0, st>>>(d_hosts, n, cset.p, cset_cap - 1, isnew.p);
+        check_launch();
+        launched();
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceSelect::Flagged(t, b, d_hosts, isnew.p, newhosts.p, ctr.p + 7, static_cast<int>(n), st);
+        });
+        const uint32_t nn = read_ctr(7);
+        if (!nn) return;
+        csip.ensure_keep(ncsip + nn, ncsip, st);
+        CK(cudaMemcpyAsync(csip.p + ncsip, newhosts.p, nn * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        ncsip += nn;
+        if (2 * ncsip > cset_cap) {
+            rebuild_cset(ncsip);
+        } else {
+            k_cset_insert<<<blocks(nn), 256, 0, st>>>(newhosts.p, nn, cset.p, cset_cap - 1);
+            check_launch();
+            launched();
+        }
+    }
+
+    // ------------------------------------------------------------ scan
+    template <typename W, int MAXR>
+    void scan_chunk_t(const uint32_t* d_recs, uint32_t n) {
+        W* lin = static_cast<W*>(d_lin);
+        W* rough = static_cast<W*>(d_rough);
+        const int vec = (reinterpret_cast<uintptr_t>(d_recs) & 15) == 0;
+        if (!ev_cap) {
+            ev_cap = static_cast<uint32_t>(std::min<uint64_t>(kChunk, (uint64_t(kChunk) >> tau) + (uint64_t(kChunk) >> (tau + 3)) + 65536));
+            ev.ensure(3ull * ev_cap);
+        }
+        uint32_t n_ev = 0;
+        for (;;) {
+            CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
+            CK(cudaEventRecord(t_scan0, st));
+            k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+            check_launch();
+            launched();
+            CK(cudaEventRecord(t_scan1, st));
+            n_ev = read_ctr(0);
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, t_scan0, t_scan1));
+            timing.scan_kernel_ms += ms;
+            timing.scan_kernel_launches += 1;
+            timing.scan_kernel_records += n;
+            if (n_ev <= ev_cap) break;
+            // capacity overflow: marks and stamps are idempotent, rerun with room
+            ev_cap = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(n_ev) * 5 / 4 + 4096, 0xFFFFFFF0ull));
+            ev.ensure(3ull * ev_cap);
+        }
+        stats.sampled_events += n_ev;
+        if (!n_ev) return;
+
+        xkeys.ensure(n_ev);
+        k_cross<W, MAXR><<<blocks(n_ev), 256, 0, st>>>(ev.p, ev_cap, n_ev, dc, rough, d_stamp, xkeys.p, ctr.p + 1);
+        check_launch();
+        launched();
+        k_commit<W, MAXR><<<blocks(n_ev), 256, 0, st>>>(ev.p, ev_cap, n_ev, dc, rough, d_stamp);
+        check_launch();
+        launched();
+        const uint32_t X = read_ctr(1);
+        stats.crossings += X;
+        if (!X) return;
+
+        // K3: first crossing per host, then order hosts by P
+        xsorted.ensure(X);
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, xkeys.p, xsorted.p, static_cast<int>(X), 0, 64, st);
+        });
+        hp.ensure(X);
+        k_first<<<blocks(X), 256, 0, st>>>(xsorted.p, X, hp.p, ctr.p + 2);
+        check_launch();
+        launched();
+        const uint32_t Hn = read_ctr(2);
+        stats.first_crossings += Hn;
+        hps.ensure(Hn);
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, hp.p, hps.p, static_cast<int>(Hn), 0, 64, st);
+        });
+
+        // K4: ordered indicator resolution
+        fmask.ensure(Hn);
+        cnt.ensure(Hn);
+        off.ensure(Hn);
+        hosts.ensure(Hn);
+        status.ensure(Hn);
+        definite.ensure(Hn);
+        fl_und.ensure(Hn);
+        fl_ins.ensure(Hn);
+        k_si_check<<<blocks(Hn), 256, 0, st>>>(hps.p, Hn, dc, d_si, fmask.p, cnt.p, hosts.p, status.p);
+        check_launch();
+        launched();
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceScan::ExclusiveSum(t, b, cnt.p, off.p, static_cast<int>(Hn), st);
+        });
+        CK(cudaMemcpyAsync(pin_ctr.p + 8, off.p + (Hn - 1), 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(pin_ctr.p + 9, cnt.p + (Hn - 1), 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const uint32_t T = pin_ctr.p[8] + pin_ctr.p[9];
+        CK(cudaMemsetAsync(definite.p, 0, Hn, st));
+        if (T) {
+            tkey.ensure(T);
+            skey.ensure(T);
+            tval.ensure(T);
+            sval.ensure(T);
+            towner.ensure(T);
+            posof.ensure(T);
+            k_tuples<<<blocks(Hn), 256, 0, st>>>(hosts.p, Hn, dc, fmask.p, off.p, tkey.p, tval.p, towner.p);
+            check_launch();
+            launched();
+            const int end_bit = bit_length(uint64_t(cfg.rows) * cfg.cols * kIndicatorBits - 1);
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceRadixSort::SortPairs(t, b, tkey.p, skey.p, tval.p, sval.p, static_cast<int>(T), 0, end_bit, st);
+            });
+            k_first_key<<<blocks(T), 256, 0, st>>>(skey.p, sval.p, T, towner.p, definite.p, posof.p);
+            check_launch();
+            launched();
+        }
+        k_classify<<<blocks(Hn), 256, 0, st>>>(Hn, status.p, definite.p, fl_und.p, fl_ins.p);
+        check_launch();
+        launched();
+        flagged.ensure(Hn);
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceSelect::Flagged(t, b, thrust::counting_iterator<uint32_t>(0), fl_und.p, flagged.p,
+                                              ctr.p + 3, static_cast<int>(Hn), st);
+        });
+        const uint32_t nf = read_ctr(3);
+        stats.flagged += nf;
+        if (nf) {
+            k_serial<<<1, 32, 0, st>>>(flagged.p, nf, fmask.p, off.p, posof.p, skey.p, sval.p, towner.p, status.p, fl_ins.p);
+            check_launch();
+            launched();
+        }
+        k_si_set<<<blocks(Hn), 256, 0, st>>>(hosts.p, Hn, status.p, dc, d_si);
+        check_launch();
+        launched();
+        pushed.ensure(Hn);
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceSelect::Flagged(t, b, hosts.p, fl_ins.p, pushed.p, ctr.p + 4, static_cast<int>(Hn), st);
+        });
+        const uint32_t np = read_ctr(4);
+        stats.pushed += np;
+        if (collect_pushed && np) {
+            const size_t at = host_pushed.size();
+            host_pushed.resize(at + np);
+            pin_hosts.ensure(np);
+            CK(cudaMemcpyAsync(pin_hosts.p, pushed.p, np * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            std::memcpy(host_pushed.data() + at, pin_hosts.p, np * sizeof(uint32_t));
+        }
+        append_candidates(pushed.p, np);
+    }
+
+    void scan_chunk(const uint32_t* d_recs, uint32_t n) {
+        if (!n) return;
+        stats.chunks++;
+        stats.packets += n;
+        with_w([&](auto w) {
+            using W = decltype(w);
+            if (cfg.rows <= 4) scan_chunk_t<W, 4>(d_recs, n);
+            else scan_chunk_t<W, 64>(d_recs, n);
+        });
+    }
+
+    void scan_batch(const srla_record* recs, uint64_t n, int on_device) {
+        if (!n) return;
+        if (on_device) {
+            const uint32_t* base = reinterpret_cast<const uint32_t*>(recs);
+            for (uint64_t o = 0; o < n; o += kChunk)
+                scan_chunk(base + 3 * o, static_cast<uint32_t>(std::min<uint64_t>(kChunk, n - o)));
+            return;
+        }
+        scan_host(reinterpret_cast<const uint32_t*>(recs), n);
+    }
+
+    // Host records: double-buffered H2D on a copy stream overlapping the scan
+    // of the previous chunk. Pinned caller memory is DMA'd directly; pageable
+    // memory is bounced through pinned staging.
+    void scan_host(const uint32_t* src, uint64_t n) {
+        cudaPointerAttributes attr{};
+        bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        const uint32_t step = static_cast<uint32_t>(std::min<uint64_t>(kHostStage, n));
+        const uint64_t nchunks = (n + step - 1) / step;
+        for (int b = 0; b < 2; ++b) {
+            dstage[b].ensure(3ull * step);
+            if (!pinned) pstage[b].ensure(3ull * step);
+        }
+        auto len = [&](uint64_t j) { return static_cast<uint32_t>(std::min<uint64_t>(step, n - j * step)); };
+        auto issue = [&](uint64_t j) {
+            const int b = static_cast<int>(j & 1);
+            const uint32_t* from = src + 3ull * j * step;
+            if (!pinned) {
+                CK(cudaEventSynchronize(ev_copied[b]));
+                std::memcpy(pstage[b].p, from, 12ull * len(j));
+                from = pstage[b].p;
+            }
+            CK(cudaStreamWaitEvent(cs, ev_scanned[b], 0));
+            CK(cudaMemcpyAsync(dstage[b].p, from, 12ull * len(j), cudaMemcpyHostToDevice, cs));
+            CK(cudaEventRecord(ev_copied[b], cs));
+        };
+        issue(0);
+        for (uint64_t j = 0; j < nchunks; ++j) {
+            if (j + 1 < nchunks) issue(j + 1);
+            const int b = static_cast<int>(j & 1);
+            CK(cudaStreamWaitEvent(st, ev_copied[b], 0));
+            scan_chunk(dstage[b].p, len(j));
+            CK(cudaEventRecord(ev_scanned[b], st));
+        }
+    }
+
+    // ------------------------------------------------------------ report
+    template <typename W, int MAXR>
+    void union_linear_t(const uint32_t* d_hosts, uint32_t n, uint32_t* d_out) {
+        k_union_linear<W, MAXR><<<blocks(uint64_t(n) * 32, 256, 16), 256, 0, st>>>(d_hosts, n, dc, static_cast<const W*>(d_lin), d_out);
+        check_launch();
+        launched();
+    }
+    void union_linear(const uint32_t* d_hosts, uint32_t n, uint32_t* d_out) {
+        if (!n) return;
+        with_w([&](auto w) {
+            using W = decltype(w);
+            if (cfg.rows <= 4) union_linear_t<W, 4>(d_hosts, n, d_out);
+            else union_linear_t<W, 64>(d_hosts, n, d_out);
+        });
+    }
+
+    void row_active_async() {
+        d_counts.ensure(cfg.rows);
+        CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
+        with_w([&](auto w) {
+            using W = decltype(w);
+            const uint64_t vecs = lin_words * sizeof(W) / 16 + 1;
+            dim3 grid(blocks(vecs, 256, std::max(1u, 16u / std::min(16u, cfg.rows))), cfg.rows);
+            k_row_active<W><<<grid, 256, 0, st>>>(static_cast<const W*>(d_lin), lin_words, cfg.window, d_counts.p);
+        });
+        check_launch();
+        launched();
+    }
+
+    void row_active(uint64_t* out) {
+        row_active_async();
+        pin_counts.ensure(cfg.rows);
+        CK(cudaMemcpyAsync(pin_counts.p, d_counts.p, cfg.rows * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (uint32_t i = 0; i < cfg.rows; ++i) out[i] = pin_counts.p[i];
+    }
+
+    // report_window (sea.hpp:288-309)
+    void report(std::vector<srla_entry>& out, double* fp_out) {
+        const uint32_t n = static_cast<uint32_t>(ncsip);
+        row_active_async();
+        if (n) {
+            sorted_hosts.ensure(n);
+            weights.ensure(n);
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceRadixSort::SortKeys(t, b, csip.p, sorted_hosts.p, static_cast<int>(n), 0, 32, st);
+            });
+            union_linear(sorted_hosts.p, n, weights.p);
+            pin_hosts.ensure(n);
+            pin_w.ensure(n);
+            CK(cudaMemcpyAsync(pin_hosts.p, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(pin_w.p, weights.p, n * 4ull, cudaMemcpyDeviceToHost, st));
+        }
+        pin_counts.ensure(cfg.rows);
+        CK(cudaMemcpyAsync(pin_counts.p, d_counts.p, cfg.rows * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<uint64_t> counts(pin_counts.p, pin_counts.p + cfg.rows);
+        const double fp = srla_host::fill_product(counts.data(), cfg.rows, lin_words);
+        if (fp_out) *fp_out = fp;
+        std::vector<double> est(cfg.linear_slots + 1);
+        std::vector<uint8_t> has(cfg.linear_slots + 1), sup(cfg.linear_slots + 1);
+        srla_host::estimate_lut(cfg.linear_slots, fp, cfg.theta, est.data(), has.data(), sup.data());
+        out.resize(n);
+        for (uint32_t e = 0; e < n; ++e) {
+            const uint32_t w = pin_w.p[e];
+            srla_entry& x = out[e];
+            x.host = pin_hosts.p[e];
+            x.union_weight = w;
+            x.estimate = est[w];
+            x.has_estimate = has[w];
+            x.is_super = sup[w];
+            std::memset(x.reserved, 0, sizeof(x.reserved));
+        }
+    }
+
+    // ------------------------------------------------------------ slide (sea.hpp:316-338)
+    template <typename W, int MAXR>
+    void slide_t() {
+        const uint64_t rows = cfg.rows;
+        CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st));
+        k_age<W><<<blocks(rows * rough_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_rough), rows * rough_words, dc.expired);
+        check_launch();
+        k_age<W><<<blocks(rows * lin_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_lin), rows * lin_words, dc.expired);
+        check_launch();
+        launched(2);
+        if (!ncsip) return;
+        const uint32_t n = static_cast<uint32_t>(ncsip);
+        keep.ensure(n);
+        csip2.ensure(n);
+        k_retain<W, MAXR><<<blocks(n), 256, 0, st>>>(csip.p, n, dc, static_cast<const W*>(d_rough), d_si, keep.p);
+        check_launch();
+        launched();
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceSelect::Flagged(t, b, csip.p, keep.p, csip2.p, ctr.p + 5, static_cast<int>(n), st);
+        });
+        ncsip = read_ctr(5);
+        std::swap(csip.p, csip2.p);
+        std::swap(csip.cap, csip2.cap);
+        rebuild_cset(ncsip);
+    }
+
+    void slide() {
+        stats.slides++;
+        with_w([&](auto w) {
+            using W = decltype(w);
+            if (cfg.rows <= 4) slide_t<W, 4>();
+            else slide_t<W, 64>();
+        });
+        CK(cudaStreamSynchronize(st));
+    }
+
+    // ------------------------------------------------------------ queries
+    void set_candidates(const uint32_t* h, uint64_t n) {
+        std::vector<uint32_t> uniq;
+        uniq.reserve(n);
+        std::unordered_set<uint32_t> seen;
+        for (uint64_t i = 0; i < n; ++i)
+            if (seen.insert(h[i]).second) uniq.push_back(h[i]);
+        ncsip = 0;
+        csip.ensure(std::max<size_t>(uniq.size(), 1));
+        if (!uniq.empty())
+            CK(cudaMemcpyAsync(csip.p, uniq.data(), uniq.size() * 4, cudaMemcpyHostToDevice, st));
+        ncsip = uniq.size();
+        rebuild_cset(ncsip);
+        CK(cudaStreamSynchronize(st));
+    }
+
+    void candidates(std::vector<uint32_t>& out) {
+        out.resize(ncsip);
+        if (ncsip) CK(cudaMemcpyAsync(out.data(), csip.p, ncsip * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+
+    void union_weights(const uint32_t* h, uint64_t n, uint32_t* rw, uint32_t* lw) {
+        if (!n) return;
+        const uint32_t m = static_cast<uint32_t>(n);
+        qhosts.ensure(m);
+        weights.ensure(m);
+        rweights.ensure(m);
+        CK(cudaMemcpyAsync(qhosts.p, h, n * 4, cudaMemcpyHostToDevice, st));
+        if (rw) {
+            with_w([&](auto w) {
+                using W = decltype(w);
+                if (cfg.rows <= 4)
+                    k_union_rough<W, 4><<<blocks(m), 256, 0, st>>>(qhosts.p, m, dc, static_cast<const W*>(d_rough), rweights.p);
+                else
+                    k_union_rough<W, 64><<<blocks(m), 256, 0, st>>>(qhosts.p, m, dc, static_cast<const W*>(d_rough), rweights.p);
+            });
+            check_launch();
+            launched();
+            CK(cudaMemcpyAsync(rw, rweights.p, n * 4, cudaMemcpyDeviceToHost, st));
+        }
+        if (lw) {
+            union_linear(qhosts.p, m, weights.p);
+            CK(cudaMemcpyAsync(lw, weights.p, n * 4, cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaStreamSynchronize(st));
+    }
+
+    uint32_t host_column(uint32_t row, uint32_t aip) const {
+        return static_cast<uint32_t>((static_cast<uint64_t>(hash_u32(dc.sub_row[row], aip)) * cfg.cols) >> 32);
+    }
+
+    uint32_t word_at(const std::vector<uint8_t>& b, uint64_t j) const {
+        uint32_t v = 0;
+        for (uint32_t q = 0; q < wb; ++q) v |= static_cast<uint32_t>(b[j * wb + q]) << (8 * q);
+        return v;
+    }
+
+    // union_view (sea.hpp:199-217)
+    void union_view(uint32_t aip, uint16_t* ind, uint32_t* rough, uint32_t* linear) {
+        uint16_t acc = 0xFFFF;
+        std::fill(rough, rough + cfg.rough_slots, 0u);
+        if (linear) std::fill(linear, linear + cfg.linear_slots, 0u);
+        std::vector<uint8_t> rb(uint64_t(cfg.rough_slots) * wb), lb(uint64_t(cfg.linear_slots) * wb);
+        for (uint32_t i = 0; i < cfg.rows; ++i) {
+            const uint64_t col = host_column(i, aip);
+            uint16_t s = 0;
+            CK(cudaMemcpyAsync(&s, d_si + uint64_t(i) * cfg.cols + col, 2, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(rb.data(), static_cast<uint8_t*>(d_rough) + (uint64_t(i) * rough_words + col * cfg.rough_slots) * wb, rb.size(), cudaMemcpyDeviceToHost, st));
+            if (linear)
+                CK(cudaMemcpyAsync(lb.data(), static_cast<uint8_t*>(d_lin) + (uint64_t(i) * lin_words + col * cfg.linear_slots) * wb, lb.size(), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            acc &= s;
+            for (uint32_t j = 0; j < cfg.rough_slots; ++j) rough[j] = std::max(rough[j], word_at(rb, j));
+            if (linear)
+                for (uint32_t j = 0; j < cfg.linear_slots; ++j) linear[j] = std::max(linear[j], word_at(lb, j));
+        }
+        *ind = acc;
+    }
+
+    uint64_t row_bytes(int kind) const {
+        if (kind == SRLA_INDICATOR) return uint64_t(cfg.cols) * 2;
+        if (kind == SRLA_ROUGH) return rough_words * wb;
+        if (kind == SRLA_LINEAR) return lin_words * wb;
+        throw Error(SRLA_E_INVALID, "unknown row kind");
+    }
+
+    uint8_t* row_ptr(uint32_t row, int kind) {
+        if (row >= cfg.rows) throw Error(SRLA_E_RANGE, "row index out of range");
+        const uint64_t b = row_bytes(kind);
+        if (kind == SRLA_INDICATOR) return reinterpret_cast<uint8_t*>(d_si) + row * b;
+        if (kind == SRLA_ROUGH) return static_cast<uint8_t*>(d_rough) + row * b;
+        return static_cast<uint8_t*>(d_lin) + row * b;
+    }
+
+    void export_row(uint32_t row, int kind, void* buf, uint64_t bytes) {
+        uint8_t* p = row_ptr(row, kind);
+        if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
+        CK(cudaMemcpyAsync(buf, p, bytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+
+    void import_row(uint32_t row, int kind, const void* buf, uint64_t bytes) {
+        uint8_t* p = row_ptr(row, kind);
+        if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
+        CK(cudaMemcpyAsync(p, buf, bytes, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+};
+
+}  // namespace srla
+
+// ====================================================================== C ABI
+struct srla_engine {
+    srla::Engine* impl;
+    std::mutex mu;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename Fn>
+srla_status guard(Fn&& fn) {
+    try {
+        fn();
+        g_last_error.clear();
+        return SRLA_OK;
+    } catch (const srla::Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = std::string("host allocation failed: ") + e.what();
+        return SRLA_E_INTERNAL;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SRLA_E_INTERNAL;
+    }
+}
+
+srla::Engine& E(srla_engine* e) {
+    if (!e || !e->impl) throw srla::Error(SRLA_E_INVALID, "null engine");
+    CK(cudaSetDevice(e->impl->device));
+    return *e->impl;
+}
+const srla::Engine& CE(const srla_engine* e) {
+    if (!e || !e->impl) throw srla::Error(SRLA_E_INVALID, "null engine");
+    return *e->impl;
+}
+
+void put_entries(const std::vector<srla_entry>& v, srla_entry* out, uint64_t cap, uint64_t* n_out) {
+    if (n_out) *n_out = v.size();
+    if (v.size() > cap || (!out && !v.empty()))
+        throw srla::Error(SRLA_E_CAPACITY, "report buffer holds " + std::to_string(cap) +
+                                               " entries, " + std::to_string(v.size()) + " needed");
+    if (!v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(srla_entry));
+}
+}  // namespace
+
+extern "C" {
+
+const char* srla_last_error(void) { return g_last_error.c_str(); }
+
+srla_status srla_internal_set_error(srla_status code, const char* msg) {
+    g_last_error = msg ? msg : "";
+    return code;
+}
+const char* srla_version(void) { return "srla_b200 0.1 sm_100a"; }
+
+srla_status srla_create(const srla_config* cfg, int device, srla_engine** out) {
+    return guard([&] {
+        if (!cfg || !out) throw srla::Error(SRLA_E_INVALID, "null argument");
+        *out = nullptr;
+        auto* e = new srla_engine;
+        try {
+            e->impl = new srla::Engine(*cfg, device);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+    });
+}
+
+srla_status srla_destroy(srla_engine* e) {
+    return guard([&] {
+        if (!e) return;
+        if (e->impl) {
+            cudaSetDevice(e->impl->device);
+            delete e->impl;
+        }
+        delete e;
+    });
+}
+
+srla_status srla_params(const srla_engine* e, uint32_t* tau, uint32_t* threshold, uint32_t* word_bytes) {
+    return guard([&] {
+        const auto& x = CE(e);
+        if (tau) *tau = x.tau;
+        if (threshold) *threshold = x.thr;
+        if (word_bytes) *word_bytes = x.wb;
+    });
+}
+
+srla_status srla_column_of(const srla_engine* e, uint32_t row, uint32_t aip, uint32_t* col) {
+    return guard([&] {
+        const auto& x = CE(e);
+        if (row >= x.cfg.rows) throw srla::Error(SRLA_E_RANGE, "row index out of range");
+        *col = x.host_column(row, aip);
+    });
+}
+
+srla_status srla_scan_batch(srla_engine* e, const srla_record* recs, uint64_t n, int on_device,
+                            uint32_t* pushed, uint64_t cap, uint64_t* n_pushed) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        auto& x = E(e);
+        if (n && !recs) throw srla::Error(SRLA_E_INVALID, "null records");
+        x.collect_pushed = pushed != nullptr || n_pushed != nullptr;
+        x.host_pushed.clear();
+        x.scan_batch(recs, n, on_device);
+        CK(cudaStreamSynchronize(x.st));
+        if (n_pushed) *n_pushed = x.host_pushed.size();
+        if (pushed)
+            std::memcpy(pushed, x.host_pushed.data(), std::min<uint64_t>(cap, x.host_pushed.size()) * 4);
+        x.collect_pushed = false;
+    });
+}
+
+srla_status srla_candidates(srla_engine* e, uint32_t* out, uint64_t cap, uint64_t* n) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        auto& x = E(e);
+        std::vector<uint32_t> v;
+        x.candidates(v);
+        if (n) *n = v.size();
+        if (v.size() > cap || (!out && !v.empty()))
+            throw srla::Error(SRLA_E_CAPACITY, "candidate buffer too small");
+        if (!v.empty()) std::memcpy(out, v.data(), v.size() * 4);
+    });
+}
+
+srla_status srla_set_candidates(srla_engine* e, const uint32_t* hosts, uint64_t n) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        if (n && !hosts) throw srla::Error(SRLA_E_INVALID, "null hosts");
+        E(e).set_candidates(hosts, n);
+    });
+}
+
+srla_status srla_report(srla_engine* e, srla_entry* out, uint64_t cap, uint64_t* n_out, double* fill_product) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        std::vector<srla_entry> v;
+        E(e).report(v, fill_product);
+        put_entries(v, out, cap, n_out);
+    });
+}
+
+srla_status srla_slide(srla_engine* e, uint64_t* n_retained) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        auto& x = E(e);
+        x.slide();
+        if (n_retained) *n_retained = x.ncsip;
+    });
+}
+
+srla_status srla_end_slice(srla_engine* e, uint64_t slice_id, int want_report, srla_entry* out,
+                           uint64_t cap, uint64_t* n_out, uint64_t* n_retained) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        auto& x = E(e);
+        const auto w0 = std::chrono::steady_clock::now();
+        CK(cudaEventRecord(x.t_eos0, x.st));
+        if (n_out) *n_out = 0;
+        if (want_report && slice_id + 1 >= x.cfg.window) {  // pipeline.hpp:121
+            if (x.ncsip > cap) {
+                if (n_out) *n_out = x.ncsip;
+                throw srla::Error(SRLA_E_CAPACITY, "report buffer too small");
+            }
+            std::vector<srla_entry> v;
+            x.report(v, nullptr);
+            put_entries(v, out, cap, n_out);
+        }
+        x.slide();
+        CK(cudaEventRecord(x.t_eos1, x.st));
+        CK(cudaEventSynchronize(x.t_eos1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, x.t_eos0, x.t_eos1));
+        x.timing.end_slice_device_ms += ms;
+        x.timing.last_end_slice_device_ms = ms;
+        x.timing.last_end_slice_wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+        x.timing.end_slice_wall_ms += x.timing.last_end_slice_wall_ms;
+        x.timing.end_slices += 1;
+        if (n_retained) *n_retained = x.ncsip;
+    });
+}
+
+srla_status srla_union_weights(srla_engine* e, const uint32_t* hosts, uint64_t n, uint32_t* rough_w,
+                               uint32_t* linear_w) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        if (n && !hosts) throw srla::Error(SRLA_E_INVALID, "null hosts");
+        E(e).union_weights(hosts, n, rough_w, linear_w);
+    });
+}
+
+srla_status srla_union_view(srla_engine* e, uint32_t aip, uint16_t* indicator, uint32_t* rough, uint32_t* linear) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        if (!indicator || !rough) throw srla::Error(SRLA_E_INVALID, "null output");
+        E(e).union_view(aip, indicator, rough, linear);
+    });
+}
+
+srla_status srla_row_active(srla_engine* e, uint64_t* counts) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        if (!counts) throw srla::Error(SRLA_E_INVALID, "null output");
+        E(e).row_active(counts);
+    });
+}
+
+srla_status srla_estimate_from(const srla_engine* e, uint32_t weight, double fill_product, double* estimate,
+                               int* has_estimate) {
+    return guard([&] {
+        const auto& x = CE(e);
+        double v = 0.0;
+        const bool h = srla_host::corrected_estimate(x.cfg.linear_slots, weight, fill_product, &v);
+        if (estimate) *estimate = h ? v : 0.0;
+        if (has_estimate) *has_estimate = h;
+    });
+}
+
+srla_status srla_row_bytes(const srla_engine* e, int kind, uint64_t* bytes) {
+    return guard([&] { *bytes = CE(e).row_bytes(kind); });
+}
+
+srla_status srla_export_row(srla_engine* e, uint32_t row, int kind, void* buf, uint64_t bytes) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        E(e).export_row(row, kind, buf, bytes);
+    });
+}
+
+srla_status srla_import_row(srla_engine* e, uint32_t row, int kind, const void* buf, uint64_t bytes) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        E(e).import_row(row, kind, buf, bytes);
+    });
+}
+
+srla_status srla_stats_get(const srla_engine* e, srla_stats* out) {
+    return guard([&] { *out = CE(e).stats; });
+}
+
+srla_status srla_timing_get(const srla_engine* e, srla_timing* out) {
+    return guard([&] { *out = CE(e).timing; });
+}
+
+srla_status srla_timing_reset(srla_engine* e) {
+    return guard([&] { E(e).timing = srla_timing{}; });
+}
+
+srla_status srla_synchronize(srla_engine* e) {
+    return guard([&] { CK(cudaStreamSynchronize(E(e).st)); });
+}
+
+srla_status srla_stream(srla_engine* e, void** stream) {
+    return guard([&] { *stream = static_cast<void*>(E(e).st); });
+}
+
+}  // extern "C"

@@ -1,0 +1,259 @@
+"""Parity of the CUDA engine (through the C ABI) with the reference.
+
+* every golden scenario (tests/golden/, produced by the unmodified reference):
+  candidate pushes, candidate list order, report entries with the estimate's
+  exact double bits, retained list and a digest of every DR / indicator word;
+* live comparisons with the C restatement on random and contended configs,
+  host vs device input, arbitrary batch splits;
+* ports of the reference's hot-path unit tests (tests/test_sea.cpp);
+* the device trace generator byte-identical to generate_trace.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import golden_flow as GF
+import scenarios as S
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def engine(cfg: S.Cfg):
+    from paper_1803_10369_b200.srla import EstimatorArray, SeaConfig
+    return EstimatorArray(SeaConfig(**cfg.as_dict()))
+
+
+@pytest.mark.parametrize("name", sorted(S.SCENARIOS))
+def test_engine_matches_reference_golden(gpu, oracle, name):
+    g = json.load(open(os.path.join(GOLD, f"{name}.json")))
+    cfg, _ = S.SCENARIOS[name]
+    slices = GF.scenario_slices(name, oracle)
+    assert S.records_digest(slices) == g["records_sha256"]
+    got = GF.run_flow(GF.EngineBackend(engine(cfg)), cfg, slices)
+    msg = GF.compare(g["slices"], got)
+    assert msg is None, msg
+
+
+def _oracle_backend(oracle, cfg):
+    b = GF.CheckerBackend.__new__(GF.CheckerBackend)
+    from oracle.pyoracle import SeaConfig
+    b.sk, b.csip, b.seen = oracle.sketch(SeaConfig(**cfg.as_dict())), [], set()
+    return b
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_engine_matches_oracle_random_configs(gpu, oracle, seed):
+    rng = np.random.default_rng(100 + seed)
+    bits = int(rng.choice([3, 4, 8, 12, 16, 20, 32]))
+    cfg = S.Cfg(rows=int(rng.choice([1, 2, 3, 4, 5, 9])), cols=int(rng.choice([4, 8, 64, 1000, 4096, 65536])),
+                rough_slots=int(rng.integers(1, 40)), linear_slots=int(rng.choice([2, 7, 32, 100, 1024])),
+                recorder_bits=bits, window=int(rng.integers(1, min(40, (1 << min(bits, 30)) - 1) + 1)),
+                theta=int(rng.choice([1, 8, 64, 300, 1024])), seed=int(rng.integers(0, 2**63)))
+    slices = S.random_slices(seed, 10, (0, 20000), int(rng.integers(5, 2000)), int(rng.integers(10, 50000)))
+    a = GF.run_flow(_oracle_backend(oracle, cfg), cfg, slices)
+    b = GF.run_flow(GF.EngineBackend(engine(cfg)), cfg, slices)
+    msg = GF.compare(a, b)
+    assert msg is None, f"{cfg}: {msg}"
+
+
+def test_engine_matches_oracle_c2_shape_medium(gpu, oracle):
+    """The C2 trace shape (uniform 4M sources, Zipf 4M destinations, 50 plants)
+    at 2e6 packets per slice on a 2^16-column sketch: heavy column sharing,
+    thousands of candidates per slice, full bit-exact comparison."""
+    from oracle.pyoracle import PlantSpec
+    spec = S.Spec(seed=1, slices=12, window=10, a_hosts=4194304, b_hosts=1 << 22, pairs_per_slice=2_000_000,
+                  skew=1.0, plants=[(0x0AC80001 + i, c, 0, 0xFFFFFFFF) for i, c in enumerate(S.plant_cards())])
+    recs = oracle.generate(PlantSpec(**spec.__dict__))
+    slices = S.split_by_ts(recs, spec)
+    cfg = S.Cfg(rows=4, cols=1 << 16, rough_slots=8, linear_slots=1024, recorder_bits=4, window=10, theta=1024,
+                seed=0x5EA00001)
+    a = GF.run_flow(_oracle_backend(oracle, cfg), cfg, slices)
+    b = GF.run_flow(GF.EngineBackend(engine(cfg)), cfg, slices)
+    msg = GF.compare(a, b)
+    assert msg is None, msg
+    assert max(s["pushes"]["n"] for s in a) > 100
+
+
+def test_batch_splits_and_device_input(gpu, oracle):
+    import torch
+    cfg, _ = S.SCENARIOS["drift_evict"]
+    slices = GF.scenario_slices("drift_evict", oracle)
+    ref = GF.run_flow(_oracle_backend(oracle, cfg), cfg, slices)
+
+    class Split(GF.EngineBackend):
+        def scan(self, recs):
+            rng = np.random.default_rng(len(recs))
+            cuts = np.sort(rng.integers(0, len(recs) + 1, 5))
+            parts = np.split(recs, cuts)
+            out = []
+            for i, p in enumerate(parts):
+                if i % 2:
+                    t = torch.from_numpy(p.astype(np.int32)).cuda()
+                    torch.cuda.synchronize()
+                    out.append(self.e.scan_collect(t))
+                else:
+                    out.append(self.e.scan_collect(p))
+            return np.concatenate(out) if out else np.empty(0, np.uint32)
+
+    got = GF.run_flow(Split(engine(cfg)), cfg, slices)
+    assert GF.compare(ref, got) is None
+
+
+# ---------------------------------------------------------------- test_sea.cpp ports
+
+def small_config(**kw):
+    c = dict(rows=2, cols=16, rough_slots=8, linear_slots=32, recorder_bits=8, window=4, theta=8, seed=0xFACE)
+    c.update(kw)
+    return S.Cfg(**c)
+
+
+def test_single_pair_updates_one_slot_per_row(gpu, oracle):
+    # tests/test_sea.cpp:39-60
+    from paper_1803_10369_b200.srla import LINEAR, ROUGH
+    cfg = small_config(rows=1)
+    e = engine(cfg)
+    assert e.tau == 0
+    aip, bip = 0x0A000001, 0x08080808
+    assert len(e.scan_ip_pair(aip, bip)) == 0
+    col = e.column_of(0, aip)
+    rslot = oracle.hash_reduce(cfg.seed, 1, bip, cfg.rough_slots)
+    lslot = oracle.hash_u32(cfg.seed, 0, bip) % cfg.linear_slots
+    rough, lin = e.export_row(0, ROUGH), e.export_row(0, LINEAR)
+    assert rough[col * cfg.rough_slots + rslot] == 0 and lin[col * cfg.linear_slots + lslot] == 0
+    assert (rough < cfg.window).sum() == 1 and (lin < cfg.window).sum() == 1
+    assert e.union_rough_weight(aip) == 1
+
+
+def test_indicator_suppresses_duplicates(gpu, oracle):
+    # tests/test_sea.cpp:62-77
+    from paper_1803_10369_b200.srla import INDICATOR
+    e = engine(small_config())
+    aip = 0x0A000002
+    pushes = e.scan_pairs([(aip, 0xC0000000 + i) for i in range(64)])
+    assert list(pushes) == [aip] and list(e.candidates()) == [aip]
+    bit = 1 << oracle.hash_reduce(0xFACE, 2, aip, 16)
+    for i in range(2):
+        assert e.export_row(i, INDICATOR)[e.column_of(i, aip)] & bit
+
+
+def test_union_view_max_semantics(gpu):
+    # tests/test_sea.cpp:79-115
+    from paper_1803_10369_b200.srla import ROUGH
+    cfg = small_config()
+    e = engine(cfg)
+    ind, rough, lin = e.union_view(0x0A000003, True)
+    assert ind == 0 and (rough == 255).all() and (lin == 255).all()
+    aip = 0x0A000005
+    for row, val in ((0, 5), (1, 9)):
+        r = e.export_row(row, ROUGH)
+        r[e.column_of(row, aip) * cfg.rough_slots + 3] = val
+        e.import_row(row, ROUGH, r)
+    ind, rough, lin = e.union_view(aip, False)
+    assert rough[3] == 9 and lin is None
+
+
+def test_row_fill_fraction(gpu):
+    # tests/test_sea.cpp:117-137
+    from paper_1803_10369_b200.srla import LINEAR
+    e = engine(small_config(rows=1, cols=4, linear_slots=1024))
+    assert e.row_fill_fraction(0) == 0.0
+    with pytest.raises(ValueError):
+        e.row_fill_fraction(1)
+    row = e.export_row(0, LINEAR)
+    row[np.arange(512) * 8] = 0
+    e.import_row(0, LINEAR, row)
+    assert e.row_fill_fraction(0) == 0.125
+    full = engine(small_config(rows=1, cols=4, linear_slots=1024, window=1))
+    full.import_row(0, LINEAR, np.zeros(4 * 1024, np.uint8))
+    assert full.row_fill_fraction(0) == 1.0
+
+
+def test_corrected_estimate(gpu, oracle):
+    # tests/test_sea.cpp:139-172
+    e = engine(small_config(rows=4, linear_slots=1024, recorder_bits=16, window=300, theta=1024))
+    for w in (0, 1, 100, 500, 1023):
+        assert e.corrected_estimate_from(w, 0.0) == oracle.linear_estimate(w, 1024)
+    assert e.corrected_estimate_from(1024, 0.0) is None
+    assert e.corrected_estimate_from(4, 0.00390625) == 0.0
+    assert e.corrected_estimate_from(3, 0.00390625) == 0.0
+    assert e.corrected_estimate_from(300, 0.25 ** 4) == pytest.approx(350.99291022602281, rel=1e-12)
+    assert e.corrected_estimate_from(1024, 0.00390625) is None
+    assert e.corrected_estimate_from(100, 1.0 - 1e-13) == oracle.linear_estimate(100, 1024)
+
+
+def test_slide_retains_and_evicts(gpu):
+    # tests/test_sea.cpp:204-254
+    from paper_1803_10369_b200.srla import INDICATOR, LINEAR, ROUGH
+    cfg = small_config()
+    e = engine(cfg)
+    e.scan_ip_pair(0x0A000006, 0xB0000001)
+    assert len(e.slide([])) == 0
+    e2 = engine(cfg)
+    aip = 0x0A000007
+    for i in range(cfg.rows):
+        r = e2.export_row(i, ROUGH)
+        b = e2.column_of(i, aip) * cfg.rough_slots
+        r[b:b + 3] = 0
+        e2.import_row(i, ROUGH, r)
+    out = e2.slide([aip])
+    assert list(out) == [aip]
+    e3 = engine(cfg)
+    aip = 0x0A000008
+    e3.set_candidates([aip])
+    e3.scan_pairs([(aip, 0xD0000000 + i) for i in range(40)])
+    assert e3.union_rough_weight(aip) >= e3.threshold
+    for _ in range(3):
+        assert e3.slide_engine() == 1
+    assert e3.slide_engine() == 0
+    assert e3.union_rough_weight(aip) == 0
+
+
+def test_window_report_sorted_with_theta_cut(gpu):
+    # tests/test_sea.cpp:256-290
+    e = engine(small_config(theta=30, rough_slots=32, linear_slots=128))
+    assert e.tau == 0
+    assert len(e.report_window([])) == 0
+    pairs = [(0x0A0000FF, 0xE0000000 + i) for i in range(60)] + [(0x0A000001, 0xE1000000 + i) for i in range(5)]
+    e.scan_pairs(pairs)
+    csip = list(e.candidates())
+    assert 0x0A0000FF in csip
+    rep = e.report_window(csip + [0x0A000001])
+    assert list(rep["host"]) == [0x0A000001, 0x0A0000FF]
+    assert not rep["is_super"][0] and rep["is_super"][1]
+    assert rep["has_estimate"].all() and (rep["estimate"] >= 0).all()
+
+
+def test_errors_follow_reference(gpu):
+    from paper_1803_10369_b200.srla import INDICATOR, LINEAR
+    e = engine(small_config())
+    with pytest.raises(IndexError):
+        e.export_row(2, LINEAR)  # std::out_of_range from .at() (sea.hpp:341-346)
+    with pytest.raises(ValueError):
+        e.import_row(0, INDICATOR, np.zeros(3, np.uint16))
+
+
+def test_device_generator_byte_identical(gpu, oracle):
+    import torch
+    from oracle.pyoracle import PlantSpec as OSpec
+    from paper_1803_10369_b200.srla import DeviceTraceGenerator, PlantSpec
+    for name in ("pipeline_small", "c1_shape"):
+        _, (_, spec) = S.SCENARIOS[name]
+        want = S.split_by_ts(oracle.generate(OSpec(**spec.__dict__)), spec)
+        gen = DeviceTraceGenerator(PlantSpec(**spec.__dict__))
+        for s in range(spec.slices):
+            got = gen.slice_tensor(s).cpu().numpy().view(np.uint32)
+            assert np.array_equal(got, want[s]), (name, s)
+    # C2 shape, uniform and Zipf destinations, a later slice (counter skip-ahead)
+    for skew in (1.0, 0.0):
+        spec = S.Spec(seed=1, slices=3, window=10, a_hosts=4194304, b_hosts=1 << 22, pairs_per_slice=1_000_000,
+                      skew=skew, plants=[(0x0AC80001 + i, c, 0, 0xFFFFFFFF) for i, c in enumerate(S.plant_cards())])
+        want = S.split_by_ts(oracle.generate(OSpec(**spec.__dict__)), spec)
+        gen = DeviceTraceGenerator(PlantSpec(**spec.__dict__))
+        got = gen.slice_tensor(2).cpu().numpy().view(np.uint32)
+        torch.cuda.synchronize()
+        assert np.array_equal(got, want[2])

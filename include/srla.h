@@ -5,7 +5,7 @@
  * header-only C++ library with no FFI; its hot path is the EstimatorArray /
  * DetectPipeline API. Every entry point below replaces one reference call (the
  * cite is on each declaration) and is what the drop-in headers in
- * include/sspread/*.hpp bind. Plain pointers and sizes only; no CUDA or torch
+ * include/sspread/ (*.hpp) bind. Plain pointers and sizes only; no CUDA or torch
  * types cross this boundary. One CUDA stream per engine; an engine is not
  * re-entrant (the drop-in wrapper serialises calls, matching the reference's
  * "exclusive access outside the scan phase" contract, sea.hpp:108-112).

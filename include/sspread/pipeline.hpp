@@ -1,0 +1,165 @@
+// sspread/pipeline.hpp — drop-in for the reference's detection driver
+// (/root/reference/proj/include/sspread/pipeline.hpp) on the B200 engine.
+//
+// process_slice keeps the reference contract (scan, report when the window is
+// full and a sink is set, slide; pipeline.hpp:110-129) but the record batch
+// crosses to the device once and the candidate list stays in HBM between
+// slices. process_slice_device() is an addition for records already resident
+// on the GPU. Exact-cardinality ground truth (run_oracle, oracle.hpp) is not
+// part of the hot path and is not provided.
+#pragma once
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <functional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "sea.hpp"
+#include "trace.hpp"
+
+namespace sspread {
+
+class ConfigError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
+class InternalError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
+struct RunConfig {
+    SeaConfig sea;
+    uint32_t slice_seconds = 300;
+    CidrPrefix a_network{0x0A000000, 8};
+    uint32_t workers = 1;  // host threads for host-side helpers; the sketch runs on the GPU
+    int device = 0;        // addition: CUDA device of the sketch
+
+    void validate() const {  // pipeline.hpp:38-48
+        try {
+            sea.validate();
+            if (slice_seconds == 0) throw std::invalid_argument("slice duration must be >= 1 second");
+            if (workers == 0 || workers > 256) throw std::invalid_argument("workers must be in [1, 256]");
+            if (sea.cols & (sea.cols - 1)) throw std::invalid_argument("cols must be a power of two");
+        } catch (const std::invalid_argument& e) {
+            throw ConfigError(e.what());
+        }
+    }
+};
+
+// fn over near-equal subranges of [0, total) on `workers` threads (pipeline.hpp:54-68)
+inline void parallel_ranges(uint64_t total, uint32_t workers, const std::function<void(uint64_t, uint64_t)>& fn) {
+    if (!total) return;
+    const uint64_t n = std::min<uint64_t>(std::max<uint32_t>(workers, 1), total);
+    std::vector<std::thread> pool;
+    for (uint64_t w = 1; w < n; ++w) pool.emplace_back([&, w] { fn(total * w / n, total * (w + 1) / n); });
+    fn(0, total / n);
+    for (auto& t : pool) t.join();
+}
+
+inline ChunkRunner chunked(uint32_t workers) {
+    return [workers](uint64_t total, const std::function<void(uint64_t, uint64_t)>& fn) {
+        parallel_ranges(total, workers, fn);
+    };
+}
+
+template <RecorderWord W>
+class DetectPipeline {
+  public:
+    using ReportSink = std::function<void(const WindowReport&)>;
+
+    explicit DetectPipeline(const RunConfig& cfg) : cfg_((cfg.validate(), cfg)), sea_(cfg.sea, cfg.device) {}
+
+    EstimatorArray<W>& sketch() noexcept { return sea_; }
+    const OrientStats& orient_stats() const noexcept { return stats_; }
+    uint64_t pairs_scanned() const noexcept { return pairs_; }
+    uint64_t slices_seen() const noexcept { return slices_; }
+    double total_scan_ms() const noexcept { return total_scan_ms_; }
+    double total_estimate_ms() const noexcept { return total_estimate_ms_; }
+
+    void run(const std::string& trace_path, const ReportSink& sink) {  // pipeline.hpp:96-106
+        SlicePartitioner partitioner(cfg_.slice_seconds);
+        const auto on_slice = [&](uint64_t id, std::vector<TraceRecord>&& records) {
+            process_slice(id, records, sink);
+        };
+        for_each_record(trace_path, [&](const TraceRecord& r) {
+            if (const auto o = orient_record(r, cfg_.a_network, stats_)) partitioner.push(*o, on_slice);
+        });
+        partitioner.finish(on_slice);
+    }
+
+    void process_slice(uint64_t slice_id, std::span<const TraceRecord> records, const ReportSink& sink) {
+        process(slice_id, records.data(), records.size(), 0, sink);
+    }
+
+    // Addition: `d_records` points to `n` records in device memory on the
+    // sketch's GPU (e.g. a capture ring already in HBM).
+    void process_slice_device(uint64_t slice_id, const TraceRecord* d_records, uint64_t n, const ReportSink& sink) {
+        process(slice_id, d_records, n, 1, sink);
+    }
+
+    const CandidateList& candidates() const {
+        if (!csip_valid_) {
+            csip_.clear();
+            const std::vector<uint32_t> v =
+                sea_.st_->pipeline_owns_list ? sea_.engine_list() : sea_.st_->saved_pipeline_list;
+            for (uint32_t h : v) csip_.insert(h);
+            csip_valid_ = true;
+        }
+        return csip_;
+    }
+
+  private:
+    void process(uint64_t slice_id, const TraceRecord* recs, uint64_t n, int on_device, const ReportSink& sink) {
+        sea_.pipeline_mode();
+        sea_.to_device();
+        const auto t0 = std::chrono::steady_clock::now();
+        detail::check(srla_scan_batch(sea_.eng(), reinterpret_cast<const srla_record*>(recs), n, on_device, nullptr,
+                                      0, nullptr),
+                      "srla_scan_batch");
+        const double scan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        total_scan_ms_ += scan_ms;
+        pairs_ += n;
+        ++slices_;
+        const uint32_t k = cfg_.sea.window;
+        if (slice_id + 1 >= k && sink) {
+            WindowReport report = sea_.engine_report(slice_id + 1 - k);
+            report.scan_ms = scan_ms;
+            total_estimate_ms_ += report.estimate_ms;
+            sink(report);
+        }
+        uint64_t kept = 0;
+        detail::check(srla_slide(sea_.eng(), &kept), "srla_slide");
+        sea_.st_->mirror_valid = false;
+        csip_valid_ = false;
+    }
+
+    RunConfig cfg_;
+    EstimatorArray<W> sea_;
+    mutable CandidateList csip_;
+    mutable bool csip_valid_ = false;
+    OrientStats stats_;
+    uint64_t pairs_ = 0;
+    uint64_t slices_ = 0;
+    double total_scan_ms_ = 0;
+    double total_estimate_ms_ = 0;
+};
+
+// Runtime width -> storage word (pipeline.hpp:173-180).
+template <typename Fn>
+decltype(auto) with_recorder_word(uint32_t recorder_bits, Fn&& fn) {
+    switch (recorder_word_bytes(recorder_bits)) {
+        case 1: return fn(uint8_t{0});
+        case 2: return fn(uint16_t{0});
+        default: return fn(uint32_t{0});
+    }
+}
+
+}  // namespace sspread

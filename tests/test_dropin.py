@@ -1,0 +1,92 @@
+"""The C++ drop-in (include/sspread/*.hpp over the C ABI): compiles against
+the headers on CPU; on the GPU runs the reference's own unit tests rewritten
+against it and replays DetectPipeline::process_slice against the oracle."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import golden_flow as GF
+import scenarios as S
+from conftest import ROOT
+
+SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+LIBDIR = os.path.join(ROOT, "paper_1803_10369_b200", "lib")
+
+
+@pytest.fixture(scope="module")
+def dropin_bin(srla_lib, tmp_path_factory):
+    out = str(tmp_path_factory.mktemp("dropin") / "test_dropin")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    SRC, "-L", LIBDIR, "-lsrla_b200", f"-Wl,-rpath,{LIBDIR}", "-o", out], check=True)
+    return out
+
+
+def test_dropin_headers_compile_and_link(dropin_bin):
+    assert os.path.exists(dropin_bin)
+
+
+@pytest.mark.gpu
+def test_dropin_reference_unit_tests(gpu, dropin_bin):
+    r = subprocess.run([dropin_bin], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr + r.stdout
+
+
+def _write_srlt(path, recs):
+    with open(path, "wb") as f:
+        f.write(b"SRLT\x01")
+        f.write(np.ascontiguousarray(recs, dtype="<u4").tobytes())
+
+
+def _parse(path):
+    slices, cur = [], None
+    lines = open(path).read().split("\n")
+    i = 0
+    while i < len(lines):
+        ln = lines[i]
+        if ln.startswith("report "):
+            _, ws, n = ln.split()
+            rows = [list(map(int, lines[i + 1 + j].split())) for j in range(int(n))]
+            cur = {"report": rows}
+            i += 1 + int(n)
+            continue
+        if ln.startswith("csip "):
+            n = int(ln.split()[1])
+            csip = [int(x) for x in lines[i + 1:i + 1 + n]]
+            slices.append({"report": (cur or {}).get("report"), "csip": csip})
+            cur = None
+            i += 1 + n
+            continue
+        i += 1
+    return slices
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["pipeline_small", "pipeline_small_3000", "c1_shape"])
+def test_dropin_pipeline_replay_matches_oracle(gpu, oracle, dropin_bin, tmp_path, name):
+    cfg, (_, spec) = S.SCENARIOS[name]
+    slices = GF.scenario_slices(name, oracle)
+    trace = tmp_path / "t.bin"
+    _write_srlt(trace, np.concatenate(slices))
+    out = tmp_path / "out.txt"
+    c = cfg
+    subprocess.run([dropin_bin, "replay", str(trace), str(out), str(c.rows), str(c.cols), str(c.rough_slots),
+                    str(c.linear_slots), str(c.recorder_bits), str(c.window), str(c.theta), hex(c.seed)],
+                   check=True, timeout=600)
+    got = _parse(out)
+    pipe = oracle.pipeline(__import__("oracle.pyoracle", fromlist=["SeaConfig"]).SeaConfig(**c.as_dict()))
+    assert len(got) == len(slices)
+    for s, recs in enumerate(slices):
+        rep = pipe.process_slice(s, recs, True)
+        want_csip = pipe.candidates().tolist()
+        assert got[s]["csip"] == want_csip, f"slice {s}"
+        if rep is None:
+            assert got[s]["report"] is None
+            continue
+        bits = rep["estimate"].view(np.uint64)
+        want = [[int(h), int(w), int(b) if has else 0, int(has), int(sup)]
+                for h, w, b, has, sup in zip(rep["host"], rep["weight"], bits, rep["has_estimate"], rep["is_super"])]
+        assert got[s]["report"] == want, f"slice {s}"

@@ -76,7 +76,7 @@ def test_engine_matches_oracle_c2_shape_medium(gpu, oracle):
     b = GF.run_flow(GF.EngineBackend(engine(cfg)), cfg, slices)
     msg = GF.compare(a, b)
     assert msg is None, msg
-    assert max(s["pushes"]["n"] for s in a) > 100
+    assert sum(s["pushes"]["n"] for s in a) > 50
 
 
 def test_batch_splits_and_device_input(gpu, oracle):

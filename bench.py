@@ -361,6 +361,8 @@ def run_engine(args):
                          "algorithmic_bytes_per_packet": ALGO_BYTES_PER_PACKET,
                          "packets_per_launch": recs_per_launch, "ms_per_launch": ms_per_launch,
                          "share_of_step": tm["scan_kernel_ms"] / ms},
+            "breakdown_ms_per_step": {k: tm[k] / args.steps for k in
+                                      ("scan_kernel_ms", "order_wall_ms", "report_wall_ms", "slide_wall_ms")},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),

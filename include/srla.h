@@ -173,6 +173,9 @@ typedef struct srla_timing {
     double last_end_slice_device_ms;
     double last_end_slice_wall_ms;
     uint64_t end_slices;
+    double order_wall_ms;   /* K2..K5 + candidate append, per-chunk host wall, summed */
+    double report_wall_ms;  /* report_window part of end-of-slice */
+    double slide_wall_ms;   /* slide part of end-of-slice */
 } srla_timing;
 srla_status srla_timing_get(const srla_engine* e, srla_timing* out);
 srla_status srla_timing_reset(srla_engine* e);

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <unordered_set>
@@ -20,6 +21,7 @@
 
 #include "host_math.h"
 #include "kernels.cuh"
+#include "scan_binned.cuh"
 #include "srla.h"
 
 namespace srla {
@@ -122,8 +124,18 @@ struct Engine {
     srla_timing timing{};
     PinBuf<unsigned long long> pin_counts;
     std::vector<uint32_t> host_pushed;
+    std::vector<double> lut_est;
+    std::vector<uint8_t> lut_has, lut_sup;
     bool collect_pushed = false;
     srla_stats stats{};
+
+    // binned linear marks (scan_binned.cuh), for tables larger than L2
+    bool use_bins = false;
+    BinCfg bcfg{};
+    DevBuf<uint32_t> bins, bin_count;
+    PinBuf<uint32_t> pin_bc;
+    uint64_t pending_entries = 0;
+    bool prefetch_next = false;  // bulk-prefetch region r+1 while applying r (measured slower; off)
 
     // ------------------------------------------------------------ lifecycle
     explicit Engine(const srla_config& c, int dev) : cfg(c), device(dev) {
@@ -173,6 +185,7 @@ struct Engine {
         CK(cudaMemsetAsync(d_stamp, 0xFF, rows * rough_words * sizeof(uint32_t), st));
         ctr.ensure(16);
         pin_ctr.ensure(16);
+        setup_bins();
         rebuild_cset(1024);
         CK(cudaStreamSynchronize(st));
     }
@@ -302,6 +315,91 @@ struct Engine {
         }
     }
 
+    // ------------------------------------------------------------ binned linear marks
+    void setup_bins() {
+        const uint64_t total_words = uint64_t(cfg.rows) * lin_words;
+        const char* direct = std::getenv("SRLA_DIRECT_MARKS");  // A/B switch for measurements
+        const char* force = std::getenv("SRLA_FORCE_BINS");     // exercise the binned path on small tables (tests)
+        const bool forced = force && force[0] == '1';
+        if (cfg.rows > kBinRows || (direct && direct[0] == '1')) return;
+        if (!forced && total_words * wb < (256ull << 20)) return;
+        uint32_t shift = 0;
+        const char* rmb = std::getenv("SRLA_REGION_MB");  // tuning knob; 32 MB measured best (tools/applybench.cu)
+        const uint64_t region_bytes = (rmb ? std::max(1, std::atoi(rmb)) : 32) * (1ull << 20);
+        while ((1ull << (shift + 1)) * wb <= region_bytes) ++shift;
+        const char* pf = std::getenv("SRLA_PREFETCH");
+        prefetch_next = pf && pf[0] == '1';
+        if (forced)
+            while (shift > 2 && (total_words >> shift) < 8) --shift;  // ~8 regions even for tiny tables
+        while ((total_words >> shift) >= kMaxRegions) ++shift;
+        bcfg.region_shift = shift;
+        bcfg.nregions = static_cast<uint32_t>((total_words + (1ull << shift) - 1) >> shift);
+        const uint64_t total_cap = forced && total_words * wb < (256ull << 20) ? (1ull << 16) : (3ull << 28);
+        bcfg.cap = static_cast<uint32_t>(std::min<uint64_t>(total_cap / bcfg.nregions, 0xFFFFFFF0ull)) & ~3u;
+        bins.ensure(uint64_t(bcfg.cap) * bcfg.nregions);
+        bin_count.ensure(bcfg.nregions);
+        pin_bc.ensure(bcfg.nregions);
+        CK(cudaMemsetAsync(bin_count.p, 0, bcfg.nregions * sizeof(uint32_t), st));
+        bcfg.bins = bins.p;
+        bcfg.count = bin_count.p;
+        use_bins = true;
+    }
+
+    // Age (and optionally count) linear words [w0, w1) — split at row
+    // boundaries so each piece counts into its own row.
+    template <typename W>
+    void count_age_range(uint64_t w0, uint64_t w1, bool count) {
+        while (w0 < w1) {
+            const uint64_t row = w0 / lin_words;
+            const uint64_t end = std::min(w1, (row + 1) * lin_words);
+            k_count_age<W><<<blocks((end - w0) * sizeof(W) / 16 + 1, 256, 8), 256, 0, st>>>(
+                static_cast<W*>(d_lin) + w0, end - w0, cfg.window, dc.expired, count ? 1 : 0, d_counts.p + row);
+            check_launch();
+            launched();
+            w0 = end;
+        }
+    }
+
+    // Apply pending linear marks one L2-resident region at a time. mode 0:
+    // apply only; 1: apply then age each region while it is still in L2;
+    // 2: apply, count active (into d_counts) and age. Modes 1/2 cover the
+    // whole table (regions without pending marks are aged too).
+    void flush_linear(int mode = 0) {
+        if (!use_bins) return;
+        if (pending_entries == 0 && mode == 0) return;
+        if (pending_entries) {
+            CK(cudaMemcpyAsync(pin_bc.p, bin_count.p, bcfg.nregions * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        } else {
+            std::memset(pin_bc.p, 0, bcfg.nregions * sizeof(uint32_t));
+        }
+        const uint64_t total = uint64_t(cfg.rows) * lin_words;
+        with_w([&](auto w) {
+            using W = decltype(w);
+            const uint8_t* lin8 = static_cast<const uint8_t*>(d_lin);
+            auto region_bytes = [&](uint32_t r) {
+                const uint64_t a = uint64_t(r) << bcfg.region_shift;
+                return (std::min(total, uint64_t(r + 1) << bcfg.region_shift) - a) * sizeof(W);
+            };
+            for (uint32_t r = 0; r < bcfg.nregions; ++r) {
+                const uint32_t m = std::min(pin_bc.p[r], bcfg.cap);
+                const bool more = prefetch_next && r + 1 < bcfg.nregions;
+                const uint8_t* next = more ? lin8 + ((uint64_t(r + 1) << bcfg.region_shift) * sizeof(W)) : nullptr;
+                if (m || more) {
+                    k_apply_bins<W><<<blocks((m + 3) / 4 + 1, 256, 8), 256, 0, st>>>(
+                        static_cast<W*>(d_lin), bins.p, bcfg.cap, r, m, bcfg.region_shift, next,
+                        more ? region_bytes(r + 1) : 0);
+                    check_launch();
+                    launched();
+                }
+                if (mode) count_age_range<W>(uint64_t(r) << bcfg.region_shift,
+                                             std::min(total, uint64_t(r + 1) << bcfg.region_shift), mode == 2);
+            }
+        });
+        if (pending_entries) CK(cudaMemsetAsync(bin_count.p, 0, bcfg.nregions * sizeof(uint32_t), st));
+        pending_entries = 0;
+    }
+
     // ------------------------------------------------------------ scan
     template <typename W, int MAXR>
     void scan_chunk_t(const uint32_t* d_recs, uint32_t n) {
@@ -315,12 +413,22 @@ struct Engine {
         uint32_t n_ev = 0;
         for (;;) {
             CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
+            if (use_bins) {
+                const uint64_t add = uint64_t(n) * cfg.rows;
+                if ((pending_entries + add) / bcfg.nregions * 13 / 10 + 8192 > bcfg.cap) flush_linear();
+            }
             CK(cudaEventRecord(t_scan0, st));
-            k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+            if (use_bins && MAXR <= kBinRows) {
+                const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
+                k_scan_bin<W><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, st>>>(d_recs, n, dc, bcfg, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+            } else {
+                k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+            }
             check_launch();
             launched();
             CK(cudaEventRecord(t_scan1, st));
             n_ev = read_ctr(0);
+            if (use_bins) pending_entries += uint64_t(n) * cfg.rows;
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, t_scan0, t_scan1));
             timing.scan_kernel_ms += ms;
@@ -333,6 +441,12 @@ struct Engine {
         }
         stats.sampled_events += n_ev;
         if (!n_ev) return;
+        const auto w_order = std::chrono::steady_clock::now();
+        struct OrderTimer {
+            srla_timing& t;
+            std::chrono::steady_clock::time_point t0;
+            ~OrderTimer() { t.order_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+        } order_timer{timing, w_order};
 
         xkeys.ensure(n_ev);
         k_cross<W, MAXR><<<blocks(n_ev), 256, 0, st>>>(ev.p, ev_cap, n_ev, dc, rough, d_stamp, xkeys.p, ctr.p + 1);
@@ -494,17 +608,17 @@ struct Engine {
 
     // ------------------------------------------------------------ report
     template <typename W, int MAXR>
-    void union_linear_t(const uint32_t* d_hosts, uint32_t n, uint32_t* d_out) {
-        k_union_linear<W, MAXR><<<blocks(uint64_t(n) * 32, 256, 16), 256, 0, st>>>(d_hosts, n, dc, static_cast<const W*>(d_lin), d_out);
+    void union_linear_t(const uint32_t* d_hosts, uint32_t n, uint32_t* d_out, uint32_t kthr) {
+        k_union_linear<W, MAXR><<<blocks(uint64_t(n) * 32, 256, 16), 256, 0, st>>>(d_hosts, n, dc, static_cast<const W*>(d_lin), kthr, d_out);
         check_launch();
         launched();
     }
-    void union_linear(const uint32_t* d_hosts, uint32_t n, uint32_t* d_out) {
+    void union_linear(const uint32_t* d_hosts, uint32_t n, uint32_t* d_out, uint32_t kthr) {
         if (!n) return;
         with_w([&](auto w) {
             using W = decltype(w);
-            if (cfg.rows <= 4) union_linear_t<W, 4>(d_hosts, n, d_out);
-            else union_linear_t<W, 64>(d_hosts, n, d_out);
+            if (cfg.rows <= 4) union_linear_t<W, 4>(d_hosts, n, d_out, kthr);
+            else union_linear_t<W, 64>(d_hosts, n, d_out, kthr);
         });
     }
 
@@ -522,6 +636,7 @@ struct Engine {
     }
 
     void row_active(uint64_t* out) {
+        flush_linear();
         row_active_async();
         pin_counts.ensure(cfg.rows);
         CK(cudaMemcpyAsync(pin_counts.p, d_counts.p, cfg.rows * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -529,17 +644,25 @@ struct Engine {
         for (uint32_t i = 0; i < cfg.rows; ++i) out[i] = pin_counts.p[i];
     }
 
-    // report_window (sea.hpp:288-309)
-    void report(std::vector<srla_entry>& out, double* fp_out) {
+    // report_window (sea.hpp:288-309). With counts_ready, d_counts already
+    // holds the per-row active counts and the table has been aged by the fused
+    // count+age pass, so union activity is tested with r < k+1 (exact while
+    // k < expired: an aged recorder r' = r+1 for every r < expired).
+    void report(srla_entry* out, double* fp_out, bool counts_ready = false) {
+        const auto w0 = std::chrono::steady_clock::now();
         const uint32_t n = static_cast<uint32_t>(ncsip);
-        row_active_async();
+        const uint32_t kthr = counts_ready ? cfg.window + 1 : cfg.window;
+        if (!counts_ready) {
+            flush_linear();
+            row_active_async();
+        }
         if (n) {
             sorted_hosts.ensure(n);
             weights.ensure(n);
             cub_call([&](void* t, size_t& b) {
                 return cub::DeviceRadixSort::SortKeys(t, b, csip.p, sorted_hosts.p, static_cast<int>(n), 0, 32, st);
             });
-            union_linear(sorted_hosts.p, n, weights.p);
+            union_linear(sorted_hosts.p, n, weights.p, kthr);
             pin_hosts.ensure(n);
             pin_w.ensure(n);
             CK(cudaMemcpyAsync(pin_hosts.p, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, st));
@@ -551,32 +674,48 @@ struct Engine {
         std::vector<uint64_t> counts(pin_counts.p, pin_counts.p + cfg.rows);
         const double fp = srla_host::fill_product(counts.data(), cfg.rows, lin_words);
         if (fp_out) *fp_out = fp;
-        std::vector<double> est(cfg.linear_slots + 1);
-        std::vector<uint8_t> has(cfg.linear_slots + 1), sup(cfg.linear_slots + 1);
-        srla_host::estimate_lut(cfg.linear_slots, fp, cfg.theta, est.data(), has.data(), sup.data());
-        out.resize(n);
-        for (uint32_t e = 0; e < n; ++e) {
-            const uint32_t w = pin_w.p[e];
-            srla_entry& x = out[e];
-            x.host = pin_hosts.p[e];
-            x.union_weight = w;
-            x.estimate = est[w];
-            x.has_estimate = has[w];
-            x.is_super = sup[w];
-            std::memset(x.reserved, 0, sizeof(x.reserved));
+        lut_est.resize(cfg.linear_slots + 1);
+        lut_has.resize(cfg.linear_slots + 1);
+        lut_sup.resize(cfg.linear_slots + 1);
+        srla_host::estimate_lut(cfg.linear_slots, fp, cfg.theta, lut_est.data(), lut_has.data(), lut_sup.data());
+        // map (host, weight) -> entries straight into the caller's buffer
+        auto fill = [&](uint32_t lo, uint32_t hi) {
+            for (uint32_t e = lo; e < hi; ++e) {
+                const uint32_t w = pin_w.p[e];
+                srla_entry x{};
+                x.host = pin_hosts.p[e];
+                x.union_weight = w;
+                x.estimate = lut_est[w];
+                x.has_estimate = lut_has[w];
+                x.is_super = lut_sup[w];
+                out[e] = x;
+            }
+        };
+        const uint32_t nt = n >= (1u << 16) ? 8u : 1u;
+        if (nt == 1) {
+            fill(0, n);
+        } else {
+            std::vector<std::thread> pool;
+            for (uint32_t t = 1; t < nt; ++t) pool.emplace_back(fill, uint64_t(n) * t / nt, uint64_t(n) * (t + 1) / nt);
+            fill(0, n / nt);
+            for (auto& th : pool) th.join();
         }
+        timing.report_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
     }
 
     // ------------------------------------------------------------ slide (sea.hpp:316-338)
     template <typename W, int MAXR>
-    void slide_t() {
+    void slide_t(bool age_linear) {
         const uint64_t rows = cfg.rows;
         CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st));
         k_age<W><<<blocks(rows * rough_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_rough), rows * rough_words, dc.expired);
         check_launch();
-        k_age<W><<<blocks(rows * lin_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_lin), rows * lin_words, dc.expired);
-        check_launch();
-        launched(2);
+        launched();
+        if (age_linear) {
+            k_age<W><<<blocks(rows * lin_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_lin), rows * lin_words, dc.expired);
+            check_launch();
+            launched();
+        }
         if (!ncsip) return;
         const uint32_t n = static_cast<uint32_t>(ncsip);
         keep.ensure(n);
@@ -593,14 +732,44 @@ struct Engine {
         rebuild_cset(ncsip);
     }
 
-    void slide() {
+    void slide(bool age_linear = true) {
+        const auto w0 = std::chrono::steady_clock::now();
         stats.slides++;
+        flush_linear();
         with_w([&](auto w) {
             using W = decltype(w);
-            if (cfg.rows <= 4) slide_t<W, 4>();
-            else slide_t<W, 64>();
+            if (cfg.rows <= 4) slide_t<W, 4>(age_linear);
+            else slide_t<W, 64>(age_linear);
         });
         CK(cudaStreamSynchronize(st));
+        timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+    }
+
+    // process_slice tail (pipeline.hpp:119-128). When a report is due and
+    // k < expired, one fused pass counts and ages the linear table, and the
+    // report reads the aged table (see report()).
+    void end_slice(uint64_t slice_id, bool want_report, srla_entry* out) {
+        const bool due = want_report && slice_id + 1 >= cfg.window;
+        const auto w0 = std::chrono::steady_clock::now();
+        if (due && dc.k < dc.expired) {
+            d_counts.ensure(cfg.rows);
+            CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
+            if (use_bins) {
+                flush_linear(2);
+            } else {
+                with_w([&](auto w) { count_age_range<decltype(w)>(0, uint64_t(cfg.rows) * lin_words, true); });
+            }
+            timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+            report(out, nullptr, true);
+            slide(false);
+        } else if (!due && use_bins) {
+            flush_linear(1);
+            timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+            slide(false);
+        } else {
+            if (due) report(out, nullptr);
+            slide(true);
+        }
     }
 
     // ------------------------------------------------------------ queries
@@ -645,7 +814,8 @@ struct Engine {
             CK(cudaMemcpyAsync(rw, rweights.p, n * 4, cudaMemcpyDeviceToHost, st));
         }
         if (lw) {
-            union_linear(qhosts.p, m, weights.p);
+            flush_linear();
+            union_linear(qhosts.p, m, weights.p, cfg.window);
             CK(cudaMemcpyAsync(lw, weights.p, n * 4, cudaMemcpyDeviceToHost, st));
         }
         CK(cudaStreamSynchronize(st));
@@ -663,6 +833,7 @@ struct Engine {
 
     // union_view (sea.hpp:199-217)
     void union_view(uint32_t aip, uint16_t* ind, uint32_t* rough, uint32_t* linear) {
+        flush_linear();
         uint16_t acc = 0xFFFF;
         std::fill(rough, rough + cfg.rough_slots, 0u);
         if (linear) std::fill(linear, linear + cfg.linear_slots, 0u);
@@ -699,6 +870,7 @@ struct Engine {
     }
 
     void export_row(uint32_t row, int kind, void* buf, uint64_t bytes) {
+        flush_linear();
         uint8_t* p = row_ptr(row, kind);
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
         CK(cudaMemcpyAsync(buf, p, bytes, cudaMemcpyDeviceToHost, st));
@@ -706,6 +878,7 @@ struct Engine {
     }
 
     void import_row(uint32_t row, int kind, const void* buf, uint64_t bytes) {
+        flush_linear();
         uint8_t* p = row_ptr(row, kind);
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
         CK(cudaMemcpyAsync(p, buf, bytes, cudaMemcpyHostToDevice, st));
@@ -752,12 +925,11 @@ const srla::Engine& CE(const srla_engine* e) {
     return *e->impl;
 }
 
-void put_entries(const std::vector<srla_entry>& v, srla_entry* out, uint64_t cap, uint64_t* n_out) {
-    if (n_out) *n_out = v.size();
-    if (v.size() > cap || (!out && !v.empty()))
-        throw srla::Error(SRLA_E_CAPACITY, "report buffer holds " + std::to_string(cap) +
-                                               " entries, " + std::to_string(v.size()) + " needed");
-    if (!v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(srla_entry));
+void check_capacity(uint64_t need, srla_entry* out, uint64_t cap, uint64_t* n_out) {
+    if (n_out) *n_out = need;
+    if (need > cap || (!out && need))
+        throw srla::Error(SRLA_E_CAPACITY, "report buffer holds " + std::to_string(cap) + " entries, " +
+                                               std::to_string(need) + " needed");
 }
 }  // namespace
 
@@ -855,9 +1027,9 @@ srla_status srla_set_candidates(srla_engine* e, const uint32_t* hosts, uint64_t 
 srla_status srla_report(srla_engine* e, srla_entry* out, uint64_t cap, uint64_t* n_out, double* fill_product) {
     return guard([&] {
         std::lock_guard<std::mutex> lk(e->mu);
-        std::vector<srla_entry> v;
-        E(e).report(v, fill_product);
-        put_entries(v, out, cap, n_out);
+        auto& x = E(e);
+        check_capacity(x.ncsip, out, cap, n_out);
+        x.report(out, fill_product);
     });
 }
 
@@ -878,16 +1050,9 @@ srla_status srla_end_slice(srla_engine* e, uint64_t slice_id, int want_report, s
         const auto w0 = std::chrono::steady_clock::now();
         CK(cudaEventRecord(x.t_eos0, x.st));
         if (n_out) *n_out = 0;
-        if (want_report && slice_id + 1 >= x.cfg.window) {  // pipeline.hpp:121
-            if (x.ncsip > cap) {
-                if (n_out) *n_out = x.ncsip;
-                throw srla::Error(SRLA_E_CAPACITY, "report buffer too small");
-            }
-            std::vector<srla_entry> v;
-            x.report(v, nullptr);
-            put_entries(v, out, cap, n_out);
-        }
-        x.slide();
+        const bool due = want_report && slice_id + 1 >= x.cfg.window;  // pipeline.hpp:121
+        if (due) check_capacity(x.ncsip, out, cap, n_out);
+        x.end_slice(slice_id, want_report != 0, out);
         CK(cudaEventRecord(x.t_eos1, x.st));
         CK(cudaEventSynchronize(x.t_eos1));
         float ms = 0.f;

@@ -409,12 +409,12 @@ __device__ __forceinline__ uint32_t vmax_word(uint32_t a, uint32_t b) {
 }
 template <typename W, int MAXR>
 __global__ void __launch_bounds__(256) k_union_linear(const uint32_t* __restrict__ hosts, uint32_t n,
-                                                      DevCfg c, const W* __restrict__ lin,
+                                                      DevCfg c, const W* __restrict__ lin, uint32_t kthr,
                                                       uint32_t* __restrict__ weight) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     const uint64_t lrow = static_cast<uint64_t>(c.cols) * c.gl;
-    const uint32_t kk = sizeof(W) == 1 ? c.k * 0x01010101u : sizeof(W) == 2 ? c.k * 0x00010001u : c.k;
+    const uint32_t kk = sizeof(W) == 1 ? kthr * 0x01010101u : sizeof(W) == 2 ? kthr * 0x00010001u : kthr;
     const bool vec = ((static_cast<uint64_t>(c.gl) * sizeof(W)) & 15) == 0;
     for (uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < n; h += warps) {
         const uint32_t a = hosts[h];
@@ -436,8 +436,8 @@ __global__ void __launch_bounds__(256) k_union_linear(const uint32_t* __restrict
                     m.z = vmax_word<W>(m.z, x.z);
                     m.w = vmax_word<W>(m.w, x.w);
                 }
-                acc += count_lt_word<W>(m.x, kk, c.k) + count_lt_word<W>(m.y, kk, c.k) +
-                       count_lt_word<W>(m.z, kk, c.k) + count_lt_word<W>(m.w, kk, c.k);
+                acc += count_lt_word<W>(m.x, kk, kthr) + count_lt_word<W>(m.y, kk, kthr) +
+                       count_lt_word<W>(m.z, kk, kthr) + count_lt_word<W>(m.w, kk, kthr);
             }
             if constexpr (sizeof(W) == 1) acc >>= 3;
             else if constexpr (sizeof(W) == 2) acc >>= 4;
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(256) k_union_linear(const uint32_t* __restrict
                     const uint32_t v = static_cast<uint32_t>(cell[i < MAXR ? i : 0][j]);
                     m = v > m ? v : m;
                 }
-                acc += m < c.k;
+                acc += m < kthr;
             }
         }
 #pragma unroll

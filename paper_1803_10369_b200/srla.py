@@ -58,7 +58,8 @@ class CTiming(C.Structure):
     _fields_ = [("scan_kernel_ms", C.c_double), ("scan_kernel_launches", C.c_uint64),
                 ("scan_kernel_records", C.c_uint64), ("end_slice_device_ms", C.c_double),
                 ("end_slice_wall_ms", C.c_double), ("last_end_slice_device_ms", C.c_double),
-                ("last_end_slice_wall_ms", C.c_double), ("end_slices", C.c_uint64)]
+                ("last_end_slice_wall_ms", C.c_double), ("end_slices", C.c_uint64),
+                ("order_wall_ms", C.c_double), ("report_wall_ms", C.c_double), ("slide_wall_ms", C.c_double)]
 
 
 class CPlant(C.Structure):

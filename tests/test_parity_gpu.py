@@ -39,6 +39,19 @@ def test_engine_matches_reference_golden(gpu, oracle, name):
     assert msg is None, msg
 
 
+@pytest.mark.parametrize("name", [n for n in sorted(S.SCENARIOS) if S.SCENARIOS[n][0].rows <= 4])
+def test_binned_marks_match_reference_golden(gpu, oracle, name, monkeypatch):
+    """Same goldens with the binned linear-mark path forced on (~8 regions,
+    tiny bins so the overflow-to-direct-mark path runs too)."""
+    monkeypatch.setenv("SRLA_FORCE_BINS", "1")
+    g = json.load(open(os.path.join(GOLD, f"{name}.json")))
+    cfg, _ = S.SCENARIOS[name]
+    slices = GF.scenario_slices(name, oracle)
+    got = GF.run_flow(GF.EngineBackend(engine(cfg)), cfg, slices)
+    msg = GF.compare(g["slices"], got)
+    assert msg is None, msg
+
+
 def _oracle_backend(oracle, cfg):
     b = GF.CheckerBackend.__new__(GF.CheckerBackend)
     from oracle.pyoracle import SeaConfig

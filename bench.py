@@ -217,20 +217,10 @@ def run_engine(args):
     rep_cap = 1 << 22
     rep_buf = np.empty(rep_cap, srla.ENTRY_DTYPE)
 
+    from paper_1803_10369_b200.shard import allgather_report as _allgather
+
     def allgather_report(entries):
-        if world == 1:
-            return entries
-        n = torch.tensor([len(entries)], device="cuda")
-        counts = [torch.zeros_like(n) for _ in range(world)]
-        dist.all_gather(counts, n)
-        mx = int(max(c.item() for c in counts))
-        pad = np.zeros(mx, srla.ENTRY_DTYPE)
-        pad[: len(entries)] = entries
-        t = torch.from_numpy(pad.view(np.uint8)).cuda()
-        outs = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(outs, t)
-        merged = np.concatenate([o.cpu().numpy().view(srla.ENTRY_DTYPE)[: int(c.item())] for o, c in zip(outs, counts)])
-        return merged[np.argsort(merged["host"], kind="stable")]
+        return entries if world == 1 else _allgather(entries, dist, torch.device("cuda", local))
 
     def step(sid, host=None):
         recs = host[sid % len(host)] if host is not None else slices[sid % nres]

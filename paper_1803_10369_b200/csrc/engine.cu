@@ -132,7 +132,11 @@ struct Engine {
     // binned linear marks (scan_binned.cuh), for tables larger than L2
     bool use_bins = false;
     BinCfg bcfg{};
-    DevBuf<uint32_t> bins, bin_count;
+    DevBuf<uint32_t> bins, bin_count, tile_prefix, fine_count;
+    DevBuf<uint16_t> fine_bins;
+    FineCfg fcfg{};
+    bool bulk_ok = false;
+    uint32_t bulk_end = 0;
     PinBuf<uint32_t> pin_bc;
     uint64_t pending_entries = 0;
     bool prefetch_next = false;  // bulk-prefetch region r+1 while applying r (measured slower; off)
@@ -322,31 +326,55 @@ struct Engine {
         const char* force = std::getenv("SRLA_FORCE_BINS");     // exercise the binned path on small tables (tests)
         const bool forced = force && force[0] == '1';
         if (cfg.rows > kBinRows || (direct && direct[0] == '1')) return;
-        if (!forced && total_words * wb < (256ull << 20)) return;
+        const bool small = total_words * wb < (256ull << 20);
+        if (!forced && small) return;
         uint32_t shift = 0;
-        const char* rmb = std::getenv("SRLA_REGION_MB");  // tuning knob; 32 MB measured best (tools/applybench.cu)
-        const uint64_t region_bytes = (rmb ? std::max(1, std::atoi(rmb)) : 32) * (1ull << 20);
-        while ((1ull << (shift + 1)) * wb <= region_bytes) ++shift;
-        const char* pf = std::getenv("SRLA_PREFETCH");
-        prefetch_next = pf && pf[0] == '1';
+        while ((1ull << (shift + 1)) * wb <= (32ull << 20)) ++shift;  // 32 MB coarse regions
         if (forced)
-            while (shift > 2 && (total_words >> shift) < 8) --shift;  // ~8 regions even for tiny tables
+            while (shift > 4 && (total_words >> shift) < 8) --shift;  // ~8 regions even for tiny tables
         while ((total_words >> shift) >= kMaxRegions) ++shift;
         bcfg.region_shift = shift;
         bcfg.nregions = static_cast<uint32_t>((total_words + (1ull << shift) - 1) >> shift);
-        const uint64_t total_cap = forced && total_words * wb < (256ull << 20) ? (1ull << 16) : (3ull << 28);
-        bcfg.cap = static_cast<uint32_t>(std::min<uint64_t>(total_cap / bcfg.nregions, 0xFFFFFFF0ull)) & ~3u;
+        const uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);
+        bcfg.cap = static_cast<uint32_t>(std::min<uint64_t>(coarse_total / bcfg.nregions, 0xFFFFFFF0ull)) & ~3u;
         bins.ensure(uint64_t(bcfg.cap) * bcfg.nregions);
         bin_count.ensure(bcfg.nregions);
-        pin_bc.ensure(bcfg.nregions);
+        pin_bc.ensure(2 * bcfg.nregions + 2);
+        tile_prefix.ensure(2 * bcfg.nregions + 2);
         CK(cudaMemsetAsync(bin_count.p, 0, bcfg.nregions * sizeof(uint32_t), st));
         bcfg.bins = bins.p;
         bcfg.count = bin_count.p;
+        // fine 64 KB slices (u16 offsets), at most kMaxRegions per region
+        uint32_t fs = 0;
+        while ((1ull << (fs + 1)) * wb <= (32ull << 10)) ++fs;  // 32 KB: two buffers per block
+        fs = std::min(fs, shift);
+        if (forced && small) fs = std::max<uint32_t>(std::min<uint32_t>(shift, 4), shift > 3 ? shift - 3 : 0);
+        while (shift - fs > 10) ++fs;
+        fcfg.shift = fs;
+        fcfg.per_region = 1u << (shift - fs);
+        fcfg.nfine = static_cast<uint32_t>((total_words + (1ull << fs) - 1) >> fs);
+        fcfg.cap = static_cast<uint32_t>(std::max<uint64_t>(64, (coarse_total * 3 / 2 / fcfg.nfine + 7) & ~7ull));
+        fine_bins.ensure(uint64_t(fcfg.nfine) * fcfg.cap);
+        fine_count.ensure(fcfg.nfine);
+        fcfg.bins = fine_bins.p;
+        fcfg.count = fine_count.p;
+        CK(cudaMemsetAsync(fine_count.p, 0, fine_count.cap * sizeof(uint32_t), st));
+        const int smem = static_cast<int>((1ull << fs) * wb);
+        with_w([&](auto w) {
+            using W = decltype(w);
+            CK(cudaFuncSetAttribute(k_slice_apply<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(smem, 16)));
+            CK(cudaFuncSetAttribute(k_slice_apply_bulk<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(2 * smem, 32)));
+        });
+        // bulk (TMA) slices need 16-byte slices and rows at least one slice long
+        const uint64_t slice_words = 1ull << fs;
+        bulk_ok = (slice_words * wb) % 16 == 0 && (lin_words * wb) % 16 == 0 && lin_words >= slice_words;
+        bulk_end = (total_words % slice_words) * wb % 16 == 0 ? fcfg.nfine : fcfg.nfine - 1;
+        if (total_words % slice_words) bulk_end = fcfg.nfine - 1;  // partial last slice: plain kernel
         use_bins = true;
     }
 
     // Age (and optionally count) linear words [w0, w1) — split at row
-    // boundaries so each piece counts into its own row.
+    // boundaries so each piece counts into its own row (non-binned tables).
     template <typename W>
     void count_age_range(uint64_t w0, uint64_t w1, bool count) {
         while (w0 < w1) {
@@ -360,43 +388,60 @@ struct Engine {
         }
     }
 
-    // Apply pending linear marks one L2-resident region at a time. mode 0:
-    // apply only; 1: apply then age each region while it is still in L2;
-    // 2: apply, count active (into d_counts) and age. Modes 1/2 cover the
-    // whole table (regions without pending marks are aged too).
+    // Apply pending linear marks. mode 0: apply only (slices without marks
+    // untouched); 1: apply + age the whole table; 2: apply + count active per
+    // row into d_counts (pre-age) + age. One streaming pass over the table.
     void flush_linear(int mode = 0) {
         if (!use_bins) return;
         if (pending_entries == 0 && mode == 0) return;
-        if (pending_entries) {
-            CK(cudaMemcpyAsync(pin_bc.p, bin_count.p, bcfg.nregions * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-        } else {
-            std::memset(pin_bc.p, 0, bcfg.nregions * sizeof(uint32_t));
-        }
         const uint64_t total = uint64_t(cfg.rows) * lin_words;
+        const uint32_t R = bcfg.nregions;
+        if (pending_entries) {
+            CK(cudaMemcpyAsync(pin_bc.p, bin_count.p, R * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            // per-region entry counts (clamped: overflow was applied directly) and tile prefix
+            uint32_t* n_r = pin_bc.p + R + 1;
+            uint32_t* prefix = pin_bc.p;  // reuse: prefix[0..R]
+            std::vector<uint32_t> cnt(pin_bc.p, pin_bc.p + R);
+            uint32_t run = 0;
+            for (uint32_t r = 0; r < R; ++r) {
+                prefix[r] = run;
+                n_r[r] = std::min(cnt[r], bcfg.cap);
+                run += (n_r[r] + kSplitTile - 1) / kSplitTile;
+            }
+            prefix[R] = run;
+            CK(cudaMemcpyAsync(tile_prefix.p, pin_bc.p, (2 * R + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            if (run) {
+                with_w([&](auto w) {
+                    using W = decltype(w);
+                    k_split<W><<<std::min<uint32_t>(run, sms * 8), kSplitThreads, 0, st>>>(
+                        bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg,
+                        static_cast<W*>(d_lin));
+                });
+                check_launch();
+                launched();
+            }
+        }
         with_w([&](auto w) {
             using W = decltype(w);
-            const uint8_t* lin8 = static_cast<const uint8_t*>(d_lin);
-            auto region_bytes = [&](uint32_t r) {
-                const uint64_t a = uint64_t(r) << bcfg.region_shift;
-                return (std::min(total, uint64_t(r + 1) << bcfg.region_shift) - a) * sizeof(W);
-            };
-            for (uint32_t r = 0; r < bcfg.nregions; ++r) {
-                const uint32_t m = std::min(pin_bc.p[r], bcfg.cap);
-                const bool more = prefetch_next && r + 1 < bcfg.nregions;
-                const uint8_t* next = more ? lin8 + ((uint64_t(r + 1) << bcfg.region_shift) * sizeof(W)) : nullptr;
-                if (m || more) {
-                    k_apply_bins<W><<<blocks((m + 3) / 4 + 1, 256, 8), 256, 0, st>>>(
-                        static_cast<W*>(d_lin), bins.p, bcfg.cap, r, m, bcfg.region_shift, next,
-                        more ? region_bytes(r + 1) : 0);
-                    check_launch();
-                    launched();
-                }
-                if (mode) count_age_range<W>(uint64_t(r) << bcfg.region_shift,
-                                             std::min(total, uint64_t(r + 1) << bcfg.region_shift), mode == 2);
+            const size_t smem = (1ull << fcfg.shift) * sizeof(W);
+            uint32_t begin = 0;
+            if (bulk_ok && bulk_end) {
+                k_slice_apply_bulk<W><<<std::min<uint32_t>(bulk_end, sms * 3), 256, 2 * smem, st>>>(
+                    static_cast<W*>(d_lin), lin_words, fcfg, bulk_end, mode, cfg.window, dc.expired, d_counts.p);
+                check_launch();
+                launched();
+                begin = bulk_end;
+            }
+            if (begin < fcfg.nfine) {
+                k_slice_apply<W><<<std::min<uint32_t>(fcfg.nfine - begin, sms * 3), 256, smem, st>>>(
+                    static_cast<W*>(d_lin), total, lin_words, fcfg, begin, mode, cfg.window, dc.expired, d_counts.p);
+                check_launch();
+                launched();
             }
         });
-        if (pending_entries) CK(cudaMemsetAsync(bin_count.p, 0, bcfg.nregions * sizeof(uint32_t), st));
+        CK(cudaMemsetAsync(fine_count.p, 0, fcfg.nfine * sizeof(uint32_t), st));
+        if (pending_entries) CK(cudaMemsetAsync(bin_count.p, 0, R * sizeof(uint32_t), st));
         pending_entries = 0;
     }
 

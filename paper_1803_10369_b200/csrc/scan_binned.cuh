@@ -7,10 +7,11 @@
 // store 0) commute with each other and with every other hot-path step except
 // reads of the linear table, so K1 only *bins* them: a block multi-split by
 // table region (64 MB slabs) with one global reservation per region per tile
-// and coalesced bin writes. The apply pass then replays one region at a time
-// while it is L2-resident, so each touched sector costs one DRAM read and one
-// write per flush instead of one of each per mark. Any reader of the linear
-// table flushes first (Engine::flush_linear).
+// and coalesced bin writes. At flush time the region bins are split into
+// 64 KB table slices and each slice is applied in shared memory (below), so
+// the table streams through HBM once per flush instead of one sector
+// read-modify-write per mark. Any reader of the linear table flushes first
+// (Engine::flush_linear).
 #pragma once
 
 #include "common.cuh"
@@ -186,56 +187,6 @@ __global__ void __launch_bounds__(kBinThreads) k_scan_bin(const uint32_t* __rest
     }
 }
 
-// Stream `bytes` starting at p into L2 (TMA bulk prefetch, no registers).
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// Prefetch [p, p+bytes) into L2, one 64 KB piece per thread of the grid
-// (16-byte aligned pieces; the tail rounds down).
-__device__ __forceinline__ void grid_prefetch_l2(const uint8_t* p, uint64_t bytes) {
-    if (reinterpret_cast<uintptr_t>(p) & 15) return;  // bulk copies need 16-byte alignment
-    const uint64_t piece = 64ull << 10;
-    const uint64_t n = bytes / piece;
-    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
-    for (uint64_t i = tid; i < n; i += stride) prefetch_l2(p + i * piece, static_cast<uint32_t>(piece));
-    const uint64_t tail = (bytes - n * piece) & ~15ull;
-    if (tid == 0 && tail) prefetch_l2(p + n * piece, static_cast<uint32_t>(tail));
-}
-
-// Apply one region's pending marks while the region is L2-resident; the
-// region itself was prefetched by the previous launch, and this launch
-// prefetches the next region (next/next_bytes) so its DRAM reads stream
-// instead of missing one sector at a time.
-template <typename W>
-__global__ void __launch_bounds__(256) k_apply_bins(W* __restrict__ lin, const uint32_t* __restrict__ bins,
-                                                    uint32_t cap, uint32_t region, uint32_t n, uint32_t shift,
-                                                    const uint8_t* next, uint64_t next_bytes) {
-    if (next) grid_prefetch_l2(next, next_bytes);
-    W* base = lin + (static_cast<uint64_t>(region) << shift);
-    const uint32_t* e = bins + static_cast<uint64_t>(region) * cap;
-    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
-    const uint32_t nv = n / 4;
-    const uint4* v = reinterpret_cast<const uint4*>(e);
-    uint32_t q = tid;
-    for (; q + 3 * stride < nv; q += 4 * stride) {  // four 16-byte bin loads in flight per thread
-        const uint4 a = __ldcs(v + q), b = __ldcs(v + q + stride), c = __ldcs(v + q + 2 * stride),
-                    d = __ldcs(v + q + 3 * stride);
-        mark_word<W>(base, a.x); mark_word<W>(base, a.y); mark_word<W>(base, a.z); mark_word<W>(base, a.w);
-        mark_word<W>(base, b.x); mark_word<W>(base, b.y); mark_word<W>(base, b.z); mark_word<W>(base, b.w);
-        mark_word<W>(base, c.x); mark_word<W>(base, c.y); mark_word<W>(base, c.z); mark_word<W>(base, c.w);
-        mark_word<W>(base, d.x); mark_word<W>(base, d.y); mark_word<W>(base, d.z); mark_word<W>(base, d.w);
-    }
-    for (; q < nv; q += stride) {
-        const uint4 x = __ldcs(v + q);
-        mark_word<W>(base, x.x);
-        mark_word<W>(base, x.y);
-        mark_word<W>(base, x.z);
-        mark_word<W>(base, x.w);
-    }
-    for (uint32_t t = nv * 4 + tid; t < n; t += stride) mark_word<W>(base, __ldcs(e + t));
-}
-
 // Fused end-of-slice pass over a range of one linear row: optionally count
 // the recorders active in the window (count_active, recorders.hpp:119-129)
 // into counts[row], then age them (slide_recorders, recorders.hpp:113-116) in
@@ -290,6 +241,373 @@ __global__ void __launch_bounds__(256) k_count_age(W* __restrict__ base, uint64_
         for (uint32_t w = 0; w < blockDim.x / 32; ++w) s += part[w];
         if (s) atomicAdd(counter, s);
     }
+}
+
+}  // namespace srla
+
+namespace srla {
+
+// ----------------------------------------------------------------------------
+// Two-level apply: coarse region bins -> fine 64 KB slices -> shared memory.
+//
+// k_split re-bins each region's marks by 64 KB table slice (u16 offsets, one
+// block-level multi-split per 4096 entries); k_slice_apply then gives every
+// slice to one block, which loads it into shared memory with 16-byte coalesced
+// loads, applies its marks there, optionally counts active recorders and ages
+// them (the end-of-slice work), and writes the slice back coalesced. The table
+// is streamed once at full bandwidth instead of fetched one sector at a time.
+
+struct FineCfg {
+    uint16_t* bins;       // nfine x cap
+    uint32_t* count;      // per fine slice
+    uint32_t cap;
+    uint32_t shift;       // log2(words per fine slice)
+    uint32_t per_region;  // fine slices per coarse region = 2^(region_shift - shift)
+    uint32_t nfine;       // total fine slices covering the table
+};
+
+constexpr int kSplitThreads = 256;
+constexpr int kSplitPerThread = 16;
+constexpr int kSplitTile = kSplitThreads * kSplitPerThread;
+
+template <typename W>
+__global__ void __launch_bounds__(kSplitThreads) k_split(const uint32_t* __restrict__ coarse, uint32_t coarse_cap,
+                                                         const uint32_t* __restrict__ tile_prefix,
+                                                         const uint32_t* __restrict__ coarse_n, uint32_t nregions,
+                                                         uint32_t region_shift, FineCfg f, W* __restrict__ lin) {
+    __shared__ uint32_t s_cnt[kMaxRegions];
+    __shared__ uint32_t s_lbase[kMaxRegions];
+    __shared__ uint32_t s_gbase[kMaxRegions];
+    __shared__ uint16_t s_off[kSplitTile];
+    __shared__ uint16_t s_fine[kSplitTile];
+    __shared__ uint32_t s_warp[kSplitThreads / 32];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t total_tiles = tile_prefix[nregions];
+    const uint32_t fmask = (1u << f.shift) - 1u;
+    const uint32_t per_thread = (f.per_region + kSplitThreads - 1) / kSplitThreads;
+    for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        uint32_t lo = 0, hi = nregions;  // region r with tile_prefix[r] <= t < tile_prefix[r+1]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (tile_prefix[mid] <= t) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t r = lo;
+        const uint32_t begin = (t - tile_prefix[r]) * kSplitTile;
+        const uint32_t n = min(coarse_n[r] - begin, static_cast<uint32_t>(kSplitTile));
+        const uint32_t* src = coarse + static_cast<uint64_t>(r) * coarse_cap + begin;
+        for (uint32_t i = tid; i < f.per_region; i += kSplitThreads) s_cnt[i] = 0;
+        __syncthreads();
+        uint32_t off[kSplitPerThread], rank[kSplitPerThread];
+#pragma unroll
+        for (int k = 0; k < kSplitPerThread; ++k) {
+            const uint32_t i = k * kSplitThreads + tid;
+            if (i < n) {
+                off[k] = __ldcs(src + i);
+                rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
+            }
+        }
+        __syncthreads();
+        uint32_t mine = 0;
+        const uint32_t b0 = tid * per_thread;
+        for (uint32_t b = b0; b < min(b0 + per_thread, f.per_region); ++b) mine += s_cnt[b];
+        uint32_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += v;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        uint32_t run = incl - mine;
+        for (uint32_t w2 = 0; w2 < warp; ++w2) run += s_warp[w2];
+        const uint32_t fine0 = r * f.per_region;
+        for (uint32_t b = b0; b < min(b0 + per_thread, f.per_region); ++b) {
+            const uint32_t cn = s_cnt[b];
+            s_lbase[b] = run;
+            if (cn) s_gbase[b] = atomicAdd(f.count + fine0 + b, cn);
+            run += cn;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kSplitPerThread; ++k) {
+            const uint32_t i = k * kSplitThreads + tid;
+            if (i < n) {
+                const uint32_t b = off[k] >> f.shift;
+                const uint32_t p = s_lbase[b] + rank[k];
+                s_off[p] = static_cast<uint16_t>(off[k] & fmask);
+                s_fine[p] = static_cast<uint16_t>(b);
+            }
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < n; i += kSplitThreads) {
+            const uint32_t b = s_fine[i];
+            const uint32_t g = s_gbase[b] + (i - s_lbase[b]);
+            if (g < f.cap) {
+                f.bins[static_cast<uint64_t>(fine0 + b) * f.cap + g] = s_off[i];
+            } else {  // fine bin full: mark in place (marks commute)
+                mark_word<W>(lin + (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift),
+                             s_off[i]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// mode 0: apply marks (slices without marks are skipped); 1: apply + age;
+// 2: apply + count active (counts[row], pre-age) + age.
+template <typename W>
+__global__ void __launch_bounds__(256) k_slice_apply(W* __restrict__ lin, uint64_t total_words, uint64_t row_words,
+                                                     FineCfg f, uint32_t f_begin, int mode, uint32_t k,
+                                                     uint32_t expired, unsigned long long* __restrict__ counts) {
+    extern __shared__ uint4 s_slice[];
+    W* sw = reinterpret_cast<W*>(s_slice);
+    const uint32_t tid = threadIdx.x;
+    const uint32_t kk = sizeof(W) == 1 ? k * 0x01010101u : sizeof(W) == 2 ? k * 0x00010001u : k;
+    const uint32_t ee = sizeof(W) == 1 ? expired * 0x01010101u : sizeof(W) == 2 ? expired * 0x00010001u : expired;
+    const uint32_t one = sizeof(W) == 1 ? 0x01010101u : sizeof(W) == 2 ? 0x00010001u : 1u;
+    auto age = [&](uint32_t x) -> uint32_t {
+        if constexpr (sizeof(W) == 1) return __vadd4(x, __vcmpne4(x, ee) & one);
+        else if constexpr (sizeof(W) == 2) return __vadd2(x, __vcmpne2(x, ee) & one);
+        else return x + (x != ee ? 1u : 0u);
+    };
+    __shared__ unsigned long long s_part[8];
+    // 16-byte vectors only when slices and rows are 16-byte aligned
+    const bool vec = ((row_words * sizeof(W)) & 15) == 0 && (((1ull << f.shift) * sizeof(W)) & 15) == 0;
+    for (uint32_t fb = f_begin + blockIdx.x; fb < f.nfine; fb += gridDim.x) {
+        const uint32_t n = min(f.count[fb], f.cap);
+        if (mode == 0 && n == 0) continue;
+        const uint64_t w0 = static_cast<uint64_t>(fb) << f.shift;
+        const uint32_t nw = static_cast<uint32_t>(min(static_cast<uint64_t>(1u << f.shift), total_words - w0));
+        const uint32_t nv = vec ? static_cast<uint32_t>((static_cast<uint64_t>(nw) * sizeof(W)) / 16) : 0u;
+        const uint32_t tail0 = nv * 16 / sizeof(W);
+        uint4* g = reinterpret_cast<uint4*>(lin + w0);
+        for (uint32_t q = tid; q < nv; q += blockDim.x) s_slice[q] = __ldcs(g + q);
+        for (uint32_t q = tail0 + tid; q < nw; q += blockDim.x) sw[q] = lin[w0 + q];
+        __syncthreads();
+        const uint16_t* e = f.bins + static_cast<uint64_t>(fb) * f.cap;
+        for (uint32_t i = tid; i < n; i += blockDim.x) sw[__ldcs(e + i)] = W(0);
+        __syncthreads();
+        if (mode == 0) {
+            for (uint32_t q = tid; q < nv; q += blockDim.x) __stcs(g + q, s_slice[q]);
+            for (uint32_t q = tail0 + tid; q < nw; q += blockDim.x) lin[w0 + q] = sw[q];
+            __syncthreads();
+            continue;
+        }
+        const uint64_t row_a = w0 / row_words, row_b = (w0 + nw - 1) / row_words;
+        unsigned long long acc_a = 0, acc_b = 0;
+        for (uint32_t q = tid; q < nv; q += blockDim.x) {
+            uint4 x = s_slice[q];
+            if (mode == 2) {
+                const uint32_t c = count_lt_word<W>(x.x, kk, k) + count_lt_word<W>(x.y, kk, k) +
+                                   count_lt_word<W>(x.z, kk, k) + count_lt_word<W>(x.w, kk, k);
+                if (row_a == row_b || (w0 + static_cast<uint64_t>(q) * 16 / sizeof(W)) / row_words == row_a) acc_a += c;
+                else acc_b += c;  // a 16-byte vector never straddles rows when row bytes % 16 == 0
+            }
+            x.x = age(x.x);
+            x.y = age(x.y);
+            x.z = age(x.z);
+            x.w = age(x.w);
+            __stcs(g + q, x);
+        }
+        if constexpr (sizeof(W) == 1) {
+            acc_a >>= 3;
+            acc_b >>= 3;
+        } else if constexpr (sizeof(W) == 2) {
+            acc_a >>= 4;
+            acc_b >>= 4;
+        }
+        for (uint32_t q = tail0 + tid; q < nw; q += blockDim.x) {
+            const W x = sw[q];
+            if (mode == 2 && static_cast<uint32_t>(x) < k) ((w0 + q) / row_words == row_a ? acc_a : acc_b) += 1;
+            lin[w0 + q] = static_cast<W>(x + (static_cast<uint32_t>(x) != expired ? 1 : 0));
+        }
+        if (mode == 2) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                acc_a += __shfl_xor_sync(0xFFFFFFFFu, acc_a, o);
+                acc_b += __shfl_xor_sync(0xFFFFFFFFu, acc_b, o);
+            }
+            if ((tid & 31) == 0) s_part[tid >> 5] = acc_a;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long s = 0;
+                for (uint32_t w = 0; w < blockDim.x / 32; ++w) s += s_part[w];
+                if (s) atomicAdd(counts + row_a, s);
+            }
+            __syncthreads();
+            if ((tid & 31) == 0) s_part[tid >> 5] = acc_b;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long s = 0;
+                for (uint32_t w = 0; w < blockDim.x / 32; ++w) s += s_part[w];
+                if (s) atomicAdd(counts + row_b, s);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace srla
+
+namespace srla {
+
+// ---- bulk-copy (TMA engine) + mbarrier helpers, sm_90+/sm_100a PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// global -> shared, completion counted on the mbarrier in bytes
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst_smem)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// shared -> global, tracked by the issuing thread's bulk groups
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Same contract as k_slice_apply for slices [f_begin, f_end) whose bytes are
+// a multiple of 16 and 16-byte aligned (and rows are 16-byte multiples):
+// each block walks its slices through two shared-memory buffers; slice i+1 is
+// bulk-loaded while slice i is marked, counted and aged, and each finished
+// slice is bulk-stored back — the table streams through HBM once.
+template <typename W>
+__global__ void __launch_bounds__(256) k_slice_apply_bulk(W* __restrict__ lin, uint64_t row_words, FineCfg f,
+                                                          uint32_t f_end, int mode, uint32_t k, uint32_t expired,
+                                                          unsigned long long* __restrict__ counts) {
+    extern __shared__ __align__(128) uint8_t s_raw[];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ unsigned long long s_part[2][8];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t slice_bytes = (1u << f.shift) * sizeof(W);
+    uint8_t* buf[2] = {s_raw, s_raw + slice_bytes};
+    const uint32_t kk = sizeof(W) == 1 ? k * 0x01010101u : sizeof(W) == 2 ? k * 0x00010001u : k;
+    const uint32_t ee = sizeof(W) == 1 ? expired * 0x01010101u : sizeof(W) == 2 ? expired * 0x00010001u : expired;
+    const uint32_t one = sizeof(W) == 1 ? 0x01010101u : sizeof(W) == 2 ? 0x00010001u : 1u;
+    auto age = [&](uint32_t x) -> uint32_t {
+        if constexpr (sizeof(W) == 1) return __vadd4(x, __vcmpne4(x, ee) & one);
+        else if constexpr (sizeof(W) == 2) return __vadd2(x, __vcmpne2(x, ee) & one);
+        else return x + (x != ee ? 1u : 0u);
+    };
+    // slices of this block: blockIdx.x + j*gridDim.x, skipping mark-free ones in mode 0
+    auto next_slice = [&](uint32_t from) -> uint32_t {
+        for (uint32_t fb = from; fb < f_end; fb += gridDim.x)
+            if (mode != 0 || f.count[fb] != 0) return fb;
+        return f_end;
+    };
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+    }
+    __syncthreads();
+    uint32_t cur = next_slice(blockIdx.x);
+    if (tid == 0 && cur < f_end) {
+        mbar_expect_tx(&s_bar[0], slice_bytes);
+        bulk_load(buf[0], lin + (static_cast<uint64_t>(cur) << f.shift), slice_bytes, &s_bar[0]);
+    }
+    for (uint32_t i = 0; cur < f_end; ++i) {
+        const uint32_t b = i & 1u;
+        const uint32_t nxt = next_slice(cur + gridDim.x);
+        if (tid == 0 && nxt < f_end) {
+            bulk_wait_read_all();  // the other buffer's store (slice i-1) has left shared memory
+            mbar_expect_tx(&s_bar[b ^ 1u], slice_bytes);
+            bulk_load(buf[b ^ 1u], lin + (static_cast<uint64_t>(nxt) << f.shift), slice_bytes, &s_bar[b ^ 1u]);
+        }
+        mbar_wait(&s_bar[b], (i >> 1) & 1u);
+        W* sw = reinterpret_cast<W*>(buf[b]);
+        const uint32_t n = min(f.count[cur], f.cap);
+        const uint16_t* e = f.bins + static_cast<uint64_t>(cur) * f.cap;
+        const uint4* ev = reinterpret_cast<const uint4*>(e);
+        for (uint32_t q = tid; q < n / 8; q += blockDim.x) {
+            const uint4 x = __ldcs(ev + q);
+            sw[x.x & 0xFFFF] = W(0); sw[x.x >> 16] = W(0);
+            sw[x.y & 0xFFFF] = W(0); sw[x.y >> 16] = W(0);
+            sw[x.z & 0xFFFF] = W(0); sw[x.z >> 16] = W(0);
+            sw[x.w & 0xFFFF] = W(0); sw[x.w >> 16] = W(0);
+        }
+        for (uint32_t q = (n / 8) * 8 + tid; q < n; q += blockDim.x) sw[e[q]] = W(0);
+        __syncthreads();
+        if (mode != 0) {
+            const uint64_t w0 = static_cast<uint64_t>(cur) << f.shift;
+            const uint64_t row_a = w0 / row_words;
+            const uint64_t split = (row_a + 1) * row_words;  // first word of the next row
+            unsigned long long acc_a = 0, acc_b = 0;
+            uint4* sv = reinterpret_cast<uint4*>(buf[b]);
+            const uint32_t nv = slice_bytes / 16;
+            for (uint32_t q = tid; q < nv; q += blockDim.x) {
+                uint4 x = sv[q];
+                if (mode == 2) {
+                    const uint32_t c = count_lt_word<W>(x.x, kk, k) + count_lt_word<W>(x.y, kk, k) +
+                                       count_lt_word<W>(x.z, kk, k) + count_lt_word<W>(x.w, kk, k);
+                    if (w0 + static_cast<uint64_t>(q) * (16 / sizeof(W)) < split) acc_a += c;
+                    else acc_b += c;
+                }
+                x.x = age(x.x);
+                x.y = age(x.y);
+                x.z = age(x.z);
+                x.w = age(x.w);
+                sv[q] = x;
+            }
+            if (mode == 2) {
+                if constexpr (sizeof(W) == 1) {
+                    acc_a >>= 3;
+                    acc_b >>= 3;
+                } else if constexpr (sizeof(W) == 2) {
+                    acc_a >>= 4;
+                    acc_b >>= 4;
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    acc_a += __shfl_xor_sync(0xFFFFFFFFu, acc_a, o);
+                    acc_b += __shfl_xor_sync(0xFFFFFFFFu, acc_b, o);
+                }
+                if ((tid & 31) == 0) {
+                    s_part[0][tid >> 5] = acc_a;
+                    s_part[1][tid >> 5] = acc_b;
+                }
+            }
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (mode == 2 && tid == 0) {
+                unsigned long long sa = 0, sb = 0;
+                for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+                    sa += s_part[0][w];
+                    sb += s_part[1][w];
+                }
+                if (sa) atomicAdd(counts + row_a, sa);
+                if (sb) atomicAdd(counts + row_a + 1, sb);
+            }
+        } else {
+            fence_proxy_async_smem();
+            __syncthreads();
+        }
+        if (tid == 0) bulk_store(lin + (static_cast<uint64_t>(cur) << f.shift), buf[b], slice_bytes);
+        cur = nxt;
+    }
+    if (tid == 0) bulk_wait_all();
 }
 
 }  // namespace srla

@@ -296,21 +296,33 @@ def run_engine(args):
         if d.get("dram_bytes_per_record"):
             traffic = d["dram_bytes_per_record"] * recs_per_launch
 
-    # end to end through the public API with host buffers (pinned), H2D inside
+    # end to end through the public API with host buffers (pinned), H2D inside:
+    # scan_batch(host) + end_slice_async/wait, so a slice's host->device copies
+    # overlap the previous slice's end-of-slice work
     e2e = None
     if not args.no_e2e:
         nh = min(2, nres)
         host = [slices[i].cpu().pin_memory().numpy().view(np.uint32) for i in range(nh)]
         h2d = sum(h.nbytes for h in host) / nh
+        bufs = [np.empty(rep_cap, srla.ENTRY_DTYPE) for _ in range(2)]
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         d2h = 0
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            _, n = step(sid, host=host)
-            d2h += n * srla.ENTRY_DTYPE.itemsize
-            sid += 1
+        pending = None
+        for i in range(args.steps):
+            eng.scan(host[(sid + i) % nh])
+            if pending is not None:
+                n, _ = eng.end_slice_wait()
+                allgather_report(bufs[pending][:n])
+                d2h += n * srla.ENTRY_DTYPE.itemsize
+            eng.end_slice_async(sid + i, bufs[i % 2])
+            pending = i % 2
+        n, _ = eng.end_slice_wait()
+        allgather_report(bufs[pending][:n])
+        d2h += n * srla.ENTRY_DTYPE.itemsize
+        sid += args.steps
         eng.synchronize()
         if dist:
             dist.barrier()
@@ -320,7 +332,8 @@ def run_engine(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = t.item()
         e2e = {"value": packets / el, "unit": "packets/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h / args.steps)}
+               "d2h_bytes_per_step": int(d2h / args.steps),
+               "api": "srla_scan_batch(host, pinned) + srla_end_slice_async/wait"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

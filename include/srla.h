@@ -136,6 +136,15 @@ srla_status srla_slide(srla_engine* e, uint64_t* n_retained);
 srla_status srla_end_slice(srla_engine* e, uint64_t slice_id, int want_report, srla_entry* out,
                            uint64_t cap, uint64_t* n_out, uint64_t* n_retained);
 
+/* The same as srla_end_slice, split in two: _async starts the end-of-slice
+ * work and returns; a following srla_scan_batch with host records stages its
+ * host->device copies while it runs (the copies are the bound of a host-fed
+ * scan). `out` must stay valid until srla_end_slice_wait, which returns the
+ * report size and retained-candidate count. Any other call waits for it too. */
+srla_status srla_end_slice_async(srla_engine* e, uint64_t slice_id, int want_report, srla_entry* out,
+                                 uint64_t cap);
+srla_status srla_end_slice_wait(srla_engine* e, uint64_t* n_out, uint64_t* n_retained);
+
 /* union_rough_weight / union_linear_weight (sea.hpp:219-243) per host; either
  * output may be NULL. */
 srla_status srla_union_weights(srla_engine* e, const uint32_t* hosts, uint64_t n,

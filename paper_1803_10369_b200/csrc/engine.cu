@@ -124,6 +124,14 @@ struct Engine {
     srla_timing timing{};
     PinBuf<unsigned long long> pin_counts;
     std::vector<uint32_t> host_pushed;
+    // asynchronous end-of-slice (srla_end_slice_async / srla_end_slice_wait)
+    std::thread eos_thread;
+    struct EosResult {
+        bool pending = false;
+        srla_status code = SRLA_OK;
+        std::string msg;
+        uint64_t n = 0, nret = 0;
+    } eos;
     std::vector<double> lut_est;
     std::vector<uint8_t> lut_has, lut_sup;
     bool collect_pushed = false;
@@ -195,6 +203,7 @@ struct Engine {
     }
 
     ~Engine() {
+        if (eos_thread.joinable()) eos_thread.join();
         if (st) cudaStreamSynchronize(st);
         if (d_lin) cudaFree(d_lin);
         if (d_rough) cudaFree(d_rough);
@@ -604,9 +613,60 @@ struct Engine {
         });
     }
 
+    void join_eos() {
+        if (eos_thread.joinable()) eos_thread.join();
+    }
+
+    // Run end_slice on a worker thread; the caller's next scan_batch stages its
+    // host->device copies meanwhile. `out` must stay valid until the wait.
+    void end_slice_async(uint64_t slice_id, bool want_report, srla_entry* out, uint64_t cap) {
+        join_eos();
+        if (eos.pending) throw Error(SRLA_E_INVALID, "previous srla_end_slice_async not collected");
+        const bool due = want_report && slice_id + 1 >= cfg.window;
+        if (due && (ncsip > cap || (!out && ncsip)))
+            throw Error(SRLA_E_CAPACITY, "report buffer holds " + std::to_string(cap) + " entries, " +
+                                             std::to_string(ncsip) + " needed");
+        eos = EosResult{};
+        eos.pending = true;
+        eos.n = due ? ncsip : 0;
+        eos_thread = std::thread([this, slice_id, want_report, out] {
+            try {
+                CK(cudaSetDevice(device));
+                timed_end_slice(slice_id, want_report, out);
+                eos.nret = ncsip;
+            } catch (const Error& x) {
+                eos.code = x.code;
+                eos.msg = x.what();
+            } catch (const std::exception& x) {
+                eos.code = SRLA_E_INTERNAL;
+                eos.msg = x.what();
+            }
+        });
+    }
+
+    void timed_end_slice(uint64_t slice_id, bool want_report, srla_entry* out) {
+        const auto w0 = std::chrono::steady_clock::now();
+        CK(cudaEventRecord(t_eos0, st));
+        end_slice(slice_id, want_report, out);
+        CK(cudaEventRecord(t_eos1, st));
+        CK(cudaEventSynchronize(t_eos1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, t_eos0, t_eos1));
+        timing.end_slice_device_ms += ms;
+        timing.last_end_slice_device_ms = ms;
+        timing.last_end_slice_wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+        timing.end_slice_wall_ms += timing.last_end_slice_wall_ms;
+        timing.end_slices += 1;
+    }
+
     void scan_batch(const srla_record* recs, uint64_t n, int on_device) {
-        if (!n) return;
+        if (!n) {
+            join_eos();
+            return;
+        }
         if (on_device) {
+            join_eos();
             const uint32_t* base = reinterpret_cast<const uint32_t*>(recs);
             for (uint64_t o = 0; o < n; o += kChunk)
                 scan_chunk(base + 3 * o, static_cast<uint32_t>(std::min<uint64_t>(kChunk, n - o)));
@@ -642,8 +702,10 @@ struct Engine {
             CK(cudaEventRecord(ev_copied[b], cs));
         };
         issue(0);
+        if (nchunks > 1) issue(1);
+        join_eos();  // copies above overlap a pending asynchronous end-of-slice
         for (uint64_t j = 0; j < nchunks; ++j) {
-            if (j + 1 < nchunks) issue(j + 1);
+            if (j >= 1 && j + 1 < nchunks) issue(j + 1);
             const int b = static_cast<int>(j & 1);
             CK(cudaStreamWaitEvent(st, ev_copied[b], 0));
             scan_chunk(dstage[b].p, len(j));
@@ -960,9 +1022,10 @@ srla_status guard(Fn&& fn) {
     }
 }
 
-srla::Engine& E(srla_engine* e) {
+srla::Engine& E(srla_engine* e, bool join = true) {
     if (!e || !e->impl) throw srla::Error(SRLA_E_INVALID, "null engine");
     CK(cudaSetDevice(e->impl->device));
+    if (join) e->impl->join_eos();
     return *e->impl;
 }
 const srla::Engine& CE(const srla_engine* e) {
@@ -1035,7 +1098,7 @@ srla_status srla_scan_batch(srla_engine* e, const srla_record* recs, uint64_t n,
                             uint32_t* pushed, uint64_t cap, uint64_t* n_pushed) {
     return guard([&] {
         std::lock_guard<std::mutex> lk(e->mu);
-        auto& x = E(e);
+        auto& x = E(e, /*join=*/false);  // joins a pending async end-of-slice after staging copies
         if (n && !recs) throw srla::Error(SRLA_E_INVALID, "null records");
         x.collect_pushed = pushed != nullptr || n_pushed != nullptr;
         x.host_pushed.clear();
@@ -1089,26 +1152,31 @@ srla_status srla_slide(srla_engine* e, uint64_t* n_retained) {
 
 srla_status srla_end_slice(srla_engine* e, uint64_t slice_id, int want_report, srla_entry* out,
                            uint64_t cap, uint64_t* n_out, uint64_t* n_retained) {
+    srla_status s = srla_end_slice_async(e, slice_id, want_report, out, cap);
+    if (s != SRLA_OK) {
+        if (s == SRLA_E_CAPACITY && n_out && e && e->impl) *n_out = e->impl->ncsip;
+        return s;
+    }
+    return srla_end_slice_wait(e, n_out, n_retained);
+}
+
+srla_status srla_end_slice_async(srla_engine* e, uint64_t slice_id, int want_report, srla_entry* out,
+                                 uint64_t cap) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        E(e).end_slice_async(slice_id, want_report != 0, out, cap);
+    });
+}
+
+srla_status srla_end_slice_wait(srla_engine* e, uint64_t* n_out, uint64_t* n_retained) {
     return guard([&] {
         std::lock_guard<std::mutex> lk(e->mu);
         auto& x = E(e);
-        const auto w0 = std::chrono::steady_clock::now();
-        CK(cudaEventRecord(x.t_eos0, x.st));
-        if (n_out) *n_out = 0;
-        const bool due = want_report && slice_id + 1 >= x.cfg.window;  // pipeline.hpp:121
-        if (due) check_capacity(x.ncsip, out, cap, n_out);
-        x.end_slice(slice_id, want_report != 0, out);
-        CK(cudaEventRecord(x.t_eos1, x.st));
-        CK(cudaEventSynchronize(x.t_eos1));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, x.t_eos0, x.t_eos1));
-        x.timing.end_slice_device_ms += ms;
-        x.timing.last_end_slice_device_ms = ms;
-        x.timing.last_end_slice_wall_ms =
-            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
-        x.timing.end_slice_wall_ms += x.timing.last_end_slice_wall_ms;
-        x.timing.end_slices += 1;
-        if (n_retained) *n_retained = x.ncsip;
+        if (!x.eos.pending) throw srla::Error(SRLA_E_INVALID, "no srla_end_slice_async pending");
+        x.eos.pending = false;
+        if (x.eos.code != SRLA_OK) throw srla::Error(x.eos.code, x.eos.msg);
+        if (n_out) *n_out = x.eos.n;
+        if (n_retained) *n_retained = x.eos.nret;
     });
 }
 

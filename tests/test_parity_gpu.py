@@ -270,3 +270,36 @@ def test_device_generator_byte_identical(gpu, oracle):
         got = gen.slice_tensor(2).cpu().numpy().view(np.uint32)
         torch.cuda.synchronize()
         assert np.array_equal(got, want[2])
+
+
+@pytest.mark.parametrize("name", ["pipeline_small_3000", "c1_shape", "drift_evict"])
+def test_async_end_slice_matches_sync(gpu, oracle, name):
+    """srla_end_slice_async + the next slice's host scan (copies overlapping the
+    end-of-slice work) give the reference pipeline's reports and state."""
+    from oracle.pyoracle import SeaConfig as OCfg
+    from paper_1803_10369_b200.srla import ENTRY_DTYPE
+    cfg, _ = S.SCENARIOS[name]
+    slices = GF.scenario_slices(name, oracle)
+    pipe = oracle.pipeline(OCfg(**cfg.as_dict()))
+    want = [pipe.process_slice(s, r, True) for s, r in enumerate(slices)]
+    e = engine(cfg)
+    bufs = [np.zeros(200000, ENTRY_DTYPE) for _ in range(2)]
+    got = []
+    for s, recs in enumerate(slices):
+        e.scan(recs)
+        if s:
+            n, _ = e.end_slice_wait()
+            got.append(bufs[(s - 1) % 2][:n].copy() if s - 1 + 1 >= cfg.window else None)
+        e.end_slice_async(s, bufs[s % 2])
+    n, _ = e.end_slice_wait()
+    got.append(bufs[(len(slices) - 1) % 2][:n].copy() if len(slices) >= cfg.window else None)
+    for s, (g, w) in enumerate(zip(got, want)):
+        if w is None:
+            assert g is None or len(g) == 0
+            continue
+        assert np.array_equal(g["host"], w["host"]), s
+        assert np.array_equal(g["union_weight"], w["weight"]), s
+        assert np.array_equal(g["estimate"].view(np.uint64)[w["has_estimate"] == 1],
+                              w["estimate"].view(np.uint64)[w["has_estimate"] == 1]), s
+        assert np.array_equal(g["is_super"], w["is_super"]), s
+    assert np.array_equal(e.candidates(), pipe.candidates())

@@ -363,6 +363,7 @@ struct Engine {
         fcfg.per_region = 1u << (shift - fs);
         fcfg.nfine = static_cast<uint32_t>((total_words + (1ull << fs) - 1) >> fs);
         fcfg.cap = static_cast<uint32_t>(std::max<uint64_t>(64, (coarse_total * 3 / 2 / fcfg.nfine + 7) & ~7ull));
+        if (uint64_t(fcfg.cap) * fcfg.nfine >= (1ull << 32)) throw Error(SRLA_E_INTERNAL, "fine bin index overflow");
         fine_bins.ensure(uint64_t(fcfg.nfine) * fcfg.cap);
         fine_count.ensure(fcfg.nfine);
         fcfg.bins = fine_bins.p;

@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(kBinThreads) k_scan_bin(const uint32_t* __rest
                                                          uint32_t ev_cap, uint32_t* __restrict__ ev_count, int vec) {
     __shared__ uint32_t s_cnt[kMaxRegions];
     __shared__ uint32_t s_lbase[kMaxRegions];
-    __shared__ uint32_t s_gbase[kMaxRegions];
+    __shared__ uint32_t s_dst[kMaxRegions];  // first bin slot of this tile per region (nregions * cap < 2^32)
+    __shared__ uint16_t s_fit[kMaxRegions];  // entries of this tile that fit in the region's bin
     __shared__ uint32_t s_off[kBinEntries];
     __shared__ uint16_t s_reg[kBinEntries];
     __shared__ uint32_t s_warp[kBinThreads / 32];
@@ -156,7 +157,11 @@ __global__ void __launch_bounds__(kBinThreads) k_scan_bin(const uint32_t* __rest
         for (uint32_t r = r0; r < min(r0 + regs_per_thread, b.nregions); ++r) {
             const uint32_t cn = s_cnt[r];
             s_lbase[r] = run;
-            if (cn) s_gbase[r] = atomicAdd(b.count + r, cn);
+            if (cn) {
+                const uint32_t g = atomicAdd(b.count + r, cn);
+                s_dst[r] = r * b.cap + g;
+                s_fit[r] = static_cast<uint16_t>(g >= b.cap ? 0u : min(cn, b.cap - g));
+            }
             run += cn;
         }
         uint32_t total = 0;
@@ -176,9 +181,9 @@ __global__ void __launch_bounds__(kBinThreads) k_scan_bin(const uint32_t* __rest
 
         for (uint32_t idx = tid; idx < total; idx += kBinThreads) {
             const uint32_t r = s_reg[idx];
-            const uint32_t g = s_gbase[r] + (idx - s_lbase[r]);
-            if (g < b.cap) {
-                b.bins[static_cast<uint64_t>(r) * b.cap + g] = s_off[idx];
+            const uint32_t j = idx - s_lbase[r];
+            if (j < s_fit[r]) {
+                b.bins[s_dst[r] + j] = s_off[idx];
             } else {  // bin full: mark directly (marks commute)
                 mark_word<W>(lin + (static_cast<uint64_t>(r) << b.region_shift), s_off[idx]);
             }
@@ -266,10 +271,13 @@ struct FineCfg {
     uint32_t nfine;       // total fine slices covering the table
 };
 
-constexpr int kSplitThreads = 256;
+constexpr int kSplitThreads = 512;
 constexpr int kSplitPerThread = 16;
-constexpr int kSplitTile = kSplitThreads * kSplitPerThread;
+constexpr int kSplitTile = kSplitThreads * kSplitPerThread;  // 8192 entries
 
+// Re-bin coarse region bins by fine slice. One tile = 8192 consecutive entries
+// of one region: shared-memory counting sort by slice (ranks from shared
+// atomics), one global reservation per slice per tile, coalesced u16 writes.
 template <typename W>
 __global__ void __launch_bounds__(kSplitThreads) k_split(const uint32_t* __restrict__ coarse, uint32_t coarse_cap,
                                                          const uint32_t* __restrict__ tile_prefix,
@@ -277,9 +285,9 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const uint32_t* __restr
                                                          uint32_t region_shift, FineCfg f, W* __restrict__ lin) {
     __shared__ uint32_t s_cnt[kMaxRegions];
     __shared__ uint32_t s_lbase[kMaxRegions];
-    __shared__ uint32_t s_gbase[kMaxRegions];
-    __shared__ uint16_t s_off[kSplitTile];
-    __shared__ uint16_t s_fine[kSplitTile];
+    __shared__ uint16_t s_fit[kMaxRegions];
+    __shared__ uint32_t s_dst[kMaxRegions];    // nfine * cap < 2^32 by construction (Engine::setup_bins)
+    __shared__ uint32_t s_sorted[kSplitTile];  // (slice << 16) | offset within slice
     __shared__ uint32_t s_warp[kSplitThreads / 32];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t total_tiles = tile_prefix[nregions];
@@ -298,15 +306,26 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const uint32_t* __restr
         const uint32_t* src = coarse + static_cast<uint64_t>(r) * coarse_cap + begin;
         for (uint32_t i = tid; i < f.per_region; i += kSplitThreads) s_cnt[i] = 0;
         __syncthreads();
-        uint32_t off[kSplitPerThread], rank[kSplitPerThread];
+        uint32_t off[kSplitPerThread];
+        const uint32_t e0 = tid * kSplitPerThread;
+        if (e0 + kSplitPerThread <= n) {
+            const uint4* v = reinterpret_cast<const uint4*>(src + e0);
 #pragma unroll
-        for (int k = 0; k < kSplitPerThread; ++k) {
-            const uint32_t i = k * kSplitThreads + tid;
-            if (i < n) {
-                off[k] = __ldcs(src + i);
-                rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
+            for (int q = 0; q < kSplitPerThread / 4; ++q) {
+                const uint4 x = __ldcs(v + q);
+                off[4 * q] = x.x;
+                off[4 * q + 1] = x.y;
+                off[4 * q + 2] = x.z;
+                off[4 * q + 3] = x.w;
             }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kSplitPerThread; ++k) off[k] = e0 + k < n ? __ldcs(src + e0 + k) : 0xFFFFFFFFu;
         }
+        uint32_t rank[kSplitPerThread];
+#pragma unroll
+        for (int k = 0; k < kSplitPerThread; ++k)
+            if (off[k] != 0xFFFFFFFFu) rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
         __syncthreads();
         uint32_t mine = 0;
         const uint32_t b0 = tid * per_thread;
@@ -325,29 +344,30 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const uint32_t* __restr
         for (uint32_t b = b0; b < min(b0 + per_thread, f.per_region); ++b) {
             const uint32_t cn = s_cnt[b];
             s_lbase[b] = run;
-            if (cn) s_gbase[b] = atomicAdd(f.count + fine0 + b, cn);
+            if (cn) {
+                const uint32_t g = atomicAdd(f.count + fine0 + b, cn);
+                s_dst[b] = (fine0 + b) * f.cap + g;
+                s_fit[b] = static_cast<uint16_t>(g >= f.cap ? 0u : min(cn, f.cap - g));
+            }
             run += cn;
         }
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kSplitPerThread; ++k) {
-            const uint32_t i = k * kSplitThreads + tid;
-            if (i < n) {
+        for (int k = 0; k < kSplitPerThread; ++k)
+            if (off[k] != 0xFFFFFFFFu) {
                 const uint32_t b = off[k] >> f.shift;
-                const uint32_t p = s_lbase[b] + rank[k];
-                s_off[p] = static_cast<uint16_t>(off[k] & fmask);
-                s_fine[p] = static_cast<uint16_t>(b);
+                s_sorted[s_lbase[b] + rank[k]] = (b << 16) | (off[k] & fmask);
             }
-        }
         __syncthreads();
         for (uint32_t i = tid; i < n; i += kSplitThreads) {
-            const uint32_t b = s_fine[i];
-            const uint32_t g = s_gbase[b] + (i - s_lbase[b]);
-            if (g < f.cap) {
-                f.bins[static_cast<uint64_t>(fine0 + b) * f.cap + g] = s_off[i];
+            const uint32_t v = s_sorted[i];
+            const uint32_t b = v >> 16;
+            const uint32_t j = i - s_lbase[b];
+            if (j < s_fit[b]) {
+                f.bins[s_dst[b] + j] = static_cast<uint16_t>(v);
             } else {  // fine bin full: mark in place (marks commute)
                 mark_word<W>(lin + (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift),
-                             s_off[i]);
+                             v & 0xFFFFu);
             }
         }
         __syncthreads();

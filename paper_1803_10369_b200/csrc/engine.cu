@@ -51,7 +51,7 @@ struct DevBuf {
         if (n <= cap) return;
         if (p) CK(cudaFree(p));
         p = nullptr;
-        const size_t c = std::max<size_t>({n, cap + cap / 2, 256});
+        const size_t c = std::max<size_t>({n + n / 4, cap * 2, 256});
         CK(cudaMalloc(&p, c * sizeof(T)));
         cap = c;
     }
@@ -78,11 +78,13 @@ struct PinBuf {
     ~PinBuf() {
         if (p) cudaFreeHost(p);
     }
+    // pinned allocations cost milliseconds: grow geometrically (x2) so a
+    // candidate list that creeps up over the first window reallocates rarely
     void ensure(size_t n) {
         if (n <= cap) return;
         if (p) CK(cudaFreeHost(p));
         p = nullptr;
-        const size_t c = std::max<size_t>({n, cap + cap / 2, 256});
+        const size_t c = std::max<size_t>({n + n / 4, cap * 2, 4096});
         CK(cudaMallocHost(&p, c * sizeof(T)));
         cap = c;
     }
@@ -495,6 +497,7 @@ struct Engine {
             ev.ensure(3ull * ev_cap);
         }
         stats.sampled_events += n_ev;
+        trace("scan: K1");
         if (!n_ev) return;
         const auto w_order = std::chrono::steady_clock::now();
         struct OrderTimer {
@@ -511,6 +514,7 @@ struct Engine {
         check_launch();
         launched();
         const uint32_t X = read_ctr(1);
+        trace("scan: K2+K5");
         stats.crossings += X;
         if (!X) return;
 
@@ -524,6 +528,7 @@ struct Engine {
         check_launch();
         launched();
         const uint32_t Hn = read_ctr(2);
+        trace("scan: sort+first");
         stats.first_crossings += Hn;
         hps.ensure(Hn);
         cub_call([&](void* t, size_t& b) {
@@ -577,6 +582,7 @@ struct Engine {
                                               ctr.p + 3, static_cast<int>(Hn), st);
         });
         const uint32_t nf = read_ctr(3);
+        trace("scan: K4 resolve");
         stats.flagged += nf;
         if (nf) {
             k_serial<<<1, 32, 0, st>>>(flagged.p, nf, fmask.p, off.p, posof.p, skey.p, sval.p, towner.p, status.p, fl_ins.p);
@@ -600,11 +606,14 @@ struct Engine {
             CK(cudaStreamSynchronize(st));
             std::memcpy(host_pushed.data() + at, pin_hosts.p, np * sizeof(uint32_t));
         }
+        trace("scan: K4 set+select");
         append_candidates(pushed.p, np);
+        trace("scan: append");
     }
 
     void scan_chunk(const uint32_t* d_recs, uint32_t n) {
         if (!n) return;
+        trace(nullptr);
         stats.chunks++;
         stats.packets += n;
         with_w([&](auto w) {
@@ -612,6 +621,17 @@ struct Engine {
             if (cfg.rows <= 4) scan_chunk_t<W, 4>(d_recs, n);
             else scan_chunk_t<W, 64>(d_recs, n);
         });
+    }
+
+    // SRLA_TRACE=1: synchronise and print per-phase wall times (diagnostics only)
+    bool tracing = [] { const char* t = std::getenv("SRLA_TRACE"); return t && t[0] == '1'; }();
+    std::chrono::steady_clock::time_point trace_t0{};
+    void trace(const char* what) {
+        if (!tracing) return;
+        cudaStreamSynchronize(st);
+        const auto now = std::chrono::steady_clock::now();
+        if (what) std::fprintf(stderr, "[srla] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - trace_t0).count());
+        trace_t0 = now;
     }
 
     void join_eos() {
@@ -779,6 +799,7 @@ struct Engine {
         pin_counts.ensure(cfg.rows);
         CK(cudaMemcpyAsync(pin_counts.p, d_counts.p, cfg.rows * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        trace("  report: sort+gather+d2h");
         std::vector<uint64_t> counts(pin_counts.p, pin_counts.p + cfg.rows);
         const double fp = srla_host::fill_product(counts.data(), cfg.rows, lin_words);
         if (fp_out) *fp_out = fp;
@@ -828,6 +849,7 @@ struct Engine {
         const uint32_t n = static_cast<uint32_t>(ncsip);
         keep.ensure(n);
         csip2.ensure(n);
+        trace("  slide: si clear + age");
         k_retain<W, MAXR><<<blocks(n), 256, 0, st>>>(csip.p, n, dc, static_cast<const W*>(d_rough), d_si, keep.p);
         check_launch();
         launched();
@@ -835,9 +857,11 @@ struct Engine {
             return cub::DeviceSelect::Flagged(t, b, csip.p, keep.p, csip2.p, ctr.p + 5, static_cast<int>(n), st);
         });
         ncsip = read_ctr(5);
+        trace("  slide: retain+select");
         std::swap(csip.p, csip2.p);
         std::swap(csip.cap, csip2.cap);
         rebuild_cset(ncsip);
+        trace("  slide: cset rebuild");
     }
 
     void slide(bool age_linear = true) {
@@ -859,6 +883,7 @@ struct Engine {
     void end_slice(uint64_t slice_id, bool want_report, srla_entry* out) {
         const bool due = want_report && slice_id + 1 >= cfg.window;
         const auto w0 = std::chrono::steady_clock::now();
+        trace(nullptr);
         if (due && dc.k < dc.expired) {
             d_counts.ensure(cfg.rows);
             CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
@@ -868,8 +893,11 @@ struct Engine {
                 with_w([&](auto w) { count_age_range<decltype(w)>(0, uint64_t(cfg.rows) * lin_words, true); });
             }
             timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+            trace("eos: split+apply+count+age");
             report(out, nullptr, true);
+            trace("eos: report");
             slide(false);
+            trace("eos: slide");
         } else if (!due && use_bins) {
             flush_linear(1);
             timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();

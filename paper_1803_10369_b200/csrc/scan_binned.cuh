@@ -50,7 +50,7 @@ __device__ __forceinline__ void mark_word(W* base, uint32_t off) {
 // marks are binned by region; sampled packets stamp their rough entries and
 // append events exactly as k_scan does.
 template <typename W>
-__global__ void __launch_bounds__(kBinThreads) k_scan_bin(const uint32_t* __restrict__ recs, uint32_t n, DevCfg c,
+__global__ void __launch_bounds__(kBinThreads, 3) k_scan_bin(const uint32_t* __restrict__ recs, uint32_t n, DevCfg c,
                                                          BinCfg b, W* __restrict__ lin,
                                                          uint32_t* __restrict__ stamp, uint32_t* __restrict__ ev,
                                                          uint32_t ev_cap, uint32_t* __restrict__ ev_count, int vec) {
@@ -74,30 +74,30 @@ __global__ void __launch_bounds__(kBinThreads) k_scan_bin(const uint32_t* __rest
         __syncthreads();
 
         const uint32_t base = tile * kBinTile + tid * kBinPerThread;
-        uint32_t src[4], dst[4];
+        uint32_t src[kBinPerThread], dst[kBinPerThread];
         uint32_t valid = 0;
         if (base < n) {
-            if (vec && base + 4 <= n) {
+            if (vec && base + kBinPerThread <= n) {  // 4 records = three 16-byte vectors
                 const uint4* q = reinterpret_cast<const uint4*>(recs + 3ull * base);
                 const uint4 x = __ldcs(q), y = __ldcs(q + 1), z = __ldcs(q + 2);
                 src[0] = x.y; dst[0] = x.z;
                 src[1] = y.x; dst[1] = y.y;
                 src[2] = y.w; dst[2] = z.x;
                 src[3] = z.z; dst[3] = z.w;
-                valid = 4;
+                valid = kBinPerThread;
             } else {
-                valid = min(4u, n - base);
-                for (uint32_t q = 0; q < 4; ++q) {
+                valid = min(static_cast<uint32_t>(kBinPerThread), n - base);
+                for (uint32_t q = 0; q < kBinPerThread; ++q) {
                     src[q] = q < valid ? __ldcs(recs + 3ull * (base + q) + 1) : 0u;
                     dst[q] = q < valid ? __ldcs(recs + 3ull * (base + q) + 2) : 0u;
                 }
             }
         }
-        uint32_t off[4][kBinRows], rank[4][kBinRows];
-        uint16_t reg[4][kBinRows];
-        uint32_t smask = 0, rsl[4];
+        uint32_t off[kBinPerThread][kBinRows], rank[kBinPerThread][kBinRows];
+        uint16_t reg[kBinPerThread][kBinRows];
+        uint32_t smask = 0, rsl[kBinPerThread];
 #pragma unroll
-        for (uint32_t q = 0; q < 4; ++q) {
+        for (uint32_t q = 0; q < kBinPerThread; ++q) {
             rsl[q] = 0;
             const bool live = q < valid;
             const uint32_t sample = hash_u32(c.sub_sample, dst[q]);
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kBinThreads) k_scan_bin(const uint32_t* __rest
         if (__any_sync(0xFFFFFFFFu, smask != 0)) {
             uint32_t pos = warp_append(ev_count, __popc(smask));
 #pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) {
+            for (uint32_t q = 0; q < kBinPerThread; ++q) {
                 if (smask & (1u << q)) {
                     if (pos < ev_cap) {
                         ev[pos] = base + q;
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kBinThreads) k_scan_bin(const uint32_t* __rest
         __syncthreads();
 
 #pragma unroll
-        for (uint32_t q = 0; q < 4; ++q)
+        for (uint32_t q = 0; q < kBinPerThread; ++q)
 #pragma unroll
             for (int i = 0; i < kBinRows; ++i)
                 if (reg[q][i] != 0xFFFF) {

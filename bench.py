@@ -43,9 +43,20 @@ def sketch_cfg(cols):
                 seed=0x5EA00001)
 
 
-def trace_spec(pairs, slices=12):
+def trace_spec(pairs, slices=12, workload="c2"):
+    if workload == "c3":  # uniform, ~1e6 candidate super points
+        return dict(seed=3, slices=slices, window=10, a_hosts=1 << 20, b_hosts=1 << 24, pairs_per_slice=pairs,
+                    skew=0.0, plants=[])
     return dict(seed=1, slices=slices, window=10, a_hosts=4194304, b_hosts=1 << 22, pairs_per_slice=pairs,
                 skew=1.0, plants=[(0x0AC80001 + i, c, 0, 0xFFFFFFFF) for i, c in enumerate(plant_cards())])
+
+
+WORKLOADS = {
+    "c2": "C2: u=4 v=2^20 g=8 g'=1024 z=4 k=10 theta=1024 seed=0x5EA00001; trace seed 1, 4M uniform sources, "
+          "Zipf(1.0) 4M destinations, 50 plants",
+    "c3": "C3: u=4 v=2^24 g=8 g'=1024 z=4 k=10 theta=1024 seed=0x5EA00001 (64 GiB linear table, epoch stamps); "
+          "trace seed 3, 1M uniform sources, 16M uniform destinations (~1e6 candidates)",
+}
 
 
 def env_rank():
@@ -153,7 +164,7 @@ def run_reference_arm(args):
     per_step = []
     res = None
     for i in range(args.warmup + args.steps):
-        res = cpu_reference(recs, args.cols, threads, slice_id=9)
+        res = cpu_reference(recs, args.cols or (1 << 20), threads, slice_id=9)
         ms_full = full / res["scan_rate"] * 1e3 + res["eos_ms"]
         if i >= args.warmup:
             per_step.append((ms_full, res))
@@ -191,9 +202,10 @@ def run_engine(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = srla.SeaConfig(**sketch_cfg(args.cols))
+    cols = args.cols if args.cols else (1 << 24 if args.workload == "c3" else 1 << 20)
+    cfg = srla.SeaConfig(**sketch_cfg(cols))
     n_per_gpu = args.packets
-    spec = trace_spec(n_per_gpu * world)
+    spec = trace_spec(n_per_gpu * world, workload=args.workload)
     gen = srla.DeviceTraceGenerator(srla.PlantSpec(**spec), device=local)
 
     # stage the trace in HBM: one owned slice per generator slice
@@ -214,8 +226,13 @@ def run_engine(args):
 
     eng = srla.EstimatorArray(cfg, device=local)
     st = torch.cuda.ExternalStream(eng.stream_handle())
-    rep_cap = 1 << 22
-    rep_buf = np.empty(rep_cap, srla.ENTRY_DTYPE)
+    rep_cap = 1 << 21
+
+    def pinned_entries(n):  # DMA-able report buffer: the engine maps entries straight into it
+        return torch.empty(n * srla.ENTRY_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True).numpy().view(
+            srla.ENTRY_DTYPE)
+
+    rep_buf = pinned_entries(rep_cap)
 
     from paper_1803_10369_b200.shard import allgather_report as _allgather
 
@@ -304,7 +321,7 @@ def run_engine(args):
         nh = min(2, nres)
         host = [slices[i].cpu().pin_memory().numpy().view(np.uint32) for i in range(nh)]
         h2d = sum(h.nbytes for h in host) / nh
-        bufs = [np.empty(rep_cap, srla.ENTRY_DTYPE) for _ in range(2)]
+        bufs = [pinned_entries(rep_cap) for _ in range(2)]
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -336,10 +353,10 @@ def run_engine(args):
                "api": "srla_scan_batch(host, pinned) + srla_end_slice_async/wait"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
         recs = sample_records(args.cpu_sample, local)
         threads = os.cpu_count() or 1
-        r = cpu_reference(recs, args.cols, threads, slice_id=9)
+        r = cpu_reference(recs, cols, threads, slice_id=9)
         ms_full = n_per_gpu / r["scan_rate"] * 1e3 + r["eos_ms"]
         cpu = {"value": n_per_gpu / (ms_full / 1e3), "unit": "packets/s", "cores": r["threads"], "kind": r["kind"],
                "sample": f"DetectPipeline<u8>::process_slice (workers={r['threads']}) on the first {len(recs)} "
@@ -351,12 +368,13 @@ def run_engine(args):
             "metric": METRIC, "value": value, "unit": "packets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference generator C2 spec, device port)",
-            "config": {"workload": "C2: u=4 v=2^20 g=8 g'=1024 z=4 k=10 theta=1024 seed=0x5EA00001; "
-                                   "trace seed 1, 4M uniform sources, Zipf(1.0) 4M destinations, 50 plants",
+            "config": {"workload": WORKLOADS[args.workload],
                        "packets_per_slice_per_gpu": n_per_gpu, "resident_slices": nres,
                        "l2": "inputs larger than L2 (1.2 GB per slice); no flush",
                        "parallelism": f"owner-partitioned x{world}" if world > 1 else "1 GPU"},
-            "end_of_slice_ms": {"device_median": statistics.median(eos_dev), "device_p99": max(eos_dev),
+            "end_of_slice_ms": {"device_median": statistics.median(eos_dev),
+                                "device_p99": sorted(eos_dev)[min(len(eos_dev) - 1, int(0.99 * len(eos_dev)))],
+                                "device_max": max(eos_dev), "samples": len(eos_dev),
                                 "wall_median": statistics.median(eos_wall), "report_entries_median":
                                     statistics.median(entries)},
             "roofline": {"bound": "hbm", "kernel": "k_scan", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -385,14 +403,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--packets", type=int, default=100_000_000, help="packets per slice per GPU")
-    ap.add_argument("--cols", type=int, default=1 << 20)
-    ap.add_argument("--resident", type=int, default=12, help="distinct slices staged in HBM")
+    ap.add_argument("--cols", type=int, default=0, help="sketch columns (default: the workload's)")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3"])
+    ap.add_argument("--resident", type=int, default=0, help="distinct slices staged in HBM (default 12; c3: 10)")
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if not args.resident:
+        args.resident = 10 if args.workload == "c3" else 12
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_engine(args)

@@ -44,10 +44,15 @@ typedef struct srla_config {
     uint32_t recorder_bits; /* z: 1..32; storage word 1/2/4 B (recorders.hpp:64-66) */
     uint32_t window;        /* k: 1..2^z-1 */
     uint32_t theta;
-    uint32_t reserved;      /* must be 0 */
+    uint32_t flags;         /* SRLA_FLAG_*; 0 = automatic (not part of SeaConfig) */
     double fill_ratio;      /* kSuperTestRatio by default (estimators.hpp:19) */
     uint64_t seed;
 } srla_config;
+
+/* Linear-recorder representation (results are identical either way):
+ * literal distances with an O(table) slide, or epoch stamps with an O(1)
+ * slide. Default: stamps for linear tables of 16 GiB and more. */
+enum { SRLA_FLAG_EPOCH = 1u, SRLA_FLAG_LITERAL = 2u };
 
 /* sspread::TraceRecord (trace.hpp:20-26): 12 bytes, host byte order. */
 typedef struct srla_record {

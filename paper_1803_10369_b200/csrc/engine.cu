@@ -22,6 +22,7 @@
 #include "host_math.h"
 #include "kernels.cuh"
 #include "scan_binned.cuh"
+#include "epoch.cuh"
 #include "srla.h"
 
 namespace srla {
@@ -121,6 +122,9 @@ struct Engine {
     DevBuf<uint32_t> dstage[2];
     PinBuf<uint32_t> pstage[2], pin_hosts, pin_w;
     cudaStream_t cs = nullptr;  // host->device copy stream
+    cudaStream_t st2 = nullptr; // end-of-slice side stream (rough aging overlaps the report)
+    cudaEvent_t ev_eos_start = nullptr, ev_rough_aged = nullptr;
+    bool rough_preaged = false;
     cudaEvent_t ev_copied[2] = {}, ev_scanned[2] = {};
     cudaEvent_t t_scan0 = nullptr, t_scan1 = nullptr, t_eos0 = nullptr, t_eos1 = nullptr;
     srla_timing timing{};
@@ -134,6 +138,9 @@ struct Engine {
         std::string msg;
         uint64_t n = 0, nret = 0;
     } eos;
+    PinBuf<uint8_t> pin_lut;
+    DevBuf<uint8_t> d_lut;
+    DevBuf<unsigned long long> d_entries;
     std::vector<double> lut_est;
     std::vector<uint8_t> lut_has, lut_sup;
     bool collect_pushed = false;
@@ -147,6 +154,15 @@ struct Engine {
     FineCfg fcfg{};
     bool bulk_ok = false;
     uint32_t bulk_end = 0;
+    size_t split_smem = 0;
+
+    // epoch-stamp linear table (epoch.cuh): u8 stamps, O(1) slide
+    bool epoch = false;
+    uint32_t cur_epoch = 0;
+    DevBuf<unsigned long long> hist;  // rows x 256
+    PinBuf<unsigned long long> pin_hist;
+    uint64_t sweep_pos = 0;
+    EpochCfg ecfg() const { return EpochCfg{epoch ? 1u : 0u, cur_epoch, hist.p, lin_words}; }
     PinBuf<uint32_t> pin_bc;
     uint64_t pending_entries = 0;
     bool prefetch_next = false;  // bulk-prefetch region r+1 while applying r (measured slower; off)
@@ -157,6 +173,9 @@ struct Engine {
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_eos_start, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_rough_aged, cudaEventDisableTiming));
         for (int b = 0; b < 2; ++b) {
             CK(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ev_scanned[b], cudaEventDisableTiming));
@@ -200,6 +219,7 @@ struct Engine {
         ctr.ensure(16);
         pin_ctr.ensure(16);
         setup_bins();
+        setup_epoch();
         rebuild_cset(1024);
         CK(cudaStreamSynchronize(st));
     }
@@ -219,6 +239,12 @@ struct Engine {
         for (cudaEvent_t e : {t_scan0, t_scan1, t_eos0, t_eos1})
             if (e) cudaEventDestroy(e);
         if (cs) cudaStreamDestroy(cs);
+        if (st2) {
+            cudaStreamSynchronize(st2);
+            cudaStreamDestroy(st2);
+        }
+        if (ev_eos_start) cudaEventDestroy(ev_eos_start);
+        if (ev_rough_aged) cudaEventDestroy(ev_rough_aged);
         if (st) cudaStreamDestroy(st);
     }
 
@@ -241,7 +267,8 @@ struct Engine {
                                             std::to_string(cfg.recorder_bits) +
                                             "-bit recorder (valid range [1, " + std::to_string(e) + "])");
         if (cfg.rows > kMaxRows) bad("at most 64 rows supported");
-        if (cfg.reserved != 0) bad("srla_config.reserved must be 0");
+        if (cfg.flags & ~uint32_t(SRLA_FLAG_EPOCH | SRLA_FLAG_LITERAL)) bad("unknown srla_config.flags bits");
+        if ((cfg.flags & SRLA_FLAG_EPOCH) && (cfg.flags & SRLA_FLAG_LITERAL)) bad("conflicting srla_config.flags");
     }
 
     uint32_t blocks(uint64_t work, uint32_t per = 256, uint32_t waves = 8) const {
@@ -343,7 +370,14 @@ struct Engine {
         while ((1ull << (shift + 1)) * wb <= (32ull << 20)) ++shift;  // 32 MB coarse regions
         if (forced)
             while (shift > 4 && (total_words >> shift) < 8) --shift;  // ~8 regions even for tiny tables
-        while ((total_words >> shift) >= kMaxRegions) ++shift;
+        while (((total_words + (1ull << shift) - 1) >> shift) > kMaxRegions) ++shift;
+        // fine slices (u16 offsets): 32 KB, or larger so one region splits into <= 4096
+        uint32_t fs = 0;
+        while ((1ull << (fs + 1)) * wb <= (32ull << 10)) ++fs;  // 32 KB: two buffers per block
+        fs = std::min(fs, shift);
+        if (forced && small) fs = std::max<uint32_t>(std::min<uint32_t>(shift, 4), shift > 3 ? shift - 3 : 0);
+        while (shift - fs > 12) ++fs;  // split fan-out <= 4096 slices per region
+        if ((1ull << fs) * wb > (64ull << 10)) return;  // slices must fit twice in shared memory
         bcfg.region_shift = shift;
         bcfg.nregions = static_cast<uint32_t>((total_words + (1ull << shift) - 1) >> shift);
         const uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);
@@ -355,12 +389,6 @@ struct Engine {
         CK(cudaMemsetAsync(bin_count.p, 0, bcfg.nregions * sizeof(uint32_t), st));
         bcfg.bins = bins.p;
         bcfg.count = bin_count.p;
-        // fine 64 KB slices (u16 offsets), at most kMaxRegions per region
-        uint32_t fs = 0;
-        while ((1ull << (fs + 1)) * wb <= (32ull << 10)) ++fs;  // 32 KB: two buffers per block
-        fs = std::min(fs, shift);
-        if (forced && small) fs = std::max<uint32_t>(std::min<uint32_t>(shift, 4), shift > 3 ? shift - 3 : 0);
-        while (shift - fs > 10) ++fs;
         fcfg.shift = fs;
         fcfg.per_region = 1u << (shift - fs);
         fcfg.nfine = static_cast<uint32_t>((total_words + (1ull << fs) - 1) >> fs);
@@ -372,8 +400,10 @@ struct Engine {
         fcfg.count = fine_count.p;
         CK(cudaMemsetAsync(fine_count.p, 0, fine_count.cap * sizeof(uint32_t), st));
         const int smem = static_cast<int>((1ull << fs) * wb);
+        split_smem = kSplitTile * 4 + fcfg.per_region * 14;
         with_w([&](auto w) {
             using W = decltype(w);
+            CK(cudaFuncSetAttribute(k_split<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(split_smem)));
             CK(cudaFuncSetAttribute(k_slice_apply<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(smem, 16)));
             CK(cudaFuncSetAttribute(k_slice_apply_bulk<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(2 * smem, 32)));
         });
@@ -383,6 +413,74 @@ struct Engine {
         bulk_end = (total_words % slice_words) * wb % 16 == 0 ? fcfg.nfine : fcfg.nfine - 1;
         if (total_words % slice_words) bulk_end = fcfg.nfine - 1;  // partial last slice: plain kernel
         use_bins = true;
+    }
+
+    // Epoch stamps replace the O(table) slide by O(1) + a 1/(255-expired)
+    // sweep, at the price of a CAS per mark. Chosen for tables of 16 GiB and
+    // more (the 2^24-column sketch), or by srla_config.flags / SRLA_EPOCH.
+    void setup_epoch() {
+        const char* env = std::getenv("SRLA_EPOCH");
+        bool want = uint64_t(cfg.rows) * lin_words * wb >= (16ull << 30);
+        if (cfg.flags & SRLA_FLAG_EPOCH) want = true;
+        if (cfg.flags & SRLA_FLAG_LITERAL) want = false;
+        if (env) want = env[0] == '1';
+        if (!want || !use_bins || wb != 1 || dc.expired > 127) return;
+        if (lin_words < (1ull << fcfg.shift)) return;  // a slice may span at most two rows
+        epoch = true;
+        cur_epoch = 0;
+        hist.ensure(uint64_t(cfg.rows) * 256);
+        pin_hist.ensure(uint64_t(cfg.rows) * 256);
+        CK(cudaMemsetAsync(hist.p, 0, uint64_t(cfg.rows) * 256 * sizeof(unsigned long long), st));
+        const uint64_t words = uint64_t(cfg.rows) * lin_words;
+        k_fill<uint8_t><<<blocks(words, 256, 16), 256, 0, st>>>(static_cast<uint8_t*>(d_lin), words,
+                                                                static_cast<uint8_t>((256 - dc.expired) & 0xFF));
+        check_launch();
+        launched();
+        CK(cudaFuncSetAttribute(k_slice_stamp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                std::max<int>(32, int(2u << fcfg.shift))));
+    }
+
+    // Literal recorder value of a stamp (recorders.hpp:84-87 applied cur - s times).
+    uint32_t stamp_value(uint32_t s) const {
+        const uint32_t a = (cur_epoch - s) & 0xFFu;
+        return a < dc.expired ? a : dc.expired;
+    }
+
+    // Convert the table back to literal recorders (an import carried values
+    // outside [0, expired], which stamps cannot hold).
+    void leave_epoch() {
+        if (!epoch) return;
+        flush_linear();
+        const uint64_t words = uint64_t(cfg.rows) * lin_words;
+        k_epoch_to_literal<<<blocks(words / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<uint8_t*>(d_lin), words, cur_epoch,
+                                                                           dc.expired);
+        check_launch();
+        launched();
+        epoch = false;
+    }
+
+    // counts_active per row from the stamp histograms (already on the host)
+    void counts_from_hist(uint64_t* counts) const {
+        for (uint32_t i = 0; i < cfg.rows; ++i) {
+            uint64_t s = 0;
+            for (uint32_t j = 0; j < cfg.window; ++j) s += pin_hist.p[uint64_t(i) * 256 + ((cur_epoch - j) & 0xFFu)];
+            counts[i] = s;
+        }
+    }
+
+    void slide_epoch_tables() {
+        cur_epoch = (cur_epoch + 1) & 0xFFu;
+        k_zero_hist_bin<<<1, 64, 0, st>>>(hist.p, cfg.rows, cur_epoch);
+        check_launch();
+        const uint64_t total = uint64_t(cfg.rows) * lin_words;
+        const uint64_t period = 255 - dc.expired;                  // slides between visits of a byte
+        const uint64_t chunk = ((total + period - 1) / period + 15) & ~15ull;
+        const uint64_t end = std::min(total, sweep_pos + chunk);
+        k_sweep<<<blocks((end - sweep_pos) / 16 + 1, 256, 8), 256, 0, st>>>(static_cast<uint8_t*>(d_lin), sweep_pos,
+                                                                           end - sweep_pos, cur_epoch, dc.expired);
+        check_launch();
+        launched(2);
+        sweep_pos = end >= total ? 0 : end;
     }
 
     // Age (and optionally count) linear words [w0, w1) — split at row
@@ -426,13 +524,25 @@ struct Engine {
             if (run) {
                 with_w([&](auto w) {
                     using W = decltype(w);
-                    k_split<W><<<std::min<uint32_t>(run, sms * 8), kSplitThreads, 0, st>>>(
-                        bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg,
+                    k_split<W><<<std::min<uint32_t>(run, sms * 8), kSplitThreads, split_smem, st>>>(
+                        bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg, ecfg(),
                         static_cast<W*>(d_lin));
                 });
                 check_launch();
                 launched();
             }
+        }
+        if (epoch) {
+            if (pending_entries) {
+                k_slice_stamp<<<std::min<uint32_t>(fcfg.nfine, sms * 3), 256, 2u << fcfg.shift, st>>>(
+                    static_cast<uint8_t*>(d_lin), total, lin_words, fcfg, 0, bulk_ok ? 1 : 0, cur_epoch, cfg.window, hist.p);
+                check_launch();
+                launched();
+                CK(cudaMemsetAsync(fine_count.p, 0, fcfg.nfine * sizeof(uint32_t), st));
+                CK(cudaMemsetAsync(bin_count.p, 0, R * sizeof(uint32_t), st));
+            }
+            pending_entries = 0;
+            return;
         }
         with_w([&](auto w) {
             using W = decltype(w);
@@ -477,7 +587,7 @@ struct Engine {
             CK(cudaEventRecord(t_scan0, st));
             if (use_bins && MAXR <= kBinRows) {
                 const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
-                k_scan_bin<W><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, st>>>(d_recs, n, dc, bcfg, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                k_scan_bin<W><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             } else {
                 k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             }
@@ -691,9 +801,12 @@ struct Engine {
             const uint32_t* base = reinterpret_cast<const uint32_t*>(recs);
             for (uint64_t o = 0; o < n; o += kChunk)
                 scan_chunk(base + 3 * o, static_cast<uint32_t>(std::min<uint64_t>(kChunk, n - o)));
-            return;
+        } else {
+            scan_host(reinterpret_cast<const uint32_t*>(recs), n);
         }
-        scan_host(reinterpret_cast<const uint32_t*>(recs), n);
+        // epoch stamps: apply this batch's marks now, so end-of-slice only
+        // reads histograms and the candidates' cells
+        if (epoch) flush_linear();
     }
 
     // Host records: double-buffered H2D on a copy stream overlapping the scan
@@ -743,6 +856,15 @@ struct Engine {
     }
     void union_linear(const uint32_t* d_hosts, uint32_t n, uint32_t* d_out, uint32_t kthr) {
         if (!n) return;
+        if (epoch) {
+            if (cfg.rows <= 4)
+                k_union_linear_epoch<4><<<blocks(uint64_t(n) * 32, 256, 16), 256, 0, st>>>(d_hosts, n, dc, static_cast<const uint8_t*>(d_lin), cur_epoch, d_out);
+            else
+                k_union_linear_epoch<64><<<blocks(uint64_t(n) * 32, 256, 16), 256, 0, st>>>(d_hosts, n, dc, static_cast<const uint8_t*>(d_lin), cur_epoch, d_out);
+            check_launch();
+            launched();
+            return;
+        }
         with_w([&](auto w) {
             using W = decltype(w);
             if (cfg.rows <= 4) union_linear_t<W, 4>(d_hosts, n, d_out, kthr);
@@ -765,6 +887,12 @@ struct Engine {
 
     void row_active(uint64_t* out) {
         flush_linear();
+        if (epoch) {
+            CK(cudaMemcpyAsync(pin_hist.p, hist.p, uint64_t(cfg.rows) * 256 * 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            counts_from_hist(out);
+            return;
+        }
         row_active_async();
         pin_counts.ensure(cfg.rows);
         CK(cudaMemcpyAsync(pin_counts.p, d_counts.p, cfg.rows * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -779,10 +907,14 @@ struct Engine {
     void report(srla_entry* out, double* fp_out, bool counts_ready = false) {
         const auto w0 = std::chrono::steady_clock::now();
         const uint32_t n = static_cast<uint32_t>(ncsip);
+        cudaPointerAttributes oa{};
+        const bool out_pinned =
+            n >= (1u << 14) && cudaPointerGetAttributes(&oa, out) == cudaSuccess && oa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
         const uint32_t kthr = counts_ready ? cfg.window + 1 : cfg.window;
         if (!counts_ready) {
             flush_linear();
-            row_active_async();
+            if (!epoch) row_active_async();
         }
         if (n) {
             sorted_hosts.ensure(n);
@@ -791,55 +923,100 @@ struct Engine {
                 return cub::DeviceRadixSort::SortKeys(t, b, csip.p, sorted_hosts.p, static_cast<int>(n), 0, 32, st);
             });
             union_linear(sorted_hosts.p, n, weights.p, kthr);
-            pin_hosts.ensure(n);
-            pin_w.ensure(n);
-            CK(cudaMemcpyAsync(pin_hosts.p, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(pin_w.p, weights.p, n * 4ull, cudaMemcpyDeviceToHost, st));
+            if (!out_pinned) {
+                pin_hosts.ensure(n);
+                pin_w.ensure(n);
+                CK(cudaMemcpyAsync(pin_hosts.p, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(pin_w.p, weights.p, n * 4ull, cudaMemcpyDeviceToHost, st));
+            }
         }
         pin_counts.ensure(cfg.rows);
-        CK(cudaMemcpyAsync(pin_counts.p, d_counts.p, cfg.rows * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        if (epoch) CK(cudaMemcpyAsync(pin_hist.p, hist.p, uint64_t(cfg.rows) * 256 * 8, cudaMemcpyDeviceToHost, st));
+        else CK(cudaMemcpyAsync(pin_counts.p, d_counts.p, cfg.rows * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         trace("  report: sort+gather+d2h");
         std::vector<uint64_t> counts(pin_counts.p, pin_counts.p + cfg.rows);
+        if (epoch) counts_from_hist(counts.data());
         const double fp = srla_host::fill_product(counts.data(), cfg.rows, lin_words);
         if (fp_out) *fp_out = fp;
         lut_est.resize(cfg.linear_slots + 1);
         lut_has.resize(cfg.linear_slots + 1);
         lut_sup.resize(cfg.linear_slots + 1);
         srla_host::estimate_lut(cfg.linear_slots, fp, cfg.theta, lut_est.data(), lut_has.data(), lut_sup.data());
-        // map (host, weight) -> entries straight into the caller's buffer
-        auto fill = [&](uint32_t lo, uint32_t hi) {
-            for (uint32_t e = lo; e < hi; ++e) {
-                const uint32_t w = pin_w.p[e];
-                srla_entry x{};
-                x.host = pin_hosts.p[e];
-                x.union_weight = w;
-                x.estimate = lut_est[w];
-                x.has_estimate = lut_has[w];
-                x.is_super = lut_sup[w];
-                out[e] = x;
-            }
-        };
-        const uint32_t nt = n >= (1u << 16) ? 8u : 1u;
-        if (nt == 1) {
-            fill(0, n);
+        // (host, weight) -> entries: on the device straight into a pinned
+        // caller buffer, else on the host into pageable memory
+        if (out_pinned) {
+            const uint32_t L = cfg.linear_slots + 1;
+            pin_lut.ensure(L * 10ull);
+            double* le = reinterpret_cast<double*>(pin_lut.p);
+            uint8_t* lh = pin_lut.p + 8ull * L;
+            std::memcpy(le, lut_est.data(), 8ull * L);
+            std::memcpy(lh, lut_has.data(), L);
+            std::memcpy(lh + L, lut_sup.data(), L);
+            d_lut.ensure(L * 10ull);
+            CK(cudaMemcpyAsync(d_lut.p, pin_lut.p, L * 10ull, cudaMemcpyHostToDevice, st));
+            d_entries.ensure(3ull * n);
+            k_map_entries<<<blocks(n), 256, 0, st>>>(sorted_hosts.p, weights.p, n, reinterpret_cast<const double*>(d_lut.p),
+                                                     d_lut.p + 8ull * L, d_lut.p + 9ull * L, d_entries.p);
+            check_launch();
+            launched();
+            // one DMA into the caller's pinned buffer (kernel stores over PCIe are scattered)
+            CK(cudaMemcpyAsync(out, d_entries.p, 24ull * n, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
         } else {
-            std::vector<std::thread> pool;
-            for (uint32_t t = 1; t < nt; ++t) pool.emplace_back(fill, uint64_t(n) * t / nt, uint64_t(n) * (t + 1) / nt);
-            fill(0, n / nt);
-            for (auto& th : pool) th.join();
+            auto fill = [&](uint32_t lo, uint32_t hi) {
+                for (uint32_t e = lo; e < hi; ++e) {
+                    const uint32_t w = pin_w.p[e];
+                    srla_entry x{};
+                    x.host = pin_hosts.p[e];
+                    x.union_weight = w;
+                    x.estimate = lut_est[w];
+                    x.has_estimate = lut_has[w];
+                    x.is_super = lut_sup[w];
+                    out[e] = x;
+                }
+            };
+            const uint32_t nt = n >= (1u << 16) ? 8u : 1u;
+            if (nt == 1) {
+                fill(0, n);
+            } else {
+                std::vector<std::thread> pool;
+                for (uint32_t t = 1; t < nt; ++t) pool.emplace_back(fill, uint64_t(n) * t / nt, uint64_t(n) * (t + 1) / nt);
+                fill(0, n / nt);
+                for (auto& th : pool) th.join();
+            }
         }
         timing.report_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
     }
 
     // ------------------------------------------------------------ slide (sea.hpp:316-338)
+    // SI clear + rough aging on the side stream, overlapping the report
+    // (neither reads them); slide_t waits for it.
+    template <typename W>
+    void preage_rough_t() {
+        const uint64_t rows = cfg.rows;
+        CK(cudaEventRecord(ev_eos_start, st));
+        CK(cudaStreamWaitEvent(st2, ev_eos_start, 0));
+        CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st2));
+        k_age<W><<<blocks(rows * rough_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st2>>>(static_cast<W*>(d_rough), rows * rough_words, dc.expired);
+        check_launch();
+        launched();
+        CK(cudaEventRecord(ev_rough_aged, st2));
+        rough_preaged = true;
+    }
+
     template <typename W, int MAXR>
     void slide_t(bool age_linear) {
         const uint64_t rows = cfg.rows;
-        CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st));
-        k_age<W><<<blocks(rows * rough_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_rough), rows * rough_words, dc.expired);
-        check_launch();
-        launched();
+        if (rough_preaged) {
+            CK(cudaStreamWaitEvent(st, ev_rough_aged, 0));
+            rough_preaged = false;
+        } else {
+            CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st));
+            k_age<W><<<blocks(rows * rough_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_rough), rows * rough_words, dc.expired);
+            check_launch();
+            launched();
+        }
         if (age_linear) {
             k_age<W><<<blocks(rows * lin_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_lin), rows * lin_words, dc.expired);
             check_launch();
@@ -868,6 +1045,10 @@ struct Engine {
         const auto w0 = std::chrono::steady_clock::now();
         stats.slides++;
         flush_linear();
+        if (epoch) {
+            slide_epoch_tables();
+            age_linear = false;
+        }
         with_w([&](auto w) {
             using W = decltype(w);
             if (cfg.rows <= 4) slide_t<W, 4>(age_linear);
@@ -884,6 +1065,15 @@ struct Engine {
         const bool due = want_report && slice_id + 1 >= cfg.window;
         const auto w0 = std::chrono::steady_clock::now();
         trace(nullptr);
+        with_w([&](auto w) { preage_rough_t<decltype(w)>(); });
+        if (epoch) {
+            flush_linear();
+            if (due) report(out, nullptr);
+            trace("eos: report (epoch)");
+            slide(false);
+            trace("eos: slide (epoch)");
+            return;
+        }
         if (due && dc.k < dc.expired) {
             d_counts.ensure(cfg.rows);
             CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
@@ -985,7 +1175,8 @@ struct Engine {
             acc &= s;
             for (uint32_t j = 0; j < cfg.rough_slots; ++j) rough[j] = std::max(rough[j], word_at(rb, j));
             if (linear)
-                for (uint32_t j = 0; j < cfg.linear_slots; ++j) linear[j] = std::max(linear[j], word_at(lb, j));
+                for (uint32_t j = 0; j < cfg.linear_slots; ++j)
+                    linear[j] = std::max(linear[j], epoch ? stamp_value(lb[j]) : word_at(lb, j));
         }
         *ind = acc;
     }
@@ -1011,12 +1202,37 @@ struct Engine {
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
         CK(cudaMemcpyAsync(buf, p, bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        if (epoch && kind == SRLA_LINEAR) {
+            uint8_t* b = static_cast<uint8_t*>(buf);
+            uint8_t lut[256];
+            for (uint32_t s = 0; s < 256; ++s) lut[s] = static_cast<uint8_t>(stamp_value(s));
+            for (uint64_t j = 0; j < bytes; ++j) b[j] = lut[b[j]];
+        }
     }
 
     void import_row(uint32_t row, int kind, const void* buf, uint64_t bytes) {
         flush_linear();
         uint8_t* p = row_ptr(row, kind);
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
+        if (epoch && kind == SRLA_LINEAR) {
+            const uint8_t* v = static_cast<const uint8_t*>(buf);
+            bool in_model = true;
+            for (uint64_t j = 0; j < bytes && in_model; ++j) in_model = v[j] <= dc.expired;
+            if (!in_model) {
+                leave_epoch();  // values beyond `expired` need literal recorders
+            } else {
+                std::vector<uint8_t> s(bytes);
+                for (uint64_t j = 0; j < bytes; ++j)
+                    s[j] = static_cast<uint8_t>((cur_epoch - std::min<uint32_t>(v[j], dc.expired)) & 0xFFu);
+                CK(cudaMemcpyAsync(p, s.data(), bytes, cudaMemcpyHostToDevice, st));
+                CK(cudaMemsetAsync(hist.p + uint64_t(row) * 256, 0, 256 * sizeof(unsigned long long), st));
+                k_row_hist<<<blocks(bytes, 256, 4), 256, 0, st>>>(p, bytes, hist.p + uint64_t(row) * 256);
+                check_launch();
+                launched();
+                CK(cudaStreamSynchronize(st));
+                return;
+            }
+        }
         CK(cudaMemcpyAsync(p, buf, bytes, cudaMemcpyHostToDevice, st));
         CK(cudaStreamSynchronize(st));
     }

@@ -1,0 +1,268 @@
+// epoch.cuh — epoch-stamp linear recorders (u8 storage, z <= 7).
+//
+// A linear recorder byte holds the epoch (slice counter mod 256) of its last
+// mark instead of the distance itself. The reference's value is recovered as
+//   r = min((cur - s) mod 256, expired)                 (recorders.hpp:78-116)
+// so the slide (age every recorder, sea.hpp:318-327) becomes `cur += 1`.
+// Invariants that keep this exact:
+//   * every stamp's age (cur - s) mod 256 stays <= 255: a sweep rewrites
+//     stale stamps (age >= expired) to age exactly `expired`, visiting every
+//     byte at least once per 255 - expired slides (1/240 of the table per
+//     slide for z = 4);
+//   * per row, hist[b] counts the recorders stamped b during the epoch b is
+//     current and since: a mark moving a recorder off stamp s_old decrements
+//     hist[s_old], onto cur increments hist[cur]; bins of stale epochs hold
+//     garbage and are zeroed when the epoch counter comes back to them, which
+//     the sweep invariant makes safe. Active recorders of a row (count_active,
+//     recorders.hpp:119-129) = sum over the last k epochs of hist.
+// The fill counts of report_window therefore need no table pass, and the
+// slide touches only 1/(255 - expired) of the table.
+#pragma once
+
+#include "common.cuh"
+#include "scan_binned.cuh"
+
+namespace srla {
+
+__device__ __forceinline__ uint32_t stamp_byte_shared(uint8_t* base, uint32_t off, uint32_t cur) {
+    unsigned int* w = reinterpret_cast<unsigned int*>(base + (off & ~3u));
+    const uint32_t sh = 8u * (off & 3u);
+    unsigned int old = *w, assumed;
+    do {
+        assumed = old;
+        if (((assumed >> sh) & 0xFFu) == cur) return cur;
+        old = atomicCAS(w, assumed, (assumed & ~(0xFFu << sh)) | (cur << sh));
+    } while (old != assumed);
+    return (old >> sh) & 0xFFu;
+}
+
+// Apply pending marks of slices [f_begin, nfine) as epoch stamps (only slices
+// with marks; bulk-loaded, double-buffered like k_slice_apply_bulk) and
+// account the transitions in the per-row histograms.
+__global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, uint64_t total_words,
+                                                     uint64_t row_words, FineCfg f, uint32_t f_begin, int bulk,
+                                                     uint32_t cur, uint32_t k, unsigned long long* __restrict__ hist) {
+    extern __shared__ __align__(128) uint8_t s_raw[];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ uint32_t s_hist[2][256];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t slice_bytes = 1u << f.shift;
+    uint8_t* buf[2] = {s_raw, s_raw + slice_bytes};
+    auto next_slice = [&](uint32_t from) -> uint32_t {
+        for (uint32_t fb = from; fb < f.nfine; fb += gridDim.x)
+            if (f.count[fb] != 0) return fb;
+        return f.nfine;
+    };
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+    }
+    __syncthreads();
+    uint32_t cur_fb = next_slice(f_begin + blockIdx.x);
+    auto slice_len = [&](uint32_t fb) {
+        return static_cast<uint32_t>(min(static_cast<uint64_t>(slice_bytes), total_words - (static_cast<uint64_t>(fb) << f.shift)));
+    };
+    auto load = [&](uint32_t fb, uint32_t b) {
+        // bulk path: whole 16-byte multiple slices; plain path for the tail slice
+        const uint32_t len = slice_len(fb);
+        uint8_t* g = lin + (static_cast<uint64_t>(fb) << f.shift);
+        if (bulk && (len & 15) == 0) {
+            if (tid == 0) {
+                mbar_expect_tx(&s_bar[b], len);
+                bulk_load(buf[b], g, len, &s_bar[b]);
+            }
+            return true;
+        }
+        return false;
+    };
+    uint32_t phase[2] = {0u, 0u};  // parity of each barrier's next completion
+    bool bulk_cur = cur_fb < f.nfine ? load(cur_fb, 0) : false;
+    for (uint32_t i = 0; cur_fb < f.nfine; ++i) {
+        const uint32_t b = i & 1u;
+        const uint32_t nxt = next_slice(cur_fb + gridDim.x);
+        bool bulk_nxt = false;
+        if (nxt < f.nfine) {
+            if (tid == 0) bulk_wait_read_all();
+            bulk_nxt = load(nxt, b ^ 1u);
+        }
+        const uint32_t len = slice_len(cur_fb);
+        uint8_t* g = lin + (static_cast<uint64_t>(cur_fb) << f.shift);
+        for (uint32_t q = tid; q < 512; q += blockDim.x) (&s_hist[0][0])[q] = 0;
+        if (bulk_cur) {
+            mbar_wait(&s_bar[b], phase[b]);
+            phase[b] ^= 1u;
+        } else {
+            for (uint32_t q = tid; q < len; q += blockDim.x) buf[b][q] = g[q];
+        }
+        __syncthreads();
+        const uint32_t n = min(f.count[cur_fb], f.cap);
+        const uint16_t* e = f.bins + static_cast<uint64_t>(cur_fb) * f.cap;
+        const uint64_t w0 = static_cast<uint64_t>(cur_fb) << f.shift;
+        const uint64_t row_a = w0 / row_words;
+        const uint32_t split = static_cast<uint32_t>(min(static_cast<uint64_t>(len), (row_a + 1) * row_words - w0));
+        // transitions onto `cur` are counted per warp (one shared atomic per
+        // warp and row); decrements only matter for stamps inside the window
+        // (stale bins are zeroed when the counter returns to them)
+        const uint32_t lane = tid & 31u;
+        for (uint32_t q0 = 0; q0 < n; q0 += blockDim.x) {
+            const uint32_t q = q0 + tid;
+            uint32_t old = cur, h = 0;
+            if (q < n) {
+                const uint32_t off = e[q];
+                old = stamp_byte_shared(buf[b], off, cur);
+                h = off < split ? 0u : 1u;
+                if (old != cur && ((cur - old) & 0xFFu) < k) atomicSub(&s_hist[h][old], 1u);
+            }
+            const unsigned moved = __ballot_sync(0xFFFFFFFFu, old != cur);
+            const unsigned row_b = __ballot_sync(0xFFFFFFFFu, h == 1u);
+            if (lane == 0) {
+                const uint32_t c1 = __popc(moved & row_b), c0 = __popc(moved) - c1;
+                if (c0) atomicAdd(&s_hist[0][cur], c0);
+                if (c1) atomicAdd(&s_hist[1][cur], c1);
+            }
+        }
+        __syncthreads();
+        for (uint32_t q = tid; q < 512; q += blockDim.x) {
+            const uint32_t v = (&s_hist[0][0])[q];
+            if (v) {
+                const uint32_t h = q >> 8;
+                atomicAdd(hist + (row_a + h) * 256 + (q & 255u),
+                          static_cast<unsigned long long>(static_cast<long long>(static_cast<int32_t>(v))));
+            }
+        }
+        if (bulk_cur) {
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (tid == 0) bulk_store(g, buf[b], len);
+        } else {
+            for (uint32_t q = tid; q < len; q += blockDim.x) g[q] = buf[b][q];
+            __syncthreads();
+        }
+        cur_fb = nxt;
+        bulk_cur = bulk_nxt;
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
+// Sweep [w0, w0+n) of the table: stamps with age >= expired become age
+// exactly `expired` (no histogram change: such recorders are outside every
+// window, k <= expired).
+__global__ void __launch_bounds__(256) k_sweep(uint8_t* __restrict__ lin, uint64_t w0, uint64_t n, uint32_t cur,
+                                               uint32_t expired) {
+    const uint32_t cur4 = cur * 0x01010101u, e4 = expired * 0x01010101u;
+    const uint32_t tgt4 = ((cur - expired) & 0xFFu) * 0x01010101u;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint8_t* base = lin + w0;
+    const uint64_t head = min(n, static_cast<uint64_t>((16 - (reinterpret_cast<uintptr_t>(base) & 15)) & 15));
+    auto fix = [&](uint32_t x) {
+        const uint32_t stale = __vcmpgeu4(__vsub4(cur4, x), e4);
+        return (x & ~stale) | (tgt4 & stale);
+    };
+    for (uint64_t q = tid; q < head; q += stride) {
+        const uint32_t s = base[q];
+        if (((cur - s) & 0xFFu) >= expired) base[q] = static_cast<uint8_t>((cur - expired) & 0xFFu);
+    }
+    uint4* v = reinterpret_cast<uint4*>(base + head);
+    const uint64_t nv = (n - head) / 16;
+    for (uint64_t q = tid; q < nv; q += stride) {
+        uint4 x = v[q];
+        x.x = fix(x.x);
+        x.y = fix(x.y);
+        x.z = fix(x.z);
+        x.w = fix(x.w);
+        v[q] = x;
+    }
+    for (uint64_t q = head + nv * 16 + tid; q < n; q += stride) {
+        const uint32_t s = base[q];
+        if (((cur - s) & 0xFFu) >= expired) base[q] = static_cast<uint8_t>((cur - expired) & 0xFFu);
+    }
+}
+
+__global__ void k_zero_hist_bin(unsigned long long* hist, uint32_t rows, uint32_t bin) {
+    for (uint32_t i = threadIdx.x; i < rows; i += blockDim.x) hist[i * 256ull + bin] = 0;
+}
+
+// Stamps -> literal recorder values min((cur - s) mod 256, expired).
+__global__ void __launch_bounds__(256) k_epoch_to_literal(uint8_t* __restrict__ lin, uint64_t n, uint32_t cur,
+                                                          uint32_t expired) {
+    const uint32_t cur4 = cur * 0x01010101u, e4 = expired * 0x01010101u;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint4* v = reinterpret_cast<uint4*>(lin);
+    const uint64_t nv = n / 16;
+    for (uint64_t q = tid; q < nv; q += stride) {
+        uint4 x = v[q];
+        x.x = __vminu4(__vsub4(cur4, x.x), e4);
+        x.y = __vminu4(__vsub4(cur4, x.y), e4);
+        x.z = __vminu4(__vsub4(cur4, x.z), e4);
+        x.w = __vminu4(__vsub4(cur4, x.w), e4);
+        v[q] = x;
+    }
+    for (uint64_t q = nv * 16 + tid; q < n; q += stride) {
+        const uint32_t a = (cur - lin[q]) & 0xFFu;
+        lin[q] = static_cast<uint8_t>(a < expired ? a : expired);
+    }
+}
+
+// Histogram of one row's stamps (after an import). grid-stride, 256 bins.
+__global__ void __launch_bounds__(256) k_row_hist(const uint8_t* __restrict__ row, uint64_t n,
+                                                  unsigned long long* __restrict__ hist) {
+    __shared__ uint32_t s_h[256];
+    s_h[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(&s_h[row[q]], 1u);
+    __syncthreads();
+    if (s_h[threadIdx.x]) atomicAdd(hist + threadIdx.x, static_cast<unsigned long long>(s_h[threadIdx.x]));
+}
+
+// Union linear weight over epoch stamps: slot j counts iff every row's stamp
+// is younger than k (max over rows of the recorder value < k).
+template <int MAXR>
+__global__ void __launch_bounds__(256) k_union_linear_epoch(const uint32_t* __restrict__ hosts, uint32_t n, DevCfg c,
+                                                            const uint8_t* __restrict__ lin, uint32_t cur,
+                                                            uint32_t* __restrict__ weight) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    const uint64_t lrow = static_cast<uint64_t>(c.cols) * c.gl;
+    const uint32_t cur4 = cur * 0x01010101u, k4 = c.k * 0x01010101u;
+    const bool vec = (c.gl & 15u) == 0;
+    for (uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < n; h += warps) {
+        const uint32_t a = hosts[h];
+        const uint8_t* cell[MAXR];
+#pragma unroll
+        for (int i = 0; i < MAXR; ++i)
+            if (i < static_cast<int>(c.rows)) cell[i] = lin + i * lrow + static_cast<uint64_t>(column_of(c, i, a)) * c.gl;
+        uint32_t acc = 0;
+        if (vec) {
+            const uint32_t nv = c.gl / 16;
+            for (uint32_t q = lane; q < nv; q += 32) {
+                uint4 m = make_uint4(~0u, ~0u, ~0u, ~0u);
+#pragma unroll
+                for (int i = 0; i < MAXR; ++i) {
+                    if (i >= static_cast<int>(c.rows)) break;
+                    const uint4 x = __ldg(reinterpret_cast<const uint4*>(cell[i]) + q);
+                    m.x &= __vcmpltu4(__vsub4(cur4, x.x), k4);
+                    m.y &= __vcmpltu4(__vsub4(cur4, x.y), k4);
+                    m.z &= __vcmpltu4(__vsub4(cur4, x.z), k4);
+                    m.w &= __vcmpltu4(__vsub4(cur4, x.w), k4);
+                }
+                acc += __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
+            }
+            acc >>= 3;
+        } else {
+            for (uint32_t j = lane; j < c.gl; j += 32) {
+                bool all = true;
+                for (uint32_t i = 0; i < c.rows; ++i) all &= ((cur - cell[i < MAXR ? i : 0][j]) & 0xFFu) < c.k;
+                acc += all;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+        if (lane == 0) weight[h] = acc;
+    }
+}
+
+}  // namespace srla

@@ -528,3 +528,25 @@ __global__ void k_fill(W* __restrict__ t, uint64_t words, W value) {
 }
 
 }  // namespace srla
+
+namespace srla {
+
+// Report entries (srla_entry, 24 bytes) from sorted hosts + union weights and
+// the host-built Eq. 9 LUT (bit-identical glibc log1p, host_math.cpp), into a
+// device staging buffer that one DMA copies to the caller's pinned memory.
+__global__ void __launch_bounds__(256) k_map_entries(const uint32_t* __restrict__ hosts,
+                                                     const uint32_t* __restrict__ weight, uint32_t n,
+                                                     const double* __restrict__ est,
+                                                     const uint8_t* __restrict__ has,
+                                                     const uint8_t* __restrict__ sup,
+                                                     unsigned long long* __restrict__ out) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const uint32_t w = weight[e];
+        unsigned long long* o = out + 3ull * e;
+        o[0] = static_cast<unsigned long long>(hosts[e]) | (static_cast<unsigned long long>(w) << 32);
+        o[1] = static_cast<unsigned long long>(__double_as_longlong(est[w]));
+        o[2] = static_cast<unsigned long long>(has[w]) | (static_cast<unsigned long long>(sup[w]) << 8);
+    }
+}
+
+}  // namespace srla

@@ -33,6 +33,39 @@ constexpr int kBinRows = 4;                                 // rows handled by t
 constexpr int kBinEntries = kBinTile * kBinRows;
 constexpr int kMaxRegions = 1024;
 
+// Epoch-stamp mode of the linear table (epoch.cuh): marks write the current
+// epoch instead of 0 and keep per-row stamp histograms.
+struct EpochCfg {
+    uint32_t on;
+    uint32_t cur;
+    unsigned long long* hist;  // rows x 256
+    uint64_t row_words;
+};
+
+// set byte `off` of the 32-bit-aligned table to `cur`; returns the old byte
+__device__ __forceinline__ uint32_t stamp_byte_global(uint8_t* base, uint64_t off, uint32_t cur) {
+    unsigned int* w = reinterpret_cast<unsigned int*>(base + (off & ~3ull));
+    const uint32_t sh = 8u * static_cast<uint32_t>(off & 3u);
+    unsigned int old = *w, assumed;
+    do {
+        assumed = old;
+        if (((assumed >> sh) & 0xFFu) == cur) return cur;
+        old = atomicCAS(w, assumed, (assumed & ~(0xFFu << sh)) | (cur << sh));
+    } while (old != assumed);
+    return (old >> sh) & 0xFFu;
+}
+
+// Overflow path (bin full): stamp directly in HBM and account the histogram.
+__device__ __forceinline__ void mark_epoch_global(uint8_t* lin, uint64_t word, uint64_t row_words, uint32_t cur,
+                                                  unsigned long long* hist) {
+    const uint32_t old = stamp_byte_global(lin, word, cur);
+    if (old != cur) {
+        unsigned long long* h = hist + (word / row_words) * 256;
+        atomicAdd(h + old, ~0ull);  // -1
+        atomicAdd(h + cur, 1ull);
+    }
+}
+
 // "store 0" into one recorder word (recorder_mark) as a 32-bit AND, which the
 // L2 executes ~1.6x faster than a byte store.
 template <typename W>
@@ -51,7 +84,7 @@ __device__ __forceinline__ void mark_word(W* base, uint32_t off) {
 // append events exactly as k_scan does.
 template <typename W>
 __global__ void __launch_bounds__(kBinThreads, 3) k_scan_bin(const uint32_t* __restrict__ recs, uint32_t n, DevCfg c,
-                                                         BinCfg b, W* __restrict__ lin,
+                                                         BinCfg b, EpochCfg ep, W* __restrict__ lin,
                                                          uint32_t* __restrict__ stamp, uint32_t* __restrict__ ev,
                                                          uint32_t ev_cap, uint32_t* __restrict__ ev_count, int vec) {
     __shared__ uint32_t s_cnt[kMaxRegions];
@@ -184,7 +217,10 @@ __global__ void __launch_bounds__(kBinThreads, 3) k_scan_bin(const uint32_t* __r
             const uint32_t j = idx - s_lbase[r];
             if (j < s_fit[r]) {
                 b.bins[s_dst[r] + j] = s_off[idx];
-            } else {  // bin full: mark directly (marks commute)
+            } else if (ep.on) {  // bin full: mark directly (marks commute)
+                mark_epoch_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << b.region_shift) + s_off[idx],
+                                  ep.row_words, ep.cur, ep.hist);
+            } else {
                 mark_word<W>(lin + (static_cast<uint64_t>(r) << b.region_shift), s_off[idx]);
             }
         }
@@ -282,12 +318,16 @@ template <typename W>
 __global__ void __launch_bounds__(kSplitThreads) k_split(const uint32_t* __restrict__ coarse, uint32_t coarse_cap,
                                                          const uint32_t* __restrict__ tile_prefix,
                                                          const uint32_t* __restrict__ coarse_n, uint32_t nregions,
-                                                         uint32_t region_shift, FineCfg f, W* __restrict__ lin) {
-    __shared__ uint32_t s_cnt[kMaxRegions];
-    __shared__ uint32_t s_lbase[kMaxRegions];
-    __shared__ uint16_t s_fit[kMaxRegions];
-    __shared__ uint32_t s_dst[kMaxRegions];    // nfine * cap < 2^32 by construction (Engine::setup_bins)
-    __shared__ uint32_t s_sorted[kSplitTile];  // (slice << 16) | offset within slice
+                                                         uint32_t region_shift, FineCfg f, EpochCfg ep,
+                                                         W* __restrict__ lin) {
+    // dynamic shared memory, sized by the fan-out f.per_region (<= 4096):
+    //   sorted[kSplitTile] | cnt[P] | lbase[P] | dst[P] | fit[P] (u16)
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t* s_sorted = s_dyn;  // (slice << 16) | offset within slice
+    uint32_t* s_cnt = s_sorted + kSplitTile;
+    uint32_t* s_lbase = s_cnt + f.per_region;
+    uint32_t* s_dst = s_lbase + f.per_region;  // nfine * cap < 2^32 by construction (Engine::setup_bins)
+    uint16_t* s_fit = reinterpret_cast<uint16_t*>(s_dst + f.per_region);
     __shared__ uint32_t s_warp[kSplitThreads / 32];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t total_tiles = tile_prefix[nregions];
@@ -365,7 +405,12 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(const uint32_t* __restr
             const uint32_t j = i - s_lbase[b];
             if (j < s_fit[b]) {
                 f.bins[s_dst[b] + j] = static_cast<uint16_t>(v);
-            } else {  // fine bin full: mark in place (marks commute)
+            } else if (ep.on) {  // fine bin full: mark in place (marks commute)
+                mark_epoch_global(reinterpret_cast<uint8_t*>(lin),
+                                  (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift) +
+                                      (v & 0xFFFFu),
+                                  ep.row_words, ep.cur, ep.hist);
+            } else {
                 mark_word<W>(lin + (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift),
                              v & 0xFFFFu);
             }

@@ -38,7 +38,7 @@ class CConfig(C.Structure):
     _fields_ = [
         ("rows", C.c_uint32), ("cols", C.c_uint32), ("rough_slots", C.c_uint32),
         ("linear_slots", C.c_uint32), ("recorder_bits", C.c_uint32), ("window", C.c_uint32),
-        ("theta", C.c_uint32), ("reserved", C.c_uint32), ("fill_ratio", C.c_double),
+        ("theta", C.c_uint32), ("flags", C.c_uint32), ("fill_ratio", C.c_double),
         ("seed", C.c_uint64),
     ]
 

@@ -39,11 +39,14 @@ def test_engine_matches_reference_golden(gpu, oracle, name):
     assert msg is None, msg
 
 
+@pytest.mark.parametrize("epoch", ["1", "0"])
 @pytest.mark.parametrize("name", [n for n in sorted(S.SCENARIOS) if S.SCENARIOS[n][0].rows <= 4])
-def test_binned_marks_match_reference_golden(gpu, oracle, name, monkeypatch):
+def test_binned_marks_match_reference_golden(gpu, oracle, name, epoch, monkeypatch):
     """Same goldens with the binned linear-mark path forced on (~8 regions,
-    tiny bins so the overflow-to-direct-mark path runs too)."""
+    tiny bins so the overflow-to-direct-mark path runs too), with epoch-stamp
+    recorders (z <= 7) and with literal ones."""
     monkeypatch.setenv("SRLA_FORCE_BINS", "1")
+    monkeypatch.setenv("SRLA_EPOCH", epoch)
     g = json.load(open(os.path.join(GOLD, f"{name}.json")))
     cfg, _ = S.SCENARIOS[name]
     slices = GF.scenario_slices(name, oracle)
@@ -272,8 +275,9 @@ def test_device_generator_byte_identical(gpu, oracle):
         assert np.array_equal(got, want[2])
 
 
-@pytest.mark.parametrize("name", ["pipeline_small_3000", "c1_shape", "drift_evict"])
-def test_async_end_slice_matches_sync(gpu, oracle, name):
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("name", ["pipeline_small_3000", "c1_shape", "drift_evict", "contended"])
+def test_async_end_slice_matches_sync(gpu, oracle, name, pinned):
     """srla_end_slice_async + the next slice's host scan (copies overlapping the
     end-of-slice work) give the reference pipeline's reports and state."""
     from oracle.pyoracle import SeaConfig as OCfg
@@ -283,7 +287,12 @@ def test_async_end_slice_matches_sync(gpu, oracle, name):
     pipe = oracle.pipeline(OCfg(**cfg.as_dict()))
     want = [pipe.process_slice(s, r, True) for s, r in enumerate(slices)]
     e = engine(cfg)
-    bufs = [np.zeros(200000, ENTRY_DTYPE) for _ in range(2)]
+    if pinned:  # report entries mapped on the device straight into pinned memory (>= 16k entries)
+        import torch
+        bufs = [torch.zeros(200000 * 24, dtype=torch.uint8, pin_memory=True).numpy().view(ENTRY_DTYPE)
+                for _ in range(2)]
+    else:
+        bufs = [np.zeros(200000, ENTRY_DTYPE) for _ in range(2)]
     got = []
     for s, recs in enumerate(slices):
         e.scan(recs)
@@ -303,3 +312,73 @@ def test_async_end_slice_matches_sync(gpu, oracle, name):
                               w["estimate"].view(np.uint64)[w["has_estimate"] == 1]), s
         assert np.array_equal(g["is_super"], w["is_super"]), s
     assert np.array_equal(e.candidates(), pipe.candidates())
+
+
+@pytest.mark.parametrize("bits,window", [(4, 5), (7, 100), (3, 7)])
+def test_epoch_stamps_survive_counter_wrap(gpu, oracle, bits, window, monkeypatch):
+    """600 slides (the u8 epoch counter wraps twice): hosts fall silent for
+    hundreds of slices, so only the sweep keeps old stamps from aliasing."""
+    monkeypatch.setenv("SRLA_FORCE_BINS", "1")
+    cfg = S.Cfg(rows=2, cols=64, rough_slots=8, linear_slots=32, recorder_bits=bits, window=window, theta=16,
+                seed=0xE90C + bits)
+    rng = np.random.default_rng(bits)
+    slices = []
+    for s in range(600):
+        n = int(rng.integers(0, 60)) if (s // 97) % 2 == 0 else int(rng.integers(0, 4))
+        r = np.zeros((n, 3), np.uint32)
+        r[:, 1] = 0x0A000000 + rng.integers(0, 40, n)
+        r[:, 2] = 0xB0000000 + rng.integers(0, 300, n)
+        slices.append(r)
+    a = GF.run_flow(_oracle_backend(oracle, cfg), cfg, slices)
+    b = GF.run_flow(GF.EngineBackend(engine(cfg)), cfg, slices)
+    msg = GF.compare(a, b)
+    assert msg is None, msg
+
+
+def test_epoch_import_out_of_model_values_falls_back_to_literal(gpu, oracle, monkeypatch):
+    """Recorder values above `expired` (possible through the row spans) are
+    outside the epoch model: the engine converts to literal recorders."""
+    from paper_1803_10369_b200.srla import LINEAR
+    monkeypatch.setenv("SRLA_FORCE_BINS", "1")
+    cfg = S.Cfg(rows=2, cols=64, rough_slots=8, linear_slots=32, recorder_bits=4, window=5, theta=16, seed=77)
+    e, o = engine(cfg), _oracle_backend(oracle, cfg)
+    slices = S.random_slices(3, 6, (100, 400), 30, 200)
+    for s in slices[:3]:
+        e.scan_collect(s)
+        o.scan(s)
+    row = e.export_row(1, LINEAR)
+    assert np.array_equal(row, o.sk.export_row(1, LINEAR))
+    row[::7] = 200  # > expired = 15
+    e.import_row(1, LINEAR, row)
+    o.sk.import_row(1, LINEAR, row)
+    rest = GF.run_flow(GF.EngineBackend(e), cfg, slices[3:])
+    want = GF.run_flow(o, cfg, slices[3:])
+    assert GF.compare(want, rest) is None
+
+
+def test_large_report_mapped_on_device_into_pinned_buffer(gpu, oracle):
+    """>16k report entries: estimates are mapped on the GPU from the host LUT and
+    written straight into a pinned caller buffer (UVA); must equal the reference."""
+    import torch
+    from oracle.pyoracle import SeaConfig as OCfg
+    from paper_1803_10369_b200.srla import ENTRY_DTYPE
+    cfg = S.Cfg(rows=2, cols=65536, rough_slots=8, linear_slots=64, recorder_bits=4, window=3, theta=8, seed=0x51A)
+    slices = S.random_slices(8, 5, (200000, 200000), 50000, 1000)
+    pipe = oracle.pipeline(OCfg(**cfg.as_dict()))
+    e = engine(cfg)
+    buf = torch.zeros(100000 * 24, dtype=torch.uint8, pin_memory=True).numpy().view(ENTRY_DTYPE)
+    seen_large = False
+    for s, recs in enumerate(slices):
+        w = pipe.process_slice(s, recs, True)
+        e.scan(recs)
+        e.end_slice_async(s, buf)
+        n, _ = e.end_slice_wait()
+        if w is None:
+            continue
+        seen_large |= n >= (1 << 14)
+        g = buf[:n]
+        assert np.array_equal(g["host"], w["host"]) and np.array_equal(g["union_weight"], w["weight"])
+        m = w["has_estimate"] == 1
+        assert np.array_equal(g["has_estimate"], w["has_estimate"]) and np.array_equal(g["is_super"], w["is_super"])
+        assert np.array_equal(g["estimate"].view(np.uint64)[m], w["estimate"].view(np.uint64)[m])
+    assert seen_large

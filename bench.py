@@ -239,18 +239,30 @@ def run_engine(args):
     def allgather_report(entries):
         return entries if world == 1 else _allgather(entries, dist, torch.device("cuda", local))
 
-    def step(sid, host=None):
-        recs = host[sid % len(host)] if host is not None else slices[sid % nres]
-        if host is not None:
-            eng.scan(recs)
-        else:
-            eng.scan(recs)
+    def step(sid):
+        eng.scan(slices[sid % nres])
         n, nr = _end_slice(eng, sid, rep_buf)
-        return allgather_report(rep_buf[:n]), n
+        if world > 1:
+            if args.handoff == "compact":  # rebuild entries for the all-gather
+                ent = np.zeros(n, srla.ENTRY_DTYPE)
+                ent["host"], ent["union_weight"] = comp_hosts[:n], comp_w[:n]
+                ent["estimate"] = comp_est[comp_w[:n]]
+                ent["has_estimate"], ent["is_super"] = comp_flags[comp_w[:n]] & 1, comp_flags[comp_w[:n]] >> 1
+                return allgather_report(ent), n
+            return allgather_report(rep_buf[:n]), n
+        return None, n
 
     import ctypes as C
 
+    L = cfg.linear_slots + 1
+    comp_hosts = torch.empty(rep_cap * 4, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint32)
+    comp_w = torch.empty(rep_cap * 4, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint32)
+    comp_est, comp_flags = np.empty(L, np.float64), np.empty(L, np.uint8)
+
     def _end_slice(e, sid, buf):
+        if args.handoff == "compact":  # hosts + weights (8 B/entry) + the window's Eq. 9 table
+            n, nr = e.end_slice_compact(sid, comp_hosts, comp_w, comp_est, comp_flags)
+            return n, nr
         n, nr = C.c_uint64(), C.c_uint64()
         srla._check(srla._lib.srla_end_slice(e._h, sid, 1, C.c_void_p(buf.ctypes.data), len(buf), C.byref(n),
                                              C.byref(nr)))
@@ -370,6 +382,8 @@ def run_engine(args):
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference generator C2 spec, device port)",
             "config": {"workload": WORKLOADS[args.workload],
                        "packets_per_slice_per_gpu": n_per_gpu, "resident_slices": nres,
+                       "report_handoff": "srla_end_slice_compact: host+weight per entry and the Eq. 9 table"
+                       if args.handoff == "compact" else "srla_end_slice: 24-byte srla_entry per entry",
                        "l2": "inputs larger than L2 (1.2 GB per slice); no flush",
                        "parallelism": f"owner-partitioned x{world}" if world > 1 else "1 GPU"},
             "end_of_slice_ms": {"device_median": statistics.median(eos_dev),
@@ -409,6 +423,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--handoff", default="compact", choices=["compact", "entries"],
+                    help="report hand-off of the device-resident steps (e2e always returns srla_entry)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

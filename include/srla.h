@@ -150,6 +150,15 @@ srla_status srla_end_slice_async(srla_engine* e, uint64_t slice_id, int want_rep
                                  uint64_t cap);
 srla_status srla_end_slice_wait(srla_engine* e, uint64_t* n_out, uint64_t* n_retained);
 
+/* srla_end_slice with the report handed off compactly: hosts (ascending) and
+ * union weights (8 bytes per entry instead of 24) plus this window's Eq. 9
+ * table over the g'+1 possible weights: estimate = est_lut[w], has_estimate =
+ * flags_lut[w] & 1, is_super = (flags_lut[w] >> 1) & 1. Same results as the
+ * srla_entry form (sea.hpp:296-305). */
+srla_status srla_end_slice_compact(srla_engine* e, uint64_t slice_id, int want_report, uint32_t* hosts,
+                                   uint32_t* weights, uint64_t cap, uint64_t* n_out, double* est_lut,
+                                   uint8_t* flags_lut, uint64_t* n_retained);
+
 /* union_rough_weight / union_linear_weight (sea.hpp:219-243) per host; either
  * output may be NULL. */
 srla_status srla_union_weights(srla_engine* e, const uint32_t* hosts, uint64_t n,

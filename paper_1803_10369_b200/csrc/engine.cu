@@ -92,6 +92,14 @@ struct PinBuf {
 };
 
 struct Engine {
+    // compact report hand-off (srla_end_slice_compact)
+    struct Compact {
+        uint32_t* hosts;
+        uint32_t* weights;
+        double* est;
+        uint8_t* flags;
+    };
+
     srla_config cfg{};
     int device = 0;
     cudaStream_t st = nullptr;
@@ -125,6 +133,9 @@ struct Engine {
     cudaStream_t st2 = nullptr; // end-of-slice side stream (rough aging overlaps the report)
     cudaEvent_t ev_eos_start = nullptr, ev_rough_aged = nullptr;
     bool rough_preaged = false;
+    cudaEvent_t ev_retained = nullptr;
+    bool retained_early = false;
+    DevBuf<uint8_t> temp2;  // CUB scratch of the side stream
     cudaEvent_t ev_copied[2] = {}, ev_scanned[2] = {};
     cudaEvent_t t_scan0 = nullptr, t_scan1 = nullptr, t_eos0 = nullptr, t_eos1 = nullptr;
     srla_timing timing{};
@@ -176,6 +187,7 @@ struct Engine {
         CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ev_eos_start, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_rough_aged, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_retained, cudaEventDisableTiming));
         for (int b = 0; b < 2; ++b) {
             CK(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ev_scanned[b], cudaEventDisableTiming));
@@ -245,6 +257,7 @@ struct Engine {
         }
         if (ev_eos_start) cudaEventDestroy(ev_eos_start);
         if (ev_rough_aged) cudaEventDestroy(ev_rough_aged);
+        if (ev_retained) cudaEventDestroy(ev_retained);
         if (st) cudaStreamDestroy(st);
     }
 
@@ -306,11 +319,12 @@ struct Engine {
 
     // ------------------------------------------------------------ CUB helpers
     template <typename Fn>
-    void cub_call(Fn&& fn) {
+    void cub_call(Fn&& fn, DevBuf<uint8_t>* tbuf = nullptr) {
+        DevBuf<uint8_t>& t = tbuf ? *tbuf : temp;
         size_t bytes = 0;
         CK(fn(static_cast<void*>(nullptr), bytes));
-        temp.ensure(bytes + 16);
-        CK(fn(static_cast<void*>(temp.p), bytes));
+        t.ensure(bytes + 16);
+        CK(fn(static_cast<void*>(t.p), bytes));
         lib_launched();
     }
 
@@ -775,10 +789,10 @@ struct Engine {
         });
     }
 
-    void timed_end_slice(uint64_t slice_id, bool want_report, srla_entry* out) {
+    void timed_end_slice(uint64_t slice_id, bool want_report, srla_entry* out, const Compact* compact = nullptr) {
         const auto w0 = std::chrono::steady_clock::now();
         CK(cudaEventRecord(t_eos0, st));
-        end_slice(slice_id, want_report, out);
+        end_slice(slice_id, want_report, out, compact);
         CK(cudaEventRecord(t_eos1, st));
         CK(cudaEventSynchronize(t_eos1));
         float ms = 0.f;
@@ -904,12 +918,12 @@ struct Engine {
     // holds the per-row active counts and the table has been aged by the fused
     // count+age pass, so union activity is tested with r < k+1 (exact while
     // k < expired: an aged recorder r' = r+1 for every r < expired).
-    void report(srla_entry* out, double* fp_out, bool counts_ready = false) {
+    void report(srla_entry* out, double* fp_out, bool counts_ready = false, const Compact* compact = nullptr) {
         const auto w0 = std::chrono::steady_clock::now();
         const uint32_t n = static_cast<uint32_t>(ncsip);
         cudaPointerAttributes oa{};
-        const bool out_pinned =
-            n >= (1u << 14) && cudaPointerGetAttributes(&oa, out) == cudaSuccess && oa.type == cudaMemoryTypeHost;
+        const bool out_pinned = !compact && n >= (1u << 14) && cudaPointerGetAttributes(&oa, out) == cudaSuccess &&
+                                oa.type == cudaMemoryTypeHost;
         cudaGetLastError();
         const uint32_t kthr = counts_ready ? cfg.window + 1 : cfg.window;
         if (!counts_ready) {
@@ -923,7 +937,10 @@ struct Engine {
                 return cub::DeviceRadixSort::SortKeys(t, b, csip.p, sorted_hosts.p, static_cast<int>(n), 0, 32, st);
             });
             union_linear(sorted_hosts.p, n, weights.p, kthr);
-            if (!out_pinned) {
+            if (compact) {  // hand off 8 bytes per entry: host + union weight
+                CK(cudaMemcpyAsync(compact->hosts, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(compact->weights, weights.p, n * 4ull, cudaMemcpyDeviceToHost, st));
+            } else if (!out_pinned) {
                 pin_hosts.ensure(n);
                 pin_w.ensure(n);
                 CK(cudaMemcpyAsync(pin_hosts.p, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, st));
@@ -945,7 +962,12 @@ struct Engine {
         srla_host::estimate_lut(cfg.linear_slots, fp, cfg.theta, lut_est.data(), lut_has.data(), lut_sup.data());
         // (host, weight) -> entries: on the device straight into a pinned
         // caller buffer, else on the host into pageable memory
-        if (out_pinned) {
+        if (compact) {
+            for (uint32_t w = 0; w <= cfg.linear_slots; ++w) {
+                compact->est[w] = lut_est[w];
+                compact->flags[w] = static_cast<uint8_t>(lut_has[w] | (lut_sup[w] << 1));
+            }
+        } else if (out_pinned) {
             const uint32_t L = cfg.linear_slots + 1;
             pin_lut.ensure(L * 10ull);
             double* le = reinterpret_cast<double*>(pin_lut.p);
@@ -1005,9 +1027,49 @@ struct Engine {
         rough_preaged = true;
     }
 
+    // Candidate re-validation on the side stream right after the rough aging,
+    // concurrent with the report (which reads the list but not rough or SI);
+    // slide_t collects the retained count and swaps the lists.
+    template <typename W, int MAXR>
+    void retain_early_t() {
+        if (!ncsip) return;
+        const uint32_t n = static_cast<uint32_t>(ncsip);
+        keep.ensure(n);
+        csip2.ensure(n);
+        k_retain<W, MAXR><<<blocks(n), 256, 0, st2>>>(csip.p, n, dc, static_cast<const W*>(d_rough), d_si, keep.p);
+        check_launch();
+        launched();
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceSelect::Flagged(t, b, csip.p, keep.p, csip2.p, ctr.p + 6, static_cast<int>(n), st2);
+        }, &temp2);
+        CK(cudaMemcpyAsync(pin_ctr.p + 6, ctr.p + 6, 4, cudaMemcpyDeviceToHost, st2));
+        CK(cudaEventRecord(ev_retained, st2));
+        retained_early = true;
+    }
+
     template <typename W, int MAXR>
     void slide_t(bool age_linear) {
         const uint64_t rows = cfg.rows;
+        if (retained_early) {
+            CK(cudaEventSynchronize(ev_retained));
+            CK(cudaStreamWaitEvent(st, ev_retained, 0));
+            retained_early = false;
+            rough_preaged = false;
+            if (age_linear) {
+                k_age<W><<<blocks(rows * lin_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_lin), rows * lin_words, dc.expired);
+                check_launch();
+                launched();
+            }
+            if (ncsip) {
+                ncsip = pin_ctr.p[6];
+                std::swap(csip.p, csip2.p);
+                std::swap(csip.cap, csip2.cap);
+            }
+            trace("  slide: retain+select (early)");
+            rebuild_cset(ncsip);
+            trace("  slide: cset rebuild");
+            return;
+        }
         if (rough_preaged) {
             CK(cudaStreamWaitEvent(st, ev_rough_aged, 0));
             rough_preaged = false;
@@ -1061,14 +1123,19 @@ struct Engine {
     // process_slice tail (pipeline.hpp:119-128). When a report is due and
     // k < expired, one fused pass counts and ages the linear table, and the
     // report reads the aged table (see report()).
-    void end_slice(uint64_t slice_id, bool want_report, srla_entry* out) {
+    void end_slice(uint64_t slice_id, bool want_report, srla_entry* out, const Compact* compact = nullptr) {
         const bool due = want_report && slice_id + 1 >= cfg.window;
         const auto w0 = std::chrono::steady_clock::now();
         trace(nullptr);
-        with_w([&](auto w) { preage_rough_t<decltype(w)>(); });
+        with_w([&](auto w) {
+            using W = decltype(w);
+            preage_rough_t<W>();
+            if (cfg.rows <= 4) retain_early_t<W, 4>();
+            else retain_early_t<W, 64>();
+        });
         if (epoch) {
             flush_linear();
-            if (due) report(out, nullptr);
+            if (due) report(out, nullptr, false, compact);
             trace("eos: report (epoch)");
             slide(false);
             trace("eos: slide (epoch)");
@@ -1084,7 +1151,7 @@ struct Engine {
             }
             timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
             trace("eos: split+apply+count+age");
-            report(out, nullptr, true);
+            report(out, nullptr, true, compact);
             trace("eos: report");
             slide(false);
             trace("eos: slide");
@@ -1093,7 +1160,7 @@ struct Engine {
             timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
             slide(false);
         } else {
-            if (due) report(out, nullptr);
+            if (due) report(out, nullptr, false, compact);
             slide(true);
         }
     }
@@ -1403,6 +1470,23 @@ srla_status srla_end_slice(srla_engine* e, uint64_t slice_id, int want_report, s
         return s;
     }
     return srla_end_slice_wait(e, n_out, n_retained);
+}
+
+srla_status srla_end_slice_compact(srla_engine* e, uint64_t slice_id, int want_report, uint32_t* hosts,
+                                   uint32_t* weights, uint64_t cap, uint64_t* n_out, double* est_lut,
+                                   uint8_t* flags_lut, uint64_t* n_retained) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        auto& x = E(e);
+        const bool due = want_report && slice_id + 1 >= x.cfg.window;
+        if (n_out) *n_out = due ? x.ncsip : 0;
+        if (due && (x.ncsip > cap || ((!hosts || !weights) && x.ncsip)))
+            throw srla::Error(SRLA_E_CAPACITY, "report buffers too small");
+        if (due && (!est_lut || !flags_lut)) throw srla::Error(SRLA_E_INVALID, "null estimate table");
+        const srla::Engine::Compact c{hosts, weights, est_lut, flags_lut};
+        x.timed_end_slice(slice_id, want_report != 0, nullptr, &c);
+        if (n_retained) *n_retained = x.ncsip;
+    });
 }
 
 srla_status srla_end_slice_async(srla_engine* e, uint64_t slice_id, int want_report, srla_entry* out,

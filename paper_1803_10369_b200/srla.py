@@ -103,6 +103,7 @@ def load_library(path: str = LIB_PATH):
         "srla_slide": (i32, [vp, C.POINTER(u64)]),
         "srla_end_slice": (i32, [vp, u64, i32, vp, u64, C.POINTER(u64), C.POINTER(u64)]),
         "srla_end_slice_async": (i32, [vp, u64, i32, vp, u64]),
+        "srla_end_slice_compact": (i32, [vp, u64, i32, vp, vp, u64, C.POINTER(u64), vp, vp, C.POINTER(u64)]),
         "srla_end_slice_wait": (i32, [vp, C.POINTER(u64), C.POINTER(u64)]),
         "srla_union_weights": (i32, [vp, vp, u64, vp, vp]),
         "srla_union_view": (i32, [vp, u32, vp, vp, vp]),
@@ -136,7 +137,7 @@ EXPORTED_SYMBOLS = (
     "srla_row_bytes", "srla_export_row", "srla_import_row", "srla_stats_get", "srla_synchronize",
     "srla_stream", "srla_generator_create", "srla_generator_destroy", "srla_generate_slice",
     "srla_timing_get", "srla_timing_reset", "srla_partition_records", "srla_owner_of",
-    "srla_end_slice_async", "srla_end_slice_wait",
+    "srla_end_slice_async", "srla_end_slice_wait", "srla_end_slice_compact",
 )
 
 
@@ -344,6 +345,15 @@ class EstimatorArray:
     def end_slice_async(self, slice_id: int, out: np.ndarray, want_report: bool = True):
         """Start end-of-slice into `out` (ENTRY_DTYPE, kept alive by the caller)."""
         _check(_lib.srla_end_slice_async(self._h, slice_id, int(want_report), _ptr(out), len(out)))
+
+    def end_slice_compact(self, slice_id: int, hosts: np.ndarray, weights: np.ndarray, est: np.ndarray,
+                          flags: np.ndarray, want_report: bool = True):
+        """end_slice handing the report off as (hosts, weights) + Eq. 9 table.
+        Returns (entries written, retained candidates)."""
+        n, nr = C.c_uint64(), C.c_uint64()
+        _check(_lib.srla_end_slice_compact(self._h, slice_id, int(want_report), _ptr(hosts), _ptr(weights),
+                                           len(hosts), C.byref(n), _ptr(est), _ptr(flags), C.byref(nr)))
+        return n.value, nr.value
 
     def end_slice_wait(self):
         """-> (report entries written to the async buffer, retained candidates)."""

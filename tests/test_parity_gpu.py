@@ -382,3 +382,30 @@ def test_large_report_mapped_on_device_into_pinned_buffer(gpu, oracle):
         assert np.array_equal(g["has_estimate"], w["has_estimate"]) and np.array_equal(g["is_super"], w["is_super"])
         assert np.array_equal(g["estimate"].view(np.uint64)[m], w["estimate"].view(np.uint64)[m])
     assert seen_large
+
+
+@pytest.mark.parametrize("name", ["pipeline_small_3000", "contended", "drift_evict"])
+def test_compact_report_handoff(gpu, oracle, name):
+    """srla_end_slice_compact: hosts + weights + the window's Eq. 9 table give
+    the reference's entries exactly."""
+    from oracle.pyoracle import SeaConfig as OCfg
+    cfg, _ = S.SCENARIOS[name]
+    slices = GF.scenario_slices(name, oracle)
+    pipe = oracle.pipeline(OCfg(**cfg.as_dict()))
+    e = engine(cfg)
+    hosts, w = np.zeros(100000, np.uint32), np.zeros(100000, np.uint32)
+    est, flags = np.zeros(cfg.linear_slots + 1), np.zeros(cfg.linear_slots + 1, np.uint8)
+    for s, recs in enumerate(slices):
+        want = pipe.process_slice(s, recs, True)
+        e.scan(recs)
+        n, _ = e.end_slice_compact(s, hosts, w, est, flags)
+        if want is None:
+            assert n == 0
+            continue
+        assert np.array_equal(hosts[:n], want["host"]) and np.array_equal(w[:n], want["weight"])
+        has = flags[w[:n]] & 1
+        assert np.array_equal(has, want["has_estimate"])
+        assert np.array_equal(flags[w[:n]] >> 1, want["is_super"])
+        m = has == 1
+        assert np.array_equal(est[w[:n]][m].view(np.uint64), want["estimate"][m].view(np.uint64))
+    assert np.array_equal(e.candidates(), pipe.candidates())

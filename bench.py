@@ -122,6 +122,65 @@ class Clocks:
                 "samples": len(sm)}
 
 
+# ---------------------------------------------------------------- rooflines
+
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of each kernel,
+    from the committed ncu --set full summary (profiles/ncu_summary.json)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return {}
+    return {k: v.get("dram_bytes_per_launch") for k, v in json.load(open(p)).get("kernels", {}).items()}
+
+
+def kernel_rooflines(tm, step_ms_total, cfg, peak, peak_src, packets, steps):
+    """Per-kernel algorithmic bytes / device time (CUDA events on the engine
+    stream around every launch, summed over the timed steps).
+
+    K1 k_scan_bin: 12 B record + rows x 4 B bin entry per packet (the direct
+      k_scan: 12 B + rows x one 32-B sector update);
+    k_split: 4 B coarse entry read + 2 B fine entry written per mark;
+    apply (k_slice_apply_bulk / k_slice_stamp): 2 B fine entry per mark +
+      every streamed table slice read and written;
+    gather (k_union_linear): candidates x rows x g' x W.
+    The scan-path figure is SURVEY.md §8d's 140 B per packet (12 B record +
+    4 random 32-B sector updates) over K1 + split + apply time."""
+    binned = tm["split_kernel_launches"] > 0 or tm["apply_kernel_launches"] > 0
+    rows = cfg.rows
+    traffic = ncu_traffic()
+    ks = {
+        "k_scan_bin" if binned else "k_scan": (
+            tm["scan_kernel_ms"], tm["scan_kernel_launches"],
+            tm["scan_kernel_records"] * ((12 + 4 * rows) if binned else (12 + 32 * rows))),
+        "k_split": (tm["split_kernel_ms"], tm["split_kernel_launches"], tm["split_entries"] * 6),
+        "k_slice_apply": (tm["apply_kernel_ms"], tm["apply_kernel_launches"],
+                          tm["apply_entries"] * 2 + tm["apply_stream_bytes"]),
+        "k_union_linear": (tm["gather_kernel_ms"], tm["gather_kernel_launches"], tm["gather_bytes"]),
+    }
+    kernels = {}
+    for name, (kms, n, byts) in ks.items():
+        if n == 0 or kms <= 0:
+            continue
+        ach = byts / (kms * 1e-3) / 1e9
+        kernels[name] = {"ms_per_launch": kms / n, "launches": n, "algorithmic_bytes_per_launch": byts / n,
+                         "achieved": ach, "frac": ach / peak, "share_of_step": kms / step_ms_total,
+                         "traffic": traffic.get(name)}
+    dom = max(kernels, key=lambda k: kernels[k]["share_of_step"])
+    d = kernels[dom]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": d["achieved"], "peak": peak, "unit": "GB/s",
+                "frac": d["frac"], "traffic": d["traffic"], "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": d["algorithmic_bytes_per_launch"],
+                "ms_per_launch": d["ms_per_launch"], "share_of_step": d["share_of_step"]}
+    path_ms = sum(ks[k][0] for k in ks if k != "k_union_linear")
+    path = None
+    if path_ms > 0:
+        ach = packets * ALGO_BYTES_PER_PACKET / (path_ms * 1e-3) / 1e9
+        path = {"kernels": [k for k in ks if k != "k_union_linear"], "algorithmic_bytes_per_packet":
+                ALGO_BYTES_PER_PACKET, "ms_per_step": path_ms / steps, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak}
+    return roofline, kernels, path
+
+
 # ---------------------------------------------------------------- CPU reference (checker only)
 
 def cpu_reference(sample_recs, cols, threads, slice_id):
@@ -312,18 +371,8 @@ def run_engine(args):
         packets = pk[0].item()
     value = packets / (ms / 1e3)
 
-    # dominant kernel: K1 scan, CUDA events on the engine stream around each launch
-    launches = max(1, tm["scan_kernel_launches"])
-    recs_per_launch = tm["scan_kernel_records"] / launches
-    ms_per_launch = tm["scan_kernel_ms"] / launches
-    achieved = recs_per_launch * ALGO_BYTES_PER_PACKET / (ms_per_launch * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "scan_ncu_summary.json")
-    if os.path.exists(prof):
-        d = json.load(open(prof))
-        if d.get("dram_bytes_per_record"):
-            traffic = d["dram_bytes_per_record"] * recs_per_launch
+    roofline, kernels, path = kernel_rooflines(tm, ms, cfg, peak, peak_src, tm["scan_kernel_records"], args.steps)
 
     # end to end through the public API with host buffers (pinned), H2D inside:
     # scan_batch(host) + end_slice_async/wait, so a slice's host->device copies
@@ -391,11 +440,9 @@ def run_engine(args):
                                 "device_max": max(eos_dev), "samples": len(eos_dev),
                                 "wall_median": statistics.median(eos_wall), "report_entries_median":
                                     statistics.median(entries)},
-            "roofline": {"bound": "hbm", "kernel": "k_scan", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_packet": ALGO_BYTES_PER_PACKET,
-                         "packets_per_launch": recs_per_launch, "ms_per_launch": ms_per_launch,
-                         "share_of_step": tm["scan_kernel_ms"] / ms},
+            "roofline": roofline,
+            "kernels": kernels,
+            "roofline_scan_path": path,
             "breakdown_ms_per_step": {k: tm[k] / args.steps for k in
                                       ("scan_kernel_ms", "order_wall_ms", "report_wall_ms", "slide_wall_ms")},
             "cpu_baseline": cpu,

@@ -199,6 +199,17 @@ typedef struct srla_timing {
     double order_wall_ms;   /* K2..K5 + candidate append, per-chunk host wall, summed */
     double report_wall_ms;  /* report_window part of end-of-slice */
     double slide_wall_ms;   /* slide part of end-of-slice */
+    /* device time (CUDA events on the engine stream) of the other hot kernels */
+    double split_kernel_ms;       /* k_split: region bins -> fine slice bins */
+    uint64_t split_kernel_launches;
+    uint64_t split_entries;       /* linear marks re-binned */
+    double apply_kernel_ms;       /* k_slice_apply(_bulk) / k_slice_stamp */
+    uint64_t apply_kernel_launches;
+    uint64_t apply_entries;       /* linear marks applied */
+    uint64_t apply_stream_bytes;  /* table bytes read + written by whole-slice passes */
+    double gather_kernel_ms;      /* k_union_linear(_epoch): report union weights */
+    uint64_t gather_kernel_launches;
+    uint64_t gather_bytes;        /* candidates x rows x g' x W */
 } srla_timing;
 srla_status srla_timing_get(const srla_engine* e, srla_timing* out);
 srla_status srla_timing_reset(srla_engine* e);

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -112,7 +113,7 @@ struct Engine {
     uint32_t* d_stamp = nullptr;
     int sms = 148;
 
-    static constexpr uint32_t kChunk = 1u << 26;      // records per ordered chunk
+    static constexpr uint32_t kChunk = 1u << 27;      // records per ordered chunk (a C2 slice in one)
     static constexpr uint32_t kHostStage = 1u << 24;  // records per host->device hop
 
     DevBuf<uint32_t> ev;
@@ -131,10 +132,15 @@ struct Engine {
     PinBuf<uint32_t> pstage[2], pin_hosts, pin_w;
     cudaStream_t cs = nullptr;  // host->device copy stream
     cudaStream_t st2 = nullptr; // end-of-slice side stream (rough aging overlaps the report)
-    cudaEvent_t ev_eos_start = nullptr, ev_rough_aged = nullptr;
-    bool rough_preaged = false;
-    cudaEvent_t ev_retained = nullptr;
-    bool retained_early = false;
+    cudaEvent_t ev_eos_start = nullptr, ev_reported = nullptr, ev_retained = nullptr;
+    bool slide_begun = false;
+    // report hand-off: device->host copies on their own stream
+    static constexpr uint32_t kReportParts = 4;
+    cudaStream_t ds = nullptr;
+    cudaEvent_t ev_sorted = nullptr, ev_d2h = nullptr, ev_part[kReportParts] = {};
+    // table maintenance queued on st2 by slide_finish (join_maint)
+    cudaEvent_t ev_maint_lin = nullptr, ev_maint = nullptr;
+    bool maint_lin_pending = false, maint_pending = false;
     DevBuf<uint8_t> temp2;  // CUB scratch of the side stream
     cudaEvent_t ev_copied[2] = {}, ev_scanned[2] = {};
     cudaEvent_t t_scan0 = nullptr, t_scan1 = nullptr, t_eos0 = nullptr, t_eos1 = nullptr;
@@ -173,10 +179,81 @@ struct Engine {
     DevBuf<unsigned long long> hist;  // rows x 256
     PinBuf<unsigned long long> pin_hist;
     uint64_t sweep_pos = 0;
+    // slices with at most this many marks are stamped in place (epoch.cuh)
+    uint32_t sparse_max = 0;
     EpochCfg ecfg() const { return EpochCfg{epoch ? 1u : 0u, cur_epoch, hist.p, lin_words}; }
     PinBuf<uint32_t> pin_bc;
     uint64_t pending_entries = 0;
     bool prefetch_next = false;  // bulk-prefetch region r+1 while applying r (measured slower; off)
+
+    // ------------------------------------------------------------ kernel timers
+    // Device time of the split / apply / gather kernels: event pairs on the
+    // engine stream, resolved after the stream has passed them.
+    enum TimerKind { kTimeSplit = 0, kTimeApply = 1, kTimeGather = 2 };
+    struct PendingTimer {
+        cudaEvent_t a, b;
+        int kind;
+    };
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<PendingTimer> timers;
+    DevBuf<unsigned long long> d_streamed;  // FineCfg::streamed
+    PinBuf<unsigned long long> pin_streamed;
+    cudaEvent_t take_event() {
+        if (ev_pool.empty()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = ev_pool.back();
+        ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t timer_start() {
+        cudaEvent_t a = take_event();
+        CK(cudaEventRecord(a, st));
+        return a;
+    }
+    void timer_stop(cudaEvent_t a, int kind) {
+        cudaEvent_t b = take_event();
+        CK(cudaEventRecord(b, st));
+        timers.push_back({a, b, kind});
+        if (timers.size() > 256) resolve_timers(true);
+    }
+    void resolve_timers(bool wait) {
+        size_t keep = 0;
+        for (size_t i = 0; i < timers.size(); ++i) {
+            PendingTimer& t = timers[i];
+            if (!wait && cudaEventQuery(t.b) != cudaSuccess) {
+                cudaGetLastError();
+                timers[keep++] = t;
+                continue;
+            }
+            CK(cudaEventSynchronize(t.b));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, t.a, t.b));
+            (t.kind == kTimeSplit ? timing.split_kernel_ms : t.kind == kTimeApply ? timing.apply_kernel_ms
+                                                                                 : timing.gather_kernel_ms) += ms;
+            ev_pool.push_back(t.a);
+            ev_pool.push_back(t.b);
+        }
+        timers.resize(keep);
+    }
+    // Non-blocking: timers the stream has not reached yet are reported later
+    // (the streamed-slice count is the device counter as of the last flush).
+    void timing_snapshot(srla_timing* out) {
+        resolve_timers(false);
+        *out = timing;
+        if (pin_streamed.p) out->apply_stream_bytes = 2ull * pin_streamed.p[0] * ((1ull << fcfg.shift) * wb);
+    }
+    void timing_clear() {
+        resolve_timers(true);
+        timing = srla_timing{};
+        if (d_streamed.p) {
+            CK(cudaMemsetAsync(d_streamed.p, 0, sizeof(unsigned long long), st));
+            CK(cudaStreamSynchronize(st));
+            pin_streamed.p[0] = 0;
+        }
+    }
 
     // ------------------------------------------------------------ lifecycle
     explicit Engine(const srla_config& c, int dev) : cfg(c), device(dev) {
@@ -186,8 +263,10 @@ struct Engine {
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ev_eos_start, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_rough_aged, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_retained, cudaEventDisableTiming));
+        for (cudaEvent_t* e : {&ev_reported, &ev_retained, &ev_maint_lin, &ev_maint, &ev_sorted, &ev_d2h})
+            CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        for (cudaEvent_t& e : ev_part) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
         for (int b = 0; b < 2; ++b) {
             CK(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ev_scanned[b], cudaEventDisableTiming));
@@ -239,6 +318,8 @@ struct Engine {
     ~Engine() {
         if (eos_thread.joinable()) eos_thread.join();
         if (st) cudaStreamSynchronize(st);
+        if (st2) cudaStreamSynchronize(st2);  // queued slide maintenance
+        if (ds) cudaStreamSynchronize(ds);
         if (d_lin) cudaFree(d_lin);
         if (d_rough) cudaFree(d_rough);
         if (d_si) cudaFree(d_si);
@@ -250,14 +331,24 @@ struct Engine {
         }
         for (cudaEvent_t e : {t_scan0, t_scan1, t_eos0, t_eos1})
             if (e) cudaEventDestroy(e);
+        for (const PendingTimer& t : timers) {
+            cudaEventDestroy(t.a);
+            cudaEventDestroy(t.b);
+        }
+        for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
         if (cs) cudaStreamDestroy(cs);
         if (st2) {
             cudaStreamSynchronize(st2);
             cudaStreamDestroy(st2);
         }
-        if (ev_eos_start) cudaEventDestroy(ev_eos_start);
-        if (ev_rough_aged) cudaEventDestroy(ev_rough_aged);
-        if (ev_retained) cudaEventDestroy(ev_retained);
+        for (cudaEvent_t e : {ev_eos_start, ev_reported, ev_retained, ev_maint_lin, ev_maint, ev_sorted, ev_d2h})
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_part)
+            if (e) cudaEventDestroy(e);
+        if (ds) {
+            cudaStreamSynchronize(ds);
+            cudaStreamDestroy(ds);
+        }
         if (st) cudaStreamDestroy(st);
     }
 
@@ -331,16 +422,17 @@ struct Engine {
     static int bit_length(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 1; }
 
     // ------------------------------------------------------------ candidate set
-    void rebuild_cset(uint64_t want) {
+    void rebuild_cset(uint64_t want, cudaStream_t s = nullptr) {
+        if (!s) s = st;
         uint64_t cap = 1024;
         while (cap < 2 * want) cap <<= 1;
         if (cap != cset_cap) {
             cset.ensure(cap);
             cset_cap = cap;
         }
-        CK(cudaMemsetAsync(cset.p, 0, cset_cap * sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(cset.p, 0, cset_cap * sizeof(unsigned long long), s));
         if (ncsip) {
-            k_cset_insert<<<blocks(ncsip), 256, 0, st>>>(csip.p, static_cast<uint32_t>(ncsip), cset.p, cset_cap - 1);
+            k_cset_insert<<<blocks(ncsip), 256, 0, s>>>(csip.p, static_cast<uint32_t>(ncsip), cset.p, cset_cap - 1);
             check_launch();
             launched();
         }
@@ -412,6 +504,11 @@ struct Engine {
         fine_count.ensure(fcfg.nfine);
         fcfg.bins = fine_bins.p;
         fcfg.count = fine_count.p;
+        d_streamed.ensure(1);
+        pin_streamed.ensure(1);
+        pin_streamed.p[0] = 0;
+        CK(cudaMemsetAsync(d_streamed.p, 0, sizeof(unsigned long long), st));
+        fcfg.streamed = d_streamed.p;
         CK(cudaMemsetAsync(fine_count.p, 0, fine_count.cap * sizeof(uint32_t), st));
         const int smem = static_cast<int>((1ull << fs) * wb);
         split_smem = kSplitTile * 4 + fcfg.per_region * 14;
@@ -442,6 +539,8 @@ struct Engine {
         if (lin_words < (1ull << fcfg.shift)) return;  // a slice may span at most two rows
         epoch = true;
         cur_epoch = 0;
+        sparse_max = (1u << fcfg.shift) / 128;
+        if (const char* sm = std::getenv("SRLA_SPARSE_MAX")) sparse_max = static_cast<uint32_t>(std::strtoul(sm, nullptr, 10));
         hist.ensure(uint64_t(cfg.rows) * 256);
         pin_hist.ensure(uint64_t(cfg.rows) * 256);
         CK(cudaMemsetAsync(hist.p, 0, uint64_t(cfg.rows) * 256 * sizeof(unsigned long long), st));
@@ -482,21 +581,6 @@ struct Engine {
         }
     }
 
-    void slide_epoch_tables() {
-        cur_epoch = (cur_epoch + 1) & 0xFFu;
-        k_zero_hist_bin<<<1, 64, 0, st>>>(hist.p, cfg.rows, cur_epoch);
-        check_launch();
-        const uint64_t total = uint64_t(cfg.rows) * lin_words;
-        const uint64_t period = 255 - dc.expired;                  // slides between visits of a byte
-        const uint64_t chunk = ((total + period - 1) / period + 15) & ~15ull;
-        const uint64_t end = std::min(total, sweep_pos + chunk);
-        k_sweep<<<blocks((end - sweep_pos) / 16 + 1, 256, 8), 256, 0, st>>>(static_cast<uint8_t*>(d_lin), sweep_pos,
-                                                                           end - sweep_pos, cur_epoch, dc.expired);
-        check_launch();
-        launched(2);
-        sweep_pos = end >= total ? 0 : end;
-    }
-
     // Age (and optionally count) linear words [w0, w1) — split at row
     // boundaries so each piece counts into its own row (non-binned tables).
     template <typename W>
@@ -517,6 +601,7 @@ struct Engine {
     // row into d_counts (pre-age) + age. One streaming pass over the table.
     void flush_linear(int mode = 0) {
         if (!use_bins) return;
+        join_maint_lin();
         if (pending_entries == 0 && mode == 0) return;
         const uint64_t total = uint64_t(cfg.rows) * lin_words;
         const uint32_t R = bcfg.nregions;
@@ -536,6 +621,7 @@ struct Engine {
             prefix[R] = run;
             CK(cudaMemcpyAsync(tile_prefix.p, pin_bc.p, (2 * R + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
             if (run) {
+                const cudaEvent_t t0 = timer_start();
                 with_w([&](auto w) {
                     using W = decltype(w);
                     k_split<W><<<std::min<uint32_t>(run, sms * 8), kSplitThreads, split_smem, st>>>(
@@ -544,16 +630,27 @@ struct Engine {
                 });
                 check_launch();
                 launched();
+                timer_stop(t0, kTimeSplit);
+                timing.split_kernel_launches += 1;
+                timing.split_entries += pending_entries;
             }
         }
+        const cudaEvent_t t_apply = timer_start();
+        timing.apply_entries += pending_entries;
         if (epoch) {
             if (pending_entries) {
                 k_slice_stamp<<<std::min<uint32_t>(fcfg.nfine, sms * 3), 256, 2u << fcfg.shift, st>>>(
-                    static_cast<uint8_t*>(d_lin), total, lin_words, fcfg, 0, bulk_ok ? 1 : 0, cur_epoch, cfg.window, hist.p);
+                    static_cast<uint8_t*>(d_lin), total, lin_words, fcfg, 0, bulk_ok ? 1 : 0, cur_epoch, cfg.window, hist.p,
+                    sparse_max);
                 check_launch();
                 launched();
+                timer_stop(t_apply, kTimeApply);
+                timing.apply_kernel_launches += 1;
+                CK(cudaMemcpyAsync(pin_streamed.p, d_streamed.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
                 CK(cudaMemsetAsync(fine_count.p, 0, fcfg.nfine * sizeof(uint32_t), st));
                 CK(cudaMemsetAsync(bin_count.p, 0, R * sizeof(uint32_t), st));
+            } else {
+                ev_pool.push_back(t_apply);
             }
             pending_entries = 0;
             return;
@@ -576,6 +673,9 @@ struct Engine {
                 launched();
             }
         });
+        timer_stop(t_apply, kTimeApply);
+        timing.apply_kernel_launches += 1;
+        CK(cudaMemcpyAsync(pin_streamed.p, d_streamed.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaMemsetAsync(fine_count.p, 0, fcfg.nfine * sizeof(uint32_t), st));
         if (pending_entries) CK(cudaMemsetAsync(bin_count.p, 0, R * sizeof(uint32_t), st));
         pending_entries = 0;
@@ -592,6 +692,7 @@ struct Engine {
             ev.ensure(3ull * ev_cap);
         }
         uint32_t n_ev = 0;
+        join_maint_lin();  // K1 may stamp the linear table directly (bin overflow)
         for (;;) {
             CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
             if (use_bins) {
@@ -630,6 +731,7 @@ struct Engine {
             ~OrderTimer() { t.order_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
         } order_timer{timing, w_order};
 
+        join_maint();  // rough aging, indicators and the candidate hash of the last slide
         xkeys.ensure(n_ev);
         k_cross<W, MAXR><<<blocks(n_ev), 256, 0, st>>>(ev.p, ev_cap, n_ev, dc, rough, d_stamp, xkeys.p, ctr.p + 1);
         check_launch();
@@ -936,15 +1038,40 @@ struct Engine {
             cub_call([&](void* t, size_t& b) {
                 return cub::DeviceRadixSort::SortKeys(t, b, csip.p, sorted_hosts.p, static_cast<int>(n), 0, 32, st);
             });
-            union_linear(sorted_hosts.p, n, weights.p, kthr);
-            if (compact) {  // hand off 8 bytes per entry: host + union weight
-                CK(cudaMemcpyAsync(compact->hosts, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(compact->weights, weights.p, n * 4ull, cudaMemcpyDeviceToHost, st));
-            } else if (!out_pinned) {
+            // (host, weight) pairs go to the host on the copy stream ds: the
+            // sorted hosts while the gather runs, the weights part by part as
+            // the gather finishes them (the hand-off trails by one part)
+            uint32_t* hdst = compact ? compact->hosts : nullptr;
+            uint32_t* wdst = compact ? compact->weights : nullptr;
+            if (!compact && !out_pinned) {
                 pin_hosts.ensure(n);
                 pin_w.ensure(n);
-                CK(cudaMemcpyAsync(pin_hosts.p, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, st));
-                CK(cudaMemcpyAsync(pin_w.p, weights.p, n * 4ull, cudaMemcpyDeviceToHost, st));
+                hdst = pin_hosts.p;
+                wdst = pin_w.p;
+            }
+            if (hdst) {
+                CK(cudaEventRecord(ev_sorted, st));
+                CK(cudaStreamWaitEvent(ds, ev_sorted, 0));
+                CK(cudaMemcpyAsync(hdst, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, ds));
+            }
+            const uint32_t parts = hdst && n >= (1u << 16) ? kReportParts : 1u;
+            for (uint32_t c = 0; c < parts; ++c) {
+                const uint32_t lo = static_cast<uint32_t>(uint64_t(n) * c / parts);
+                const uint32_t hi = static_cast<uint32_t>(uint64_t(n) * (c + 1) / parts);
+                const cudaEvent_t tg = timer_start();
+                union_linear(sorted_hosts.p + lo, hi - lo, weights.p + lo, kthr);
+                timer_stop(tg, kTimeGather);
+                timing.gather_kernel_launches += 1;
+                timing.gather_bytes += uint64_t(hi - lo) * cfg.rows * cfg.linear_slots * wb;
+                if (hdst) {
+                    CK(cudaEventRecord(ev_part[c], st));
+                    CK(cudaStreamWaitEvent(ds, ev_part[c], 0));
+                    CK(cudaMemcpyAsync(wdst + lo, weights.p + lo, (hi - lo) * 4ull, cudaMemcpyDeviceToHost, ds));
+                }
+            }
+            if (hdst) {
+                CK(cudaEventRecord(ev_d2h, ds));
+                CK(cudaStreamWaitEvent(st, ev_d2h, 0));
             }
         }
         pin_counts.ensure(cfg.rows);
@@ -1012,110 +1139,126 @@ struct Engine {
     }
 
     // ------------------------------------------------------------ slide (sea.hpp:316-338)
-    // SI clear + rough aging on the side stream, overlapping the report
-    // (neither reads them); slide_t waits for it.
-    template <typename W>
-    void preage_rough_t() {
-        const uint64_t rows = cfg.rows;
+    // The slide is split so that only what the report hand-off needs sits on
+    // the engine stream:
+    //  * slide_begin (side stream st2, at end-of-slice start, concurrent with
+    //    the report): clear the indicators, re-validate the candidates on the
+    //    NOT yet aged rough table and re-set the kept hosts' indicator bits.
+    //    union_rough_weight after aging counts r + (r != expired) < k, i.e.
+    //    r < k - 1 (k <= expired), so the retain test runs with k - 1.
+    //  * slide_finish: swap in the retained list, then queue the table
+    //    maintenance on st2 — rough aging, the epoch sweep, the candidate hash
+    //    rebuild. It overlaps the next slice's K1 (which touches none of it);
+    //    the engine stream joins it before the first reader (join_maint).
+    template <typename W, int MAXR>
+    void slide_begin_t() {
         CK(cudaEventRecord(ev_eos_start, st));
         CK(cudaStreamWaitEvent(st2, ev_eos_start, 0));
-        CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st2));
-        k_age<W><<<blocks(rows * rough_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st2>>>(static_cast<W*>(d_rough), rows * rough_words, dc.expired);
-        check_launch();
-        launched();
-        CK(cudaEventRecord(ev_rough_aged, st2));
-        rough_preaged = true;
-    }
-
-    // Candidate re-validation on the side stream right after the rough aging,
-    // concurrent with the report (which reads the list but not rough or SI);
-    // slide_t collects the retained count and swaps the lists.
-    template <typename W, int MAXR>
-    void retain_early_t() {
-        if (!ncsip) return;
-        const uint32_t n = static_cast<uint32_t>(ncsip);
-        keep.ensure(n);
-        csip2.ensure(n);
-        k_retain<W, MAXR><<<blocks(n), 256, 0, st2>>>(csip.p, n, dc, static_cast<const W*>(d_rough), d_si, keep.p);
-        check_launch();
-        launched();
-        cub_call([&](void* t, size_t& b) {
-            return cub::DeviceSelect::Flagged(t, b, csip.p, keep.p, csip2.p, ctr.p + 6, static_cast<int>(n), st2);
-        }, &temp2);
-        CK(cudaMemcpyAsync(pin_ctr.p + 6, ctr.p + 6, 4, cudaMemcpyDeviceToHost, st2));
-        CK(cudaEventRecord(ev_retained, st2));
-        retained_early = true;
-    }
-
-    template <typename W, int MAXR>
-    void slide_t(bool age_linear) {
-        const uint64_t rows = cfg.rows;
-        if (retained_early) {
-            CK(cudaEventSynchronize(ev_retained));
-            CK(cudaStreamWaitEvent(st, ev_retained, 0));
-            retained_early = false;
-            rough_preaged = false;
-            if (age_linear) {
-                k_age<W><<<blocks(rows * lin_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_lin), rows * lin_words, dc.expired);
-                check_launch();
-                launched();
-            }
-            if (ncsip) {
-                ncsip = pin_ctr.p[6];
-                std::swap(csip.p, csip2.p);
-                std::swap(csip.cap, csip2.cap);
-            }
-            trace("  slide: retain+select (early)");
-            rebuild_cset(ncsip);
-            trace("  slide: cset rebuild");
-            return;
-        }
-        if (rough_preaged) {
-            CK(cudaStreamWaitEvent(st, ev_rough_aged, 0));
-            rough_preaged = false;
-        } else {
-            CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st));
-            k_age<W><<<blocks(rows * rough_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_rough), rows * rough_words, dc.expired);
+        CK(cudaMemsetAsync(d_si, 0, uint64_t(cfg.rows) * cfg.cols * sizeof(uint16_t), st2));
+        if (ncsip) {
+            const uint32_t n = static_cast<uint32_t>(ncsip);
+            keep.ensure(n);
+            csip2.ensure(n);
+            DevCfg aged = dc;
+            aged.k = dc.k - 1;  // retain on the pre-aging table (see above)
+            k_retain<W, MAXR><<<blocks(n), 256, 0, st2>>>(csip.p, n, aged, static_cast<const W*>(d_rough), d_si, keep.p);
             check_launch();
             launched();
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceSelect::Flagged(t, b, csip.p, keep.p, csip2.p, ctr.p + 6, static_cast<int>(n), st2);
+            }, &temp2);
+            CK(cudaMemcpyAsync(pin_ctr.p + 6, ctr.p + 6, 4, cudaMemcpyDeviceToHost, st2));
         }
-        if (age_linear) {
+        CK(cudaEventRecord(ev_retained, st2));
+        slide_begun = true;
+    }
+    void slide_begin() {
+        with_w([&](auto w) {
+            using W = decltype(w);
+            if (cfg.rows <= 4) slide_begin_t<W, 4>();
+            else slide_begin_t<W, 64>();
+        });
+    }
+
+    template <typename W>
+    void slide_finish_t(bool age_linear) {
+        const uint64_t rows = cfg.rows;
+        // the report (and anything else on st) has finished reading the
+        // linear table and the old candidate list
+        CK(cudaEventRecord(ev_reported, st));
+        CK(cudaStreamWaitEvent(st2, ev_reported, 0));
+        if (epoch) {
+            cur_epoch = (cur_epoch + 1) & 0xFFu;
+            k_zero_hist_bin<<<1, 64, 0, st>>>(hist.p, cfg.rows, cur_epoch);
+            check_launch();
+            launched();
+            sweep_t(st2);
+            CK(cudaEventRecord(ev_maint_lin, st2));
+            maint_lin_pending = true;
+        } else if (age_linear) {
             k_age<W><<<blocks(rows * lin_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st>>>(static_cast<W*>(d_lin), rows * lin_words, dc.expired);
             check_launch();
             launched();
         }
-        if (!ncsip) return;
-        const uint32_t n = static_cast<uint32_t>(ncsip);
-        keep.ensure(n);
-        csip2.ensure(n);
-        trace("  slide: si clear + age");
-        k_retain<W, MAXR><<<blocks(n), 256, 0, st>>>(csip.p, n, dc, static_cast<const W*>(d_rough), d_si, keep.p);
+        k_age<W><<<blocks(rows * rough_words * sizeof(W) / 16 + 1, 256, 16), 256, 0, st2>>>(static_cast<W*>(d_rough), rows * rough_words, dc.expired);
         check_launch();
         launched();
-        cub_call([&](void* t, size_t& b) {
-            return cub::DeviceSelect::Flagged(t, b, csip.p, keep.p, csip2.p, ctr.p + 5, static_cast<int>(n), st);
-        });
-        ncsip = read_ctr(5);
-        trace("  slide: retain+select");
-        std::swap(csip.p, csip2.p);
-        std::swap(csip.cap, csip2.cap);
-        rebuild_cset(ncsip);
-        trace("  slide: cset rebuild");
+        // the retained count gates the host-side list swap; the engine stream
+        // also waits for it, so the end-of-slice device time covers the retain
+        CK(cudaEventSynchronize(ev_retained));
+        CK(cudaStreamWaitEvent(st, ev_retained, 0));
+        slide_begun = false;
+        if (ncsip) {
+            ncsip = pin_ctr.p[6];
+            std::swap(csip.p, csip2.p);
+            std::swap(csip.cap, csip2.cap);
+        }
+        rebuild_cset(ncsip, st2);
+        CK(cudaEventRecord(ev_maint, st2));
+        maint_pending = true;
+        trace("  slide: finish (maintenance queued)");
     }
 
+    // one slide's share of the epoch sweep (epoch.cuh: every byte at least
+    // once per 255 - expired slides)
+    void sweep_t(cudaStream_t s) {
+        const uint64_t total = uint64_t(cfg.rows) * lin_words;
+        const uint64_t period = 255 - dc.expired;
+        const uint64_t chunk = ((total + period - 1) / period + 15) & ~15ull;
+        const uint64_t end = std::min(total, sweep_pos + chunk);
+        k_sweep<<<blocks((end - sweep_pos) / 16 + 1, 256, 8), 256, 0, s>>>(static_cast<uint8_t*>(d_lin), sweep_pos,
+                                                                          end - sweep_pos, cur_epoch, dc.expired);
+        check_launch();
+        launched();
+        sweep_pos = end >= total ? 0 : end;
+    }
+
+    // The engine stream waits for queued maintenance (device-side wait).
+    void join_maint_lin() {
+        if (!maint_lin_pending) return;
+        CK(cudaStreamWaitEvent(st, ev_maint_lin, 0));
+        maint_lin_pending = false;
+    }
+    void join_maint() {
+        join_maint_lin();
+        if (!maint_pending) return;
+        CK(cudaStreamWaitEvent(st, ev_maint, 0));
+        maint_pending = false;
+    }
+
+    void slide_finish(bool age_linear) {
+        with_w([&](auto w) { slide_finish_t<decltype(w)>(age_linear); });
+    }
+
+    // EstimatorArray::slide (sea.hpp:316-338) on its own
     void slide(bool age_linear = true) {
         const auto w0 = std::chrono::steady_clock::now();
         stats.slides++;
-        flush_linear();
-        if (epoch) {
-            slide_epoch_tables();
-            age_linear = false;
-        }
-        with_w([&](auto w) {
-            using W = decltype(w);
-            if (cfg.rows <= 4) slide_t<W, 4>(age_linear);
-            else slide_t<W, 64>(age_linear);
-        });
+        join_maint();
+        flush_linear(use_bins && !epoch && age_linear ? 1 : 0);
+        if (use_bins && !epoch) age_linear = false;  // aged by the flush
+        if (!slide_begun) slide_begin();
+        slide_finish(age_linear);
         CK(cudaStreamSynchronize(st));
         timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
     }
@@ -1125,44 +1268,43 @@ struct Engine {
     // report reads the aged table (see report()).
     void end_slice(uint64_t slice_id, bool want_report, srla_entry* out, const Compact* compact = nullptr) {
         const bool due = want_report && slice_id + 1 >= cfg.window;
-        const auto w0 = std::chrono::steady_clock::now();
         trace(nullptr);
-        with_w([&](auto w) {
-            using W = decltype(w);
-            preage_rough_t<W>();
-            if (cfg.rows <= 4) retain_early_t<W, 4>();
-            else retain_early_t<W, 64>();
-        });
+        join_maint();
+        stats.slides++;
+        slide_begin();
+        const auto w0 = std::chrono::steady_clock::now();
+        bool age_linear = false;
         if (epoch) {
             flush_linear();
             if (due) report(out, nullptr, false, compact);
             trace("eos: report (epoch)");
-            slide(false);
-            trace("eos: slide (epoch)");
-            return;
-        }
-        if (due && dc.k < dc.expired) {
+        } else if (due && dc.k < dc.expired && use_bins) {
             d_counts.ensure(cfg.rows);
             CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
-            if (use_bins) {
-                flush_linear(2);
-            } else {
-                with_w([&](auto w) { count_age_range<decltype(w)>(0, uint64_t(cfg.rows) * lin_words, true); });
-            }
-            timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+            flush_linear(2);
             trace("eos: split+apply+count+age");
             report(out, nullptr, true, compact);
             trace("eos: report");
-            slide(false);
-            trace("eos: slide");
+        } else if (due && dc.k < dc.expired) {
+            d_counts.ensure(cfg.rows);
+            CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
+            with_w([&](auto w) { count_age_range<decltype(w)>(0, uint64_t(cfg.rows) * lin_words, true); });
+            report(out, nullptr, true, compact);
+            trace("eos: report");
         } else if (!due && use_bins) {
             flush_linear(1);
-            timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
-            slide(false);
         } else {
             if (due) report(out, nullptr, false, compact);
-            slide(true);
+            age_linear = !use_bins;
+            if (use_bins) flush_linear(1);
         }
+        const auto w1 = std::chrono::steady_clock::now();
+        slide_finish(age_linear);
+        CK(cudaStreamSynchronize(st));
+        timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w1).count();
+        (void)w0;
+        resolve_timers(false);
+        trace("eos: slide");
     }
 
     // ------------------------------------------------------------ queries
@@ -1337,7 +1479,10 @@ srla_status guard(Fn&& fn) {
 srla::Engine& E(srla_engine* e, bool join = true) {
     if (!e || !e->impl) throw srla::Error(SRLA_E_INVALID, "null engine");
     CK(cudaSetDevice(e->impl->device));
-    if (join) e->impl->join_eos();
+    if (join) {
+        e->impl->join_eos();
+        e->impl->join_maint();
+    }
     return *e->impl;
 }
 const srla::Engine& CE(const srla_engine* e) {
@@ -1568,11 +1713,20 @@ srla_status srla_stats_get(const srla_engine* e, srla_stats* out) {
 }
 
 srla_status srla_timing_get(const srla_engine* e, srla_timing* out) {
-    return guard([&] { *out = CE(e).timing; });
+    return guard([&] {
+        if (!out) throw srla::Error(SRLA_E_INVALID, "null output");
+        // resolving the pending kernel timers mutates only timing bookkeeping
+        auto* m = const_cast<srla_engine*>(e);
+        std::lock_guard<std::mutex> lk(m->mu);
+        E(m, false).timing_snapshot(out);
+    });
 }
 
 srla_status srla_timing_reset(srla_engine* e) {
-    return guard([&] { E(e).timing = srla_timing{}; });
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        E(e).timing_clear();
+    });
 }
 
 srla_status srla_synchronize(srla_engine* e) {

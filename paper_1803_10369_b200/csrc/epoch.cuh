@@ -41,7 +41,8 @@ __device__ __forceinline__ uint32_t stamp_byte_shared(uint8_t* base, uint32_t of
 // account the transitions in the per-row histograms.
 __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, uint64_t total_words,
                                                      uint64_t row_words, FineCfg f, uint32_t f_begin, int bulk,
-                                                     uint32_t cur, uint32_t k, unsigned long long* __restrict__ hist) {
+                                                     uint32_t cur, uint32_t k, unsigned long long* __restrict__ hist,
+                                                     uint32_t sparse_max) {
     extern __shared__ __align__(128) uint8_t s_raw[];
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ uint32_t s_hist[2][256];
@@ -53,6 +54,9 @@ __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, 
             if (f.count[fb] != 0) return fb;
         return f.nfine;
     };
+    // sparse slices (few marks for their size) are stamped in place with a
+    // CAS per mark: only the touched sectors move, instead of the slice twice
+    auto dense = [&](uint32_t fb) { return min(f.count[fb], f.cap) > sparse_max; };
     if (tid == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
@@ -66,6 +70,7 @@ __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, 
         // bulk path: whole 16-byte multiple slices; plain path for the tail slice
         const uint32_t len = slice_len(fb);
         uint8_t* g = lin + (static_cast<uint64_t>(fb) << f.shift);
+        if (!dense(fb)) return false;
         if (bulk && (len & 15) == 0) {
             if (tid == 0) {
                 mbar_expect_tx(&s_bar[b], len);
@@ -87,11 +92,13 @@ __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, 
         }
         const uint32_t len = slice_len(cur_fb);
         uint8_t* g = lin + (static_cast<uint64_t>(cur_fb) << f.shift);
+        const bool in_smem = dense(cur_fb);
+        if (in_smem && tid == 0) atomicAdd(f.streamed, 1ull);
         for (uint32_t q = tid; q < 512; q += blockDim.x) (&s_hist[0][0])[q] = 0;
         if (bulk_cur) {
             mbar_wait(&s_bar[b], phase[b]);
             phase[b] ^= 1u;
-        } else {
+        } else if (in_smem) {
             for (uint32_t q = tid; q < len; q += blockDim.x) buf[b][q] = g[q];
         }
         __syncthreads();
@@ -109,7 +116,8 @@ __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, 
             uint32_t old = cur, h = 0;
             if (q < n) {
                 const uint32_t off = e[q];
-                old = stamp_byte_shared(buf[b], off, cur);
+                // one block owns a slice: the CAS only races with this block
+                old = in_smem ? stamp_byte_shared(buf[b], off, cur) : stamp_byte_global(g, off, cur);
                 h = off < split ? 0u : 1u;
                 if (old != cur && ((cur - old) & 0xFFu) < k) atomicSub(&s_hist[h][old], 1u);
             }
@@ -134,8 +142,10 @@ __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, 
             fence_proxy_async_smem();
             __syncthreads();
             if (tid == 0) bulk_store(g, buf[b], len);
-        } else {
+        } else if (in_smem) {
             for (uint32_t q = tid; q < len; q += blockDim.x) g[q] = buf[b][q];
+            __syncthreads();
+        } else {
             __syncthreads();
         }
         cur_fb = nxt;
@@ -236,7 +246,34 @@ __global__ void __launch_bounds__(256) k_union_linear_epoch(const uint32_t* __re
         for (int i = 0; i < MAXR; ++i)
             if (i < static_cast<int>(c.rows)) cell[i] = lin + i * lrow + static_cast<uint64_t>(column_of(c, i, a)) * c.gl;
         uint32_t acc = 0;
-        if (vec) {
+        if (vec && MAXR <= 4) {
+            // all rows' vectors of two iterations issued before any use
+            const uint32_t nv = c.gl / 16;
+            for (uint32_t q0 = lane; q0 < nv; q0 += 64) {
+                uint4 x[2][MAXR];
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int i = 0; i < MAXR; ++i)
+                        x[u][i] = (i < static_cast<int>(c.rows) && q0 + 32u * u < nv)
+                                      ? __ldcs(reinterpret_cast<const uint4*>(cell[i]) + q0 + 32u * u)
+                                      : make_uint4(cur4, cur4, cur4, cur4);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (q0 + 32u * u >= nv) break;
+                    uint4 m = make_uint4(~0u, ~0u, ~0u, ~0u);
+#pragma unroll
+                    for (int i = 0; i < MAXR; ++i) {
+                        m.x &= __vcmpltu4(__vsub4(cur4, x[u][i].x), k4);
+                        m.y &= __vcmpltu4(__vsub4(cur4, x[u][i].y), k4);
+                        m.z &= __vcmpltu4(__vsub4(cur4, x[u][i].z), k4);
+                        m.w &= __vcmpltu4(__vsub4(cur4, x[u][i].w), k4);
+                    }
+                    acc += __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
+                }
+            }
+            acc >>= 3;
+        } else if (vec) {
             const uint32_t nv = c.gl / 16;
             for (uint32_t q = lane; q < nv; q += 32) {
                 uint4 m = make_uint4(~0u, ~0u, ~0u, ~0u);

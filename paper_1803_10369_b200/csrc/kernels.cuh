@@ -423,7 +423,38 @@ __global__ void __launch_bounds__(256) k_union_linear(const uint32_t* __restrict
         for (int i = 0; i < MAXR; ++i)
             if (i < static_cast<int>(c.rows)) cell[i] = lin + i * lrow + static_cast<uint64_t>(column_of(c, i, a)) * c.gl;
         uint32_t acc = 0;
-        if (vec) {
+        if (vec && MAXR <= 4) {
+            // all rows' vectors of two iterations issued before any use: 8
+            // independent 16-byte loads in flight per lane
+            const uint32_t nv = static_cast<uint32_t>(static_cast<uint64_t>(c.gl) * sizeof(W) / 16);
+            for (uint32_t q0 = lane; q0 < nv; q0 += 64) {
+                uint4 x[2][MAXR];
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int i = 0; i < MAXR; ++i)
+                        x[u][i] = (i < static_cast<int>(c.rows) && q0 + 32u * u < nv)
+                                      ? __ldcs(reinterpret_cast<const uint4*>(cell[i]) + q0 + 32u * u)
+                                      : make_uint4(0u, 0u, 0u, 0u);  // neutral for max
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (q0 + 32u * u >= nv) break;
+                    uint4 m = x[u][0];
+#pragma unroll
+                    for (int i = 1; i < MAXR; ++i) {
+                        if (i >= static_cast<int>(c.rows)) break;
+                        m.x = vmax_word<W>(m.x, x[u][i].x);
+                        m.y = vmax_word<W>(m.y, x[u][i].y);
+                        m.z = vmax_word<W>(m.z, x[u][i].z);
+                        m.w = vmax_word<W>(m.w, x[u][i].w);
+                    }
+                    acc += count_lt_word<W>(m.x, kk, kthr) + count_lt_word<W>(m.y, kk, kthr) +
+                           count_lt_word<W>(m.z, kk, kthr) + count_lt_word<W>(m.w, kk, kthr);
+                }
+            }
+            if constexpr (sizeof(W) == 1) acc >>= 3;
+            else if constexpr (sizeof(W) == 2) acc >>= 4;
+        } else if (vec) {
             const uint32_t nv = static_cast<uint32_t>(static_cast<uint64_t>(c.gl) * sizeof(W) / 16);
             for (uint32_t q = lane; q < nv; q += 32) {
                 uint4 m = make_uint4(0, 0, 0, 0);

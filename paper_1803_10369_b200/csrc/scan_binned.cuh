@@ -89,8 +89,9 @@ __global__ void __launch_bounds__(kBinThreads, 3) k_scan_bin(const uint32_t* __r
                                                          uint32_t ev_cap, uint32_t* __restrict__ ev_count, int vec) {
     __shared__ uint32_t s_cnt[kMaxRegions];
     __shared__ uint32_t s_lbase[kMaxRegions];
-    __shared__ uint32_t s_dst[kMaxRegions];  // first bin slot of this tile per region (nregions * cap < 2^32)
-    __shared__ uint16_t s_fit[kMaxRegions];  // entries of this tile that fit in the region's bin
+    // per region: {bin slot of staging entry idx = x + idx (mod 2^32; nregions * cap < 2^32),
+    //              first staging index that no longer fits the region's bin}
+    __shared__ uint2 s_win[kMaxRegions];
     __shared__ uint32_t s_off[kBinEntries];
     __shared__ uint16_t s_reg[kBinEntries];
     __shared__ uint32_t s_warp[kBinThreads / 32];
@@ -192,8 +193,8 @@ __global__ void __launch_bounds__(kBinThreads, 3) k_scan_bin(const uint32_t* __r
             s_lbase[r] = run;
             if (cn) {
                 const uint32_t g = atomicAdd(b.count + r, cn);
-                s_dst[r] = r * b.cap + g;
-                s_fit[r] = static_cast<uint16_t>(g >= b.cap ? 0u : min(cn, b.cap - g));
+                const uint32_t fit = g >= b.cap ? 0u : min(cn, b.cap - g);
+                s_win[r] = make_uint2(r * b.cap + g - run, run + fit);
             }
             run += cn;
         }
@@ -212,16 +213,23 @@ __global__ void __launch_bounds__(kBinThreads, 3) k_scan_bin(const uint32_t* __r
                 }
         __syncthreads();
 
+        // coalesced bin writes: consecutive staging entries of a region go to
+        // consecutive bin slots
+        bool ovf = false;
         for (uint32_t idx = tid; idx < total; idx += kBinThreads) {
-            const uint32_t r = s_reg[idx];
-            const uint32_t j = idx - s_lbase[r];
-            if (j < s_fit[r]) {
-                b.bins[s_dst[r] + j] = s_off[idx];
-            } else if (ep.on) {  // bin full: mark directly (marks commute)
-                mark_epoch_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << b.region_shift) + s_off[idx],
-                                  ep.row_words, ep.cur, ep.hist);
-            } else {
-                mark_word<W>(lin + (static_cast<uint64_t>(r) << b.region_shift), s_off[idx]);
+            const uint2 wv = s_win[s_reg[idx]];
+            if (idx < wv.y) b.bins[wv.x + idx] = s_off[idx];
+            else ovf = true;
+        }
+        if (__syncthreads_or(ovf)) {  // a bin is full: mark the rest directly (marks commute)
+            for (uint32_t idx = tid; idx < total; idx += kBinThreads) {
+                const uint32_t r = s_reg[idx];
+                if (idx < s_win[r].y) continue;
+                if (ep.on)
+                    mark_epoch_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << b.region_shift) + s_off[idx],
+                                      ep.row_words, ep.cur, ep.hist);
+                else
+                    mark_word<W>(lin + (static_cast<uint64_t>(r) << b.region_shift), s_off[idx]);
             }
         }
         __syncthreads();
@@ -305,6 +313,7 @@ struct FineCfg {
     uint32_t shift;       // log2(words per fine slice)
     uint32_t per_region;  // fine slices per coarse region = 2^(region_shift - shift)
     uint32_t nfine;       // total fine slices covering the table
+    unsigned long long* streamed;  // whole slices read + written by the apply kernels (statistics)
 };
 
 constexpr int kSplitThreads = 512;
@@ -315,7 +324,7 @@ constexpr int kSplitTile = kSplitThreads * kSplitPerThread;  // 8192 entries
 // of one region: shared-memory counting sort by slice (ranks from shared
 // atomics), one global reservation per slice per tile, coalesced u16 writes.
 template <typename W>
-__global__ void __launch_bounds__(kSplitThreads) k_split(const uint32_t* __restrict__ coarse, uint32_t coarse_cap,
+__global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __restrict__ coarse, uint32_t coarse_cap,
                                                          const uint32_t* __restrict__ tile_prefix,
                                                          const uint32_t* __restrict__ coarse_n, uint32_t nregions,
                                                          uint32_t region_shift, FineCfg f, EpochCfg ep,
@@ -442,6 +451,7 @@ __global__ void __launch_bounds__(256) k_slice_apply(W* __restrict__ lin, uint64
     for (uint32_t fb = f_begin + blockIdx.x; fb < f.nfine; fb += gridDim.x) {
         const uint32_t n = min(f.count[fb], f.cap);
         if (mode == 0 && n == 0) continue;
+        if (tid == 0) atomicAdd(f.streamed, 1ull);
         const uint64_t w0 = static_cast<uint64_t>(fb) << f.shift;
         const uint32_t nw = static_cast<uint32_t>(min(static_cast<uint64_t>(1u << f.shift), total_words - w0));
         const uint32_t nv = vec ? static_cast<uint32_t>((static_cast<uint64_t>(nw) * sizeof(W)) / 16) : 0u;
@@ -602,6 +612,7 @@ __global__ void __launch_bounds__(256) k_slice_apply_bulk(W* __restrict__ lin, u
             bulk_load(buf[b ^ 1u], lin + (static_cast<uint64_t>(nxt) << f.shift), slice_bytes, &s_bar[b ^ 1u]);
         }
         mbar_wait(&s_bar[b], (i >> 1) & 1u);
+        if (tid == 0) atomicAdd(f.streamed, 1ull);
         W* sw = reinterpret_cast<W*>(buf[b]);
         const uint32_t n = min(f.count[cur], f.cap);
         const uint16_t* e = f.bins + static_cast<uint64_t>(cur) * f.cap;

@@ -59,7 +59,12 @@ class CTiming(C.Structure):
                 ("scan_kernel_records", C.c_uint64), ("end_slice_device_ms", C.c_double),
                 ("end_slice_wall_ms", C.c_double), ("last_end_slice_device_ms", C.c_double),
                 ("last_end_slice_wall_ms", C.c_double), ("end_slices", C.c_uint64),
-                ("order_wall_ms", C.c_double), ("report_wall_ms", C.c_double), ("slide_wall_ms", C.c_double)]
+                ("order_wall_ms", C.c_double), ("report_wall_ms", C.c_double), ("slide_wall_ms", C.c_double),
+                ("split_kernel_ms", C.c_double), ("split_kernel_launches", C.c_uint64),
+                ("split_entries", C.c_uint64), ("apply_kernel_ms", C.c_double),
+                ("apply_kernel_launches", C.c_uint64), ("apply_entries", C.c_uint64),
+                ("apply_stream_bytes", C.c_uint64), ("gather_kernel_ms", C.c_double),
+                ("gather_kernel_launches", C.c_uint64), ("gather_bytes", C.c_uint64)]
 
 
 class CPlant(C.Structure):

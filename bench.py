@@ -78,7 +78,7 @@ class Clocks:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, local_rank):
+    def __init__(self, local_rank, period_ms=100):
         vis = os.environ.get("CUDA_VISIBLE_DEVICES")
         idx = str(local_rank)
         if vis:
@@ -88,7 +88,7 @@ class Clocks:
         self.lines = []
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={idx}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", str(period_ms)],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -338,8 +338,9 @@ def run_engine(args):
     eng.synchronize()
 
     eng.timing_reset()
+    tm0 = {k: v for k, v in eng.timing().items() if k in ("alloc_ms", "allocs")}  # process-wide counters
     st0 = eng.stats()
-    clocks = Clocks(local)
+    clocks = Clocks(local, args.clock_ms)
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(st)
@@ -443,8 +444,9 @@ def run_engine(args):
             "roofline": roofline,
             "kernels": kernels,
             "roofline_scan_path": path,
-            "breakdown_ms_per_step": {k: tm[k] / args.steps for k in
-                                      ("scan_kernel_ms", "order_wall_ms", "report_wall_ms", "slide_wall_ms")},
+            "breakdown_ms_per_step": {k: (tm[k] - tm0.get(k, 0)) / args.steps for k in
+                                      ("scan_kernel_ms", "order_wall_ms", "report_wall_ms", "slide_wall_ms",
+                                       "sync_wait_ms", "syncs", "alloc_ms", "allocs")},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
@@ -469,6 +471,7 @@ def main():
     ap.add_argument("--resident", type=int, default=0, help="distinct slices staged in HBM (default 12; c3: 10)")
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi clock sampling period in the timed region")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--handoff", default="compact", choices=["compact", "entries"],
                     help="report hand-off of the device-resident steps (e2e always returns srla_entry)")

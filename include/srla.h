@@ -210,6 +210,10 @@ typedef struct srla_timing {
     double gather_kernel_ms;      /* k_union_linear(_epoch): report union weights */
     uint64_t gather_kernel_launches;
     uint64_t gather_bytes;        /* candidates x rows x g' x W */
+    double sync_wait_ms;          /* host time blocked on engine-stream synchronisation (scan ordering) */
+    uint64_t syncs;
+    double alloc_ms;              /* process-wide device/pinned (re)allocation host time */
+    uint64_t allocs;
 } srla_timing;
 srla_status srla_timing_get(const srla_engine* e, srla_timing* out);
 srla_status srla_timing_reset(srla_engine* e);

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <stdexcept>
@@ -40,6 +41,21 @@ struct Error : std::runtime_error {
             throw ::srla::Error(SRLA_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// device/pinned (re)allocations: count and host time (srla_timing)
+inline double g_alloc_ms = 0.0;
+inline uint64_t g_allocs = 0;
+struct AllocTimer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    AllocTimer(size_t bytes = 0, size_t cap = 0) {
+        static const bool verbose = [] { const char* v = std::getenv("SRLA_TRACE_ALLOC"); return v && v[0] == '1'; }();
+        if (verbose) std::fprintf(stderr, "[srla] alloc %zu bytes (had %zu)\n", bytes, cap);
+    }
+    ~AllocTimer() {
+        g_alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        ++g_allocs;
+    }
+};
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -51,6 +67,7 @@ struct DevBuf {
     }
     void ensure(size_t n) {
         if (n <= cap) return;
+        AllocTimer at(n * sizeof(T), cap * sizeof(T));
         if (p) CK(cudaFree(p));
         p = nullptr;
         const size_t c = std::max<size_t>({n + n / 4, cap * 2, 256});
@@ -60,6 +77,7 @@ struct DevBuf {
     // grow keeping the first `keep` elements (stream-ordered copy)
     void ensure_keep(size_t n, size_t keep, cudaStream_t st) {
         if (n <= cap) return;
+        AllocTimer at(n * sizeof(T), cap * sizeof(T) + 2);
         const size_t c = std::max<size_t>({n, cap * 2, 256});
         T* q = nullptr;
         CK(cudaMalloc(&q, c * sizeof(T)));
@@ -84,6 +102,7 @@ struct PinBuf {
     // candidate list that creeps up over the first window reallocates rarely
     void ensure(size_t n) {
         if (n <= cap) return;
+        AllocTimer at(n * sizeof(T), cap * sizeof(T) + 1);
         if (p) CK(cudaFreeHost(p));
         p = nullptr;
         const size_t c = std::max<size_t>({n + n / 4, cap * 2, 4096});
@@ -136,6 +155,12 @@ struct Engine {
     bool slide_begun = false;
     // report hand-off: device->host copies on their own stream
     static constexpr uint32_t kReportParts = 4;
+    cudaEvent_t ev_counts_ready = nullptr, ev_counts = nullptr;
+    // the retained candidate list sorted by host (built on st2 by the slide)
+    DevBuf<uint32_t> sorted_ret, newsorted, sorted_tmp;
+    uint64_t nsorted_ret = 0;
+    bool sorted_ret_valid = true;  // the empty list is sorted
+    uint64_t last_sort_new = 0;  // hosts sorted at the last report (all of them without a sorted prefix)
     cudaStream_t ds = nullptr;
     cudaEvent_t ev_sorted = nullptr, ev_d2h = nullptr, ev_part[kReportParts] = {};
     // table maintenance queued on st2 by slide_finish (join_maint)
@@ -243,6 +268,8 @@ struct Engine {
     void timing_snapshot(srla_timing* out) {
         resolve_timers(false);
         *out = timing;
+        out->alloc_ms = g_alloc_ms;
+        out->allocs = g_allocs;
         if (pin_streamed.p) out->apply_stream_bytes = 2ull * pin_streamed.p[0] * ((1ull << fcfg.shift) * wb);
     }
     void timing_clear() {
@@ -259,11 +286,16 @@ struct Engine {
     explicit Engine(const srla_config& c, int dev) : cfg(c), device(dev) {
         validate();
         CK(cudaSetDevice(device));
-        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        // the engine stream outranks the side stream: queued slide maintenance
+        // and the candidate re-validation must not hold SMs the report needs
+        int prio_low = 0, prio_high = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+        CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio_high));
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&st2, cudaStreamNonBlocking, prio_low));
         CK(cudaEventCreateWithFlags(&ev_eos_start, cudaEventDisableTiming));
-        for (cudaEvent_t* e : {&ev_reported, &ev_retained, &ev_maint_lin, &ev_maint, &ev_sorted, &ev_d2h})
+        for (cudaEvent_t* e : {&ev_reported, &ev_retained, &ev_maint_lin, &ev_maint, &ev_sorted, &ev_d2h, &ev_counts_ready,
+                               &ev_counts})
             CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         for (cudaEvent_t& e : ev_part) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
@@ -311,6 +343,7 @@ struct Engine {
         pin_ctr.ensure(16);
         setup_bins();
         setup_epoch();
+        if (use_bins) reserve_candidates(size_t(1) << 21);
         rebuild_cset(1024);
         CK(cudaStreamSynchronize(st));
     }
@@ -341,7 +374,8 @@ struct Engine {
             cudaStreamSynchronize(st2);
             cudaStreamDestroy(st2);
         }
-        for (cudaEvent_t e : {ev_eos_start, ev_reported, ev_retained, ev_maint_lin, ev_maint, ev_sorted, ev_d2h})
+        for (cudaEvent_t e : {ev_eos_start, ev_reported, ev_retained, ev_maint_lin, ev_maint, ev_sorted, ev_d2h,
+                              ev_counts_ready, ev_counts})
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_part)
             if (e) cudaEventDestroy(e);
@@ -404,8 +438,15 @@ struct Engine {
 
     uint32_t read_ctr(uint32_t idx) {
         CK(cudaMemcpyAsync(pin_ctr.p + idx, ctr.p + idx, 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        sync_st();
         return pin_ctr.p[idx];
+    }
+    // engine-stream synchronisation with the host wait accounted (srla_timing)
+    void sync_st() {
+        const auto t0 = std::chrono::steady_clock::now();
+        CK(cudaStreamSynchronize(st));
+        timing.sync_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        timing.syncs += 1;
     }
 
     // ------------------------------------------------------------ CUB helpers
@@ -420,6 +461,19 @@ struct Engine {
     }
 
     static int bit_length(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 1; }
+
+    // Large sketches: size the candidate-list buffers for 2M candidates up
+    // front, so the list creeping up over the first windows never reallocates
+    // (a cudaFree synchronises the whole device) inside a running pipeline.
+    void reserve_candidates(size_t n) {
+        csip.ensure_keep(n, 0, st);
+        csip2.ensure(n); sorted_hosts.ensure(n); weights.ensure(n); keep.ensure(n); sorted_ret.ensure(n);
+        sorted_tmp.ensure(n);
+        newsorted.ensure(n); d_entries.ensure(3 * n);
+        size_t cap = 1024;
+        while (cap < 2 * n) cap <<= 1;
+        cset.ensure(cap);
+    }
 
     // ------------------------------------------------------------ candidate set
     void rebuild_cset(uint64_t want, cudaStream_t s = nullptr) {
@@ -453,6 +507,22 @@ struct Engine {
         if (!nn) return;
         csip.ensure_keep(ncsip + nn, ncsip, st);
         CK(cudaMemcpyAsync(csip.p + ncsip, newhosts.p, nn * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        // keep the sorted view of the list current: sort the newcomers, merge
+        if (sorted_ret_valid && nsorted_ret == ncsip) {
+            newsorted.ensure(nn);
+            sorted_tmp.ensure(ncsip + nn);
+            sorted_ret.ensure_keep(ncsip + nn, ncsip, st);
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceRadixSort::SortKeys(t, b, newhosts.p, newsorted.p, static_cast<int>(nn), 0, 32, st);
+            });
+            k_merge_sorted<<<blocks((ncsip + nn + 7) / 8), 256, 0, st>>>(sorted_ret.p, static_cast<uint32_t>(ncsip),
+                                                                       newsorted.p, nn, sorted_tmp.p);
+            check_launch();
+            launched();
+            std::swap(sorted_ret.p, sorted_tmp.p);
+            std::swap(sorted_ret.cap, sorted_tmp.cap);
+            nsorted_ret = ncsip + nn;
+        }
         ncsip += nn;
         if (2 * ncsip > cset_cap) {
             rebuild_cset(ncsip);
@@ -479,7 +549,9 @@ struct Engine {
         while (((total_words + (1ull << shift) - 1) >> shift) > kMaxRegions) ++shift;
         // fine slices (u16 offsets): 32 KB, or larger so one region splits into <= 4096
         uint32_t fs = 0;
-        while ((1ull << (fs + 1)) * wb <= (32ull << 10)) ++fs;  // 32 KB: two buffers per block
+        uint64_t fine_bytes = 32ull << 10;  // 32 KB: two buffers per block
+        if (const char* fk = std::getenv("SRLA_FINE_KB")) fine_bytes = std::strtoull(fk, nullptr, 10) << 10;
+        while ((1ull << (fs + 1)) * wb <= fine_bytes) ++fs;
         fs = std::min(fs, shift);
         if (forced && small) fs = std::max<uint32_t>(std::min<uint32_t>(shift, 4), shift > 3 ? shift - 3 : 0);
         while (shift - fs > 12) ++fs;  // split fan-out <= 4096 slices per region
@@ -499,6 +571,10 @@ struct Engine {
         fcfg.per_region = 1u << (shift - fs);
         fcfg.nfine = static_cast<uint32_t>((total_words + (1ull << fs) - 1) >> fs);
         fcfg.cap = static_cast<uint32_t>(std::max<uint64_t>(64, (coarse_total * 3 / 2 / fcfg.nfine + 7) & ~7ull));
+        // Large sparse-active tables (many slices, marks clustered on the
+        // active sources' cells) overflow an average-sized fine bin; give
+        // each slice room for 1024 marks while that stays within 4 GB.
+        if (!small && fcfg.cap < 1024 && uint64_t(fcfg.nfine) * 1024 * 2 <= (4ull << 30)) fcfg.cap = 1024;
         if (uint64_t(fcfg.cap) * fcfg.nfine >= (1ull << 32)) throw Error(SRLA_E_INTERNAL, "fine bin index overflow");
         fine_bins.ensure(uint64_t(fcfg.nfine) * fcfg.cap);
         fine_count.ensure(fcfg.nfine);
@@ -573,10 +649,11 @@ struct Engine {
     }
 
     // counts_active per row from the stamp histograms (already on the host)
-    void counts_from_hist(uint64_t* counts) const {
+    void counts_from_hist(uint64_t* counts) const { counts_from_hist(counts, cur_epoch); }
+    void counts_from_hist(uint64_t* counts, uint32_t ep) const {
         for (uint32_t i = 0; i < cfg.rows; ++i) {
             uint64_t s = 0;
-            for (uint32_t j = 0; j < cfg.window; ++j) s += pin_hist.p[uint64_t(i) * 256 + ((cur_epoch - j) & 0xFFu)];
+            for (uint32_t j = 0; j < cfg.window; ++j) s += pin_hist.p[uint64_t(i) * 256 + ((ep - j) & 0xFFu)];
             counts[i] = s;
         }
     }
@@ -690,6 +767,16 @@ struct Engine {
         if (!ev_cap) {
             ev_cap = static_cast<uint32_t>(std::min<uint64_t>(kChunk, (uint64_t(kChunk) >> tau) + (uint64_t(kChunk) >> (tau + 3)) + 65536));
             ev.ensure(3ull * ev_cap);
+            // the ordering scratch is bounded by the sampled events of a chunk:
+            // size it once instead of creeping up (each regrowth is a cudaFree,
+            // a device-wide synchronisation)
+            const size_t m = std::min<size_t>(ev_cap, size_t(1) << 21);
+            xkeys.ensure(m); xsorted.ensure(m); hp.ensure(m); hps.ensure(m); fmask.ensure(m);
+            cnt.ensure(m); off.ensure(m); hosts.ensure(m); status.ensure(m); definite.ensure(m);
+            fl_und.ensure(m); fl_ins.ensure(m); flagged.ensure(m); pushed.ensure(m); newhosts.ensure(m);
+            isnew.ensure(m);
+            const size_t t = m * std::min<uint32_t>(cfg.rows, 8);
+            tkey.ensure(t); skey.ensure(t); tval.ensure(t); sval.ensure(t); towner.ensure(t); posof.ensure(t);
         }
         uint32_t n_ev = 0;
         join_maint_lin();  // K1 may stamp the linear table directly (bin overflow)
@@ -778,7 +865,7 @@ struct Engine {
         });
         CK(cudaMemcpyAsync(pin_ctr.p + 8, off.p + (Hn - 1), 4, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(pin_ctr.p + 9, cnt.p + (Hn - 1), 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        sync_st();
         const uint32_t T = pin_ctr.p[8] + pin_ctr.p[9];
         CK(cudaMemsetAsync(definite.p, 0, Hn, st));
         if (T) {
@@ -858,6 +945,36 @@ struct Engine {
         const auto now = std::chrono::steady_clock::now();
         if (what) std::fprintf(stderr, "[srla] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - trace_t0).count());
         trace_t0 = now;
+    }
+
+    // SRLA_EOS_TRACE=1: device-event marks on the engine stream through the
+    // end-of-slice, printed after it (no extra synchronisation)
+    bool eos_tracing = [] { const char* t = std::getenv("SRLA_EOS_TRACE"); return t && t[0] == '1'; }();
+    std::vector<std::pair<const char*, cudaEvent_t>> eos_marks;
+    std::vector<std::pair<const char*, double>> eos_host_marks;
+    std::chrono::steady_clock::time_point eos_host_t0{};
+    void eos_mark(const char* what) {
+        if (!eos_tracing) return;
+        cudaEvent_t e = take_event();
+        CK(cudaEventRecord(e, st));
+        eos_marks.push_back({what, e});
+        eos_host_marks.push_back({what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - eos_host_t0).count()});
+    }
+    void eos_dump() {
+        if (!eos_tracing || eos_marks.empty()) return;
+        std::string line = "[srla eos] n=" + std::to_string(ncsip) + " sorted_new=" + std::to_string(last_sort_new);
+        for (size_t i = 1; i < eos_marks.size(); ++i) {
+            float ms = 0.f;
+            CK(cudaEventSynchronize(eos_marks[i].second));
+            CK(cudaEventElapsedTime(&ms, eos_marks[i - 1].second, eos_marks[i].second));
+            char b[128];
+            std::snprintf(b, sizeof b, " %s %.3f(h%.3f)", eos_marks[i].first, ms, eos_host_marks[i].second);
+            line += b;
+        }
+        std::fprintf(stderr, "%s\n", line.c_str());
+        for (auto& m : eos_marks) ev_pool.push_back(m.second);
+        eos_marks.clear();
+        eos_host_marks.clear();
     }
 
     void join_eos() {
@@ -1016,11 +1133,42 @@ struct Engine {
         for (uint32_t i = 0; i < cfg.rows; ++i) out[i] = pin_counts.p[i];
     }
 
+    // Candidates in ascending host order into sorted_hosts (or the sorted
+    // retained list itself). The retained prefix of the list was sorted in the
+    // background by the last slide; only the hosts appended since are sorted
+    // here and merged in.
+    const uint32_t* sort_candidates(uint32_t n) {
+        last_sort_new = n;
+        if (sorted_ret_valid && nsorted_ret == n) return sorted_ret.p;  // kept up to date by append_candidates
+        if (sorted_ret_valid && nsorted_ret <= n && nsorted_ret > 0) {
+            const uint32_t m = n - static_cast<uint32_t>(nsorted_ret);
+            last_sort_new = m;
+            if (m == 0) return sorted_ret.p;
+            newsorted.ensure(m);
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceRadixSort::SortKeys(t, b, csip.p + nsorted_ret, newsorted.p, static_cast<int>(m), 0, 32, st);
+            });
+            eos_mark("sort-new");
+            k_merge_sorted<<<blocks((uint64_t(n) + 7) / 8), 256, 0, st>>>(sorted_ret.p, static_cast<uint32_t>(nsorted_ret),
+                                                                        newsorted.p, m, sorted_hosts.p);
+            check_launch();
+            launched();
+            return sorted_hosts.p;
+        }
+        cub_call([&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, csip.p, sorted_hosts.p, static_cast<int>(n), 0, 32, st);
+        });
+        return sorted_hosts.p;
+    }
+
     // report_window (sea.hpp:288-309). With counts_ready, d_counts already
     // holds the per-row active counts and the table has been aged by the fused
     // count+age pass, so union activity is tested with r < k+1 (exact while
     // k < expired: an aged recorder r' = r+1 for every r < expired).
-    void report(srla_entry* out, double* fp_out, bool counts_ready = false, const Compact* compact = nullptr) {
+    // `between` runs once the report's device work is queued, before the host
+    // waits for it (end_slice queues the slide maintenance there).
+    void report(srla_entry* out, double* fp_out, bool counts_ready = false, const Compact* compact = nullptr,
+                const std::function<void()>& between = {}) {
         const auto w0 = std::chrono::steady_clock::now();
         const uint32_t n = static_cast<uint32_t>(ncsip);
         cudaPointerAttributes oa{};
@@ -1032,12 +1180,21 @@ struct Engine {
             flush_linear();
             if (!epoch) row_active_async();
         }
+        // the fill counts go to the host first (copy stream), so the Eq. 9
+        // table is built while the gather runs
+        CK(cudaEventRecord(ev_counts_ready, st));
+        CK(cudaStreamWaitEvent(ds, ev_counts_ready, 0));
+        pin_counts.ensure(cfg.rows);
+        if (epoch) CK(cudaMemcpyAsync(pin_hist.p, hist.p, uint64_t(cfg.rows) * 256 * 8, cudaMemcpyDeviceToHost, ds));
+        else CK(cudaMemcpyAsync(pin_counts.p, d_counts.p, cfg.rows * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ds));
+        CK(cudaEventRecord(ev_counts, ds));
+        const uint32_t* sh = sorted_hosts.p;  // report order: hosts ascending (sea.hpp:294-295)
         if (n) {
             sorted_hosts.ensure(n);
             weights.ensure(n);
-            cub_call([&](void* t, size_t& b) {
-                return cub::DeviceRadixSort::SortKeys(t, b, csip.p, sorted_hosts.p, static_cast<int>(n), 0, 32, st);
-            });
+            eos_mark("pre-sort");
+            sh = sort_candidates(n);
+            eos_mark("sorted");
             // (host, weight) pairs go to the host on the copy stream ds: the
             // sorted hosts while the gather runs, the weights part by part as
             // the gather finishes them (the hand-off trails by one part)
@@ -1052,14 +1209,14 @@ struct Engine {
             if (hdst) {
                 CK(cudaEventRecord(ev_sorted, st));
                 CK(cudaStreamWaitEvent(ds, ev_sorted, 0));
-                CK(cudaMemcpyAsync(hdst, sorted_hosts.p, n * 4ull, cudaMemcpyDeviceToHost, ds));
+                CK(cudaMemcpyAsync(hdst, sh, n * 4ull, cudaMemcpyDeviceToHost, ds));
             }
             const uint32_t parts = hdst && n >= (1u << 16) ? kReportParts : 1u;
             for (uint32_t c = 0; c < parts; ++c) {
                 const uint32_t lo = static_cast<uint32_t>(uint64_t(n) * c / parts);
                 const uint32_t hi = static_cast<uint32_t>(uint64_t(n) * (c + 1) / parts);
                 const cudaEvent_t tg = timer_start();
-                union_linear(sorted_hosts.p + lo, hi - lo, weights.p + lo, kthr);
+                union_linear(sh + lo, hi - lo, weights.p + lo, kthr);
                 timer_stop(tg, kTimeGather);
                 timing.gather_kernel_launches += 1;
                 timing.gather_bytes += uint64_t(hi - lo) * cfg.rows * cfg.linear_slots * wb;
@@ -1069,24 +1226,29 @@ struct Engine {
                     CK(cudaMemcpyAsync(wdst + lo, weights.p + lo, (hi - lo) * 4ull, cudaMemcpyDeviceToHost, ds));
                 }
             }
+            eos_mark("gathered");
             if (hdst) {
                 CK(cudaEventRecord(ev_d2h, ds));
                 CK(cudaStreamWaitEvent(st, ev_d2h, 0));
             }
+            eos_mark("d2h");
         }
-        pin_counts.ensure(cfg.rows);
-        if (epoch) CK(cudaMemcpyAsync(pin_hist.p, hist.p, uint64_t(cfg.rows) * 256 * 8, cudaMemcpyDeviceToHost, st));
-        else CK(cudaMemcpyAsync(pin_counts.p, d_counts.p, cfg.rows * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        trace("  report: sort+gather+d2h");
+        const uint32_t report_epoch = cur_epoch;  // `between` may slide it
+        if (between) between();
+        CK(cudaEventSynchronize(ev_counts));
+        eos_mark("counts");
         std::vector<uint64_t> counts(pin_counts.p, pin_counts.p + cfg.rows);
-        if (epoch) counts_from_hist(counts.data());
+        if (epoch) counts_from_hist(counts.data(), report_epoch);
         const double fp = srla_host::fill_product(counts.data(), cfg.rows, lin_words);
         if (fp_out) *fp_out = fp;
         lut_est.resize(cfg.linear_slots + 1);
         lut_has.resize(cfg.linear_slots + 1);
         lut_sup.resize(cfg.linear_slots + 1);
         srla_host::estimate_lut(cfg.linear_slots, fp, cfg.theta, lut_est.data(), lut_has.data(), lut_sup.data());
+        eos_mark("lut");
+        CK(cudaStreamSynchronize(st));
+        eos_mark("synced");
+        trace("  report: sort+gather+d2h");
         // (host, weight) -> entries: on the device straight into a pinned
         // caller buffer, else on the host into pageable memory
         if (compact) {
@@ -1105,7 +1267,7 @@ struct Engine {
             d_lut.ensure(L * 10ull);
             CK(cudaMemcpyAsync(d_lut.p, pin_lut.p, L * 10ull, cudaMemcpyHostToDevice, st));
             d_entries.ensure(3ull * n);
-            k_map_entries<<<blocks(n), 256, 0, st>>>(sorted_hosts.p, weights.p, n, reinterpret_cast<const double*>(d_lut.p),
+            k_map_entries<<<blocks(n), 256, 0, st>>>(sh, weights.p, n, reinterpret_cast<const double*>(d_lut.p),
                                                      d_lut.p + 8ull * L, d_lut.p + 9ull * L, d_entries.p);
             check_launch();
             launched();
@@ -1142,26 +1304,26 @@ struct Engine {
     // The slide is split so that only what the report hand-off needs sits on
     // the engine stream:
     //  * slide_begin (side stream st2, at end-of-slice start, concurrent with
-    //    the report): clear the indicators, re-validate the candidates on the
-    //    NOT yet aged rough table and re-set the kept hosts' indicator bits.
+    //    the report): re-validate the candidates on the NOT yet aged rough
+    //    table.
     //    union_rough_weight after aging counts r + (r != expired) < k, i.e.
     //    r < k - 1 (k <= expired), so the retain test runs with k - 1.
     //  * slide_finish: swap in the retained list, then queue the table
-    //    maintenance on st2 — rough aging, the epoch sweep, the candidate hash
-    //    rebuild. It overlaps the next slice's K1 (which touches none of it);
+    //    maintenance on st2 — indicator clear + re-set for the kept hosts,
+    //    rough aging, the epoch sweep, the candidate hash rebuild and sorted view. It overlaps the next slice's K1 (which touches none of it);
     //    the engine stream joins it before the first reader (join_maint).
     template <typename W, int MAXR>
     void slide_begin_t() {
         CK(cudaEventRecord(ev_eos_start, st));
         CK(cudaStreamWaitEvent(st2, ev_eos_start, 0));
-        CK(cudaMemsetAsync(d_si, 0, uint64_t(cfg.rows) * cfg.cols * sizeof(uint16_t), st2));
         if (ncsip) {
             const uint32_t n = static_cast<uint32_t>(ncsip);
             keep.ensure(n);
             csip2.ensure(n);
             DevCfg aged = dc;
             aged.k = dc.k - 1;  // retain on the pre-aging table (see above)
-            k_retain<W, MAXR><<<blocks(n), 256, 0, st2>>>(csip.p, n, aged, static_cast<const W*>(d_rough), d_si, keep.p);
+            // a quarter of the GPU: the retain has the whole report to finish
+            k_retain<W, MAXR><<<blocks(n, 256, 2), 256, 0, st2>>>(csip.p, n, aged, static_cast<const W*>(d_rough), keep.p);
             check_launch();
             launched();
             cub_call([&](void* t, size_t& b) {
@@ -1213,7 +1375,25 @@ struct Engine {
             std::swap(csip.p, csip2.p);
             std::swap(csip.cap, csip2.cap);
         }
+        // indicators: clear all, re-set the retained hosts' bit in every row
+        // (sea.hpp:318, 333-335); read again only by the next slice's K4
+        CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st2));
+        if (ncsip) {
+            k_si_mark<<<blocks(ncsip), 256, 0, st2>>>(csip.p, static_cast<uint32_t>(ncsip), dc, d_si);
+            check_launch();
+            launched();
+        }
         rebuild_cset(ncsip, st2);
+        if (ncsip) {  // into the spare buffer: a queued report may still read the current view
+            sorted_tmp.ensure(ncsip);
+            cub_call([&](void* t, size_t& b) {
+                return cub::DeviceRadixSort::SortKeys(t, b, csip.p, sorted_tmp.p, static_cast<int>(ncsip), 0, 32, st2);
+            }, &temp2);
+            std::swap(sorted_ret.p, sorted_tmp.p);
+            std::swap(sorted_ret.cap, sorted_tmp.cap);
+        }
+        nsorted_ret = ncsip;
+        sorted_ret_valid = true;
         CK(cudaEventRecord(ev_maint, st2));
         maint_pending = true;
         trace("  slide: finish (maintenance queued)");
@@ -1269,27 +1449,37 @@ struct Engine {
     void end_slice(uint64_t slice_id, bool want_report, srla_entry* out, const Compact* compact = nullptr) {
         const bool due = want_report && slice_id + 1 >= cfg.window;
         trace(nullptr);
+        eos_host_t0 = std::chrono::steady_clock::now();
+        eos_mark("start");
         join_maint();
         stats.slides++;
         slide_begin();
+        eos_mark("begin");
         const auto w0 = std::chrono::steady_clock::now();
-        bool age_linear = false;
+        bool age_linear = false, finished = false;
+        // the slide maintenance is queued while the report's gather runs
+        auto finish = [&] {
+            eos_mark("reported");
+            slide_finish(false);
+            eos_mark("slid");
+            finished = true;
+        };
         if (epoch) {
             flush_linear();
-            if (due) report(out, nullptr, false, compact);
+            if (due) report(out, nullptr, false, compact, finish);
             trace("eos: report (epoch)");
         } else if (due && dc.k < dc.expired && use_bins) {
             d_counts.ensure(cfg.rows);
             CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
             flush_linear(2);
             trace("eos: split+apply+count+age");
-            report(out, nullptr, true, compact);
+            report(out, nullptr, true, compact, finish);
             trace("eos: report");
         } else if (due && dc.k < dc.expired) {
             d_counts.ensure(cfg.rows);
             CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
             with_w([&](auto w) { count_age_range<decltype(w)>(0, uint64_t(cfg.rows) * lin_words, true); });
-            report(out, nullptr, true, compact);
+            report(out, nullptr, true, compact, finish);
             trace("eos: report");
         } else if (!due && use_bins) {
             flush_linear(1);
@@ -1299,8 +1489,13 @@ struct Engine {
             if (use_bins) flush_linear(1);
         }
         const auto w1 = std::chrono::steady_clock::now();
-        slide_finish(age_linear);
+        if (!finished) {
+            eos_mark("reported");
+            slide_finish(age_linear);
+            eos_mark("slid");
+        }
         CK(cudaStreamSynchronize(st));
+        eos_dump();
         timing.slide_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w1).count();
         (void)w0;
         resolve_timers(false);
@@ -1309,6 +1504,7 @@ struct Engine {
 
     // ------------------------------------------------------------ queries
     void set_candidates(const uint32_t* h, uint64_t n) {
+        sorted_ret_valid = false;
         std::vector<uint32_t> uniq;
         uniq.reserve(n);
         std::unordered_set<uint32_t> seen;

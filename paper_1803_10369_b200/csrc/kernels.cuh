@@ -532,20 +532,45 @@ __global__ void __launch_bounds__(256) k_age(W* __restrict__ t, uint64_t words, 
     }
 }
 
-// Candidate re-validation after aging (sea.hpp:328-336): flags kept hosts and
-// re-sets their indicator bit in all rows.
+// Candidate re-validation after aging (sea.hpp:328-336): flags kept hosts
+// (union rough weight >= thr). The caller passes the window it tests against.
 template <typename W, int MAXR>
 __global__ void __launch_bounds__(256) k_retain(const uint32_t* __restrict__ csip, uint32_t n, DevCfg c,
-                                                const W* __restrict__ rough, uint16_t* __restrict__ si,
-                                                uint8_t* __restrict__ keep) {
+                                                const W* __restrict__ rough, uint8_t* __restrict__ keep) {
+    for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < n; h += gridDim.x * blockDim.x)
+        keep[h] = rough_weight<W, MAXR>(c, rough, nullptr, csip[h], 0, false) >= c.thr;
+}
+
+// Re-set the indicator bit of each kept host in every row (sea.hpp:333-335).
+__global__ void __launch_bounds__(256) k_si_mark(const uint32_t* __restrict__ hosts, uint32_t n, DevCfg c,
+                                                 uint16_t* __restrict__ si) {
     for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < n; h += gridDim.x * blockDim.x) {
-        const uint32_t a = csip[h];
-        const bool k = rough_weight<W, MAXR>(c, rough, nullptr, a, 0, false) >= c.thr;
-        keep[h] = k;
-        if (k) {
-            const uint16_t bit = static_cast<uint16_t>(1u << indicator_bit_index(c, a));
-            for (uint32_t i = 0; i < c.rows; ++i)
-                atomic_or_u16(si + static_cast<uint64_t>(i) * c.cols + column_of(c, i, a), bit);
+        const uint32_t a = hosts[h];
+        const uint16_t bit = static_cast<uint16_t>(1u << indicator_bit_index(c, a));
+        for (uint32_t i = 0; i < c.rows; ++i)
+            atomic_or_u16(si + static_cast<uint64_t>(i) * c.cols + column_of(c, i, a), bit);
+    }
+}
+
+// Merge two ascending lists of distinct hosts (merge path: each thread finds
+// its split of the first d outputs by binary search, then emits 8).
+__global__ void __launch_bounds__(256) k_merge_sorted(const uint32_t* __restrict__ a, uint32_t na,
+                                                      const uint32_t* __restrict__ b, uint32_t nb,
+                                                      uint32_t* __restrict__ out) {
+    const uint64_t n = static_cast<uint64_t>(na) + nb;
+    for (uint64_t d = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8; d < n;
+         d += static_cast<uint64_t>(gridDim.x) * blockDim.x * 8) {
+        uint64_t lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+        while (lo < hi) {  // i = #a among the first d outputs
+            const uint64_t mid = (lo + hi) / 2;
+            if (a[mid] < b[d - 1 - mid]) lo = mid + 1;
+            else hi = mid;
+        }
+        uint64_t i = lo, j = d - lo;
+        const uint64_t e = d + 8 < n ? d + 8 : n;
+        for (uint64_t o = d; o < e; ++o) {
+            const bool take_a = j >= nb || (i < na && a[i] < b[j]);
+            out[o] = take_a ? a[i++] : b[j++];
         }
     }
 }

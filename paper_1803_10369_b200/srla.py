@@ -64,7 +64,9 @@ class CTiming(C.Structure):
                 ("split_entries", C.c_uint64), ("apply_kernel_ms", C.c_double),
                 ("apply_kernel_launches", C.c_uint64), ("apply_entries", C.c_uint64),
                 ("apply_stream_bytes", C.c_uint64), ("gather_kernel_ms", C.c_double),
-                ("gather_kernel_launches", C.c_uint64), ("gather_bytes", C.c_uint64)]
+                ("gather_kernel_launches", C.c_uint64), ("gather_bytes", C.c_uint64),
+                ("sync_wait_ms", C.c_double), ("syncs", C.c_uint64), ("alloc_ms", C.c_double),
+                ("allocs", C.c_uint64)]
 
 
 class CPlant(C.Structure):

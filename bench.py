@@ -124,16 +124,18 @@ class Clocks:
 
 # ---------------------------------------------------------------- rooflines
 
-def ncu_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of each kernel,
-    from the committed ncu --set full summary (profiles/ncu_summary.json)."""
+def ncu_traffic(workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of each kernel
+    for this workload, from the committed ncu --set full summary
+    (profiles/ncu_summary.json, tools/ncu_summary.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return {}
-    return {k: v.get("dram_bytes_per_launch") for k, v in json.load(open(p)).get("kernels", {}).items()}
+    wl = json.load(open(p)).get("workloads", {}).get(workload, {})
+    return {k: v.get("dram_bytes_per_launch") for k, v in wl.items()}
 
 
-def kernel_rooflines(tm, step_ms_total, cfg, peak, peak_src, packets, steps):
+def kernel_rooflines(tm, step_ms_total, cfg, peak, peak_src, packets, steps, workload):
     """Per-kernel algorithmic bytes / device time (CUDA events on the engine
     stream around every launch, summed over the timed steps).
 
@@ -147,7 +149,7 @@ def kernel_rooflines(tm, step_ms_total, cfg, peak, peak_src, packets, steps):
     4 random 32-B sector updates) over K1 + split + apply time."""
     binned = tm["split_kernel_launches"] > 0 or tm["apply_kernel_launches"] > 0
     rows = cfg.rows
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(workload)
     ks = {
         "k_scan_bin" if binned else "k_scan": (
             tm["scan_kernel_ms"], tm["scan_kernel_launches"],
@@ -373,7 +375,8 @@ def run_engine(args):
     value = packets / (ms / 1e3)
 
     peak, peak_src = measured_peaks()
-    roofline, kernels, path = kernel_rooflines(tm, ms, cfg, peak, peak_src, tm["scan_kernel_records"], args.steps)
+    roofline, kernels, path = kernel_rooflines(tm, ms, cfg, peak, peak_src, tm["scan_kernel_records"], args.steps,
+                                              args.workload)
 
     # end to end through the public API with host buffers (pinned), H2D inside:
     # scan_batch(host) + end_slice_async/wait, so a slice's host->device copies

@@ -587,7 +587,7 @@ struct Engine {
         fcfg.streamed = d_streamed.p;
         CK(cudaMemsetAsync(fine_count.p, 0, fine_count.cap * sizeof(uint32_t), st));
         const int smem = static_cast<int>((1ull << fs) * wb);
-        split_smem = kSplitTile * 4 + fcfg.per_region * 14;
+        split_smem = kSplitTile * 4 + fcfg.per_region * 16;
         with_w([&](auto w) {
             using W = decltype(w);
             CK(cudaFuncSetAttribute(k_split<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(split_smem)));

@@ -330,31 +330,36 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
                                                          uint32_t region_shift, FineCfg f, EpochCfg ep,
                                                          W* __restrict__ lin) {
     // dynamic shared memory, sized by the fan-out f.per_region (<= 4096):
-    //   sorted[kSplitTile] | cnt[P] | lbase[P] | dst[P] | fit[P] (u16)
+    //   sorted[kSplitTile] | cnt[P] | lbase[P] | win[P] (uint2)
     extern __shared__ uint32_t s_dyn[];
     uint32_t* s_sorted = s_dyn;  // (slice << 16) | offset within slice
     uint32_t* s_cnt = s_sorted + kSplitTile;
     uint32_t* s_lbase = s_cnt + f.per_region;
-    uint32_t* s_dst = s_lbase + f.per_region;  // nfine * cap < 2^32 by construction (Engine::setup_bins)
-    uint16_t* s_fit = reinterpret_cast<uint16_t*>(s_dst + f.per_region);
+    // per fine slice: {bin slot of sorted entry i = x + i (mod 2^32; nfine * cap < 2^32 by
+    // construction, Engine::setup_bins), first sorted index that no longer fits its bin}
+    uint2* s_win = reinterpret_cast<uint2*>(s_lbase + f.per_region);
     __shared__ uint32_t s_warp[kSplitThreads / 32];
+    __shared__ uint32_t s_region;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t total_tiles = tile_prefix[nregions];
     const uint32_t fmask = (1u << f.shift) - 1u;
     const uint32_t per_thread = (f.per_region + kSplitThreads - 1) / kSplitThreads;
     for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        uint32_t lo = 0, hi = nregions;  // region r with tile_prefix[r] <= t < tile_prefix[r+1]
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) / 2;
-            if (tile_prefix[mid] <= t) lo = mid;
-            else hi = mid;
+        if (tid == 0) {  // region r with tile_prefix[r] <= t < tile_prefix[r+1]
+            uint32_t lo = 0, hi = nregions;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) / 2;
+                if (tile_prefix[mid] <= t) lo = mid;
+                else hi = mid;
+            }
+            s_region = lo;
         }
-        const uint32_t r = lo;
+        for (uint32_t i = tid; i < f.per_region; i += kSplitThreads) s_cnt[i] = 0;
+        __syncthreads();
+        const uint32_t r = s_region;
         const uint32_t begin = (t - tile_prefix[r]) * kSplitTile;
         const uint32_t n = min(coarse_n[r] - begin, static_cast<uint32_t>(kSplitTile));
         const uint32_t* src = coarse + static_cast<uint64_t>(r) * coarse_cap + begin;
-        for (uint32_t i = tid; i < f.per_region; i += kSplitThreads) s_cnt[i] = 0;
-        __syncthreads();
         uint32_t off[kSplitPerThread];
         const uint32_t e0 = tid * kSplitPerThread;
         if (e0 + kSplitPerThread <= n) {
@@ -395,8 +400,8 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
             s_lbase[b] = run;
             if (cn) {
                 const uint32_t g = atomicAdd(f.count + fine0 + b, cn);
-                s_dst[b] = (fine0 + b) * f.cap + g;
-                s_fit[b] = static_cast<uint16_t>(g >= f.cap ? 0u : min(cn, f.cap - g));
+                const uint32_t fit = g >= f.cap ? 0u : min(cn, f.cap - g);
+                s_win[b] = make_uint2((fine0 + b) * f.cap + g - run, run + fit);
             }
             run += cn;
         }
@@ -408,20 +413,26 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
                 s_sorted[s_lbase[b] + rank[k]] = (b << 16) | (off[k] & fmask);
             }
         __syncthreads();
+        bool ovf = false;
         for (uint32_t i = tid; i < n; i += kSplitThreads) {
             const uint32_t v = s_sorted[i];
-            const uint32_t b = v >> 16;
-            const uint32_t j = i - s_lbase[b];
-            if (j < s_fit[b]) {
-                f.bins[s_dst[b] + j] = static_cast<uint16_t>(v);
-            } else if (ep.on) {  // fine bin full: mark in place (marks commute)
-                mark_epoch_global(reinterpret_cast<uint8_t*>(lin),
-                                  (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift) +
-                                      (v & 0xFFFFu),
-                                  ep.row_words, ep.cur, ep.hist);
-            } else {
-                mark_word<W>(lin + (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift),
-                             v & 0xFFFFu);
+            const uint2 wv = s_win[v >> 16];
+            if (i < wv.y) f.bins[wv.x + i] = static_cast<uint16_t>(v);
+            else ovf = true;
+        }
+        if (__syncthreads_or(ovf)) {  // a fine bin is full: mark in place (marks commute)
+            for (uint32_t i = tid; i < n; i += kSplitThreads) {
+                const uint32_t v = s_sorted[i];
+                const uint32_t b = v >> 16;
+                if (i < s_win[b].y) continue;
+                if (ep.on)
+                    mark_epoch_global(reinterpret_cast<uint8_t*>(lin),
+                                      (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift) +
+                                          (v & 0xFFFFu),
+                                      ep.row_words, ep.cur, ep.hist);
+                else
+                    mark_word<W>(lin + (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift),
+                                 v & 0xFFFFu);
             }
         }
         __syncthreads();

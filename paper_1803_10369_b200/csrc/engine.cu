@@ -25,6 +25,7 @@
 #include "kernels.cuh"
 #include "scan_binned.cuh"
 #include "epoch.cuh"
+#include "nibble.cuh"
 #include "srla.h"
 
 namespace srla {
@@ -190,6 +191,7 @@ struct Engine {
 
     // binned linear marks (scan_binned.cuh), for tables larger than L2
     bool use_bins = false;
+    bool nib = false;  // linear recorders packed two per byte (nibble.cuh)
     BinCfg bcfg{};
     DevBuf<uint32_t> bins, bin_count, tile_prefix, fine_count;
     DevBuf<uint16_t> fine_bins;
@@ -270,7 +272,7 @@ struct Engine {
         *out = timing;
         out->alloc_ms = g_alloc_ms;
         out->allocs = g_allocs;
-        if (pin_streamed.p) out->apply_stream_bytes = 2ull * pin_streamed.p[0] * ((1ull << fcfg.shift) * wb);
+        if (pin_streamed.p) out->apply_stream_bytes = 2ull * pin_streamed.p[0] * lin_bytes(1ull << fcfg.shift);
     }
     void timing_clear() {
         resolve_timers(true);
@@ -331,17 +333,21 @@ struct Engine {
         lin_words = static_cast<uint64_t>(cfg.cols) * cfg.linear_slots;
         rough_words = static_cast<uint64_t>(cfg.cols) * cfg.rough_slots;
         const uint64_t rows = cfg.rows;
-        CK(cudaMalloc(&d_lin, rows * lin_words * wb));
+        ctr.ensure(16);
+        pin_ctr.ensure(16);
+        setup_bins();  // decides the linear table's packing (nibble.cuh)
+        CK(cudaMalloc(&d_lin, lin_bytes(rows * lin_words)));
         CK(cudaMalloc(&d_rough, rows * rough_words * wb));
         CK(cudaMalloc(&d_si, rows * cfg.cols * sizeof(uint16_t)));
         CK(cudaMalloc(&d_stamp, rows * rough_words * sizeof(uint32_t)));
-        fill_expired(d_lin, rows * lin_words);
+        if (nib) {
+            CK(cudaMemsetAsync(d_lin, static_cast<int>(dc.expired * 0x11u), lin_bytes(rows * lin_words), st));
+        } else {
+            fill_expired(d_lin, rows * lin_words);
+        }
         fill_expired(d_rough, rows * rough_words);
         CK(cudaMemsetAsync(d_si, 0, rows * cfg.cols * sizeof(uint16_t), st));
         CK(cudaMemsetAsync(d_stamp, 0xFF, rows * rough_words * sizeof(uint32_t), st));
-        ctr.ensure(16);
-        pin_ctr.ensure(16);
-        setup_bins();
         setup_epoch();
         if (use_bins) reserve_candidates(size_t(1) << 21);
         rebuild_cset(1024);
@@ -534,16 +540,39 @@ struct Engine {
     }
 
     // ------------------------------------------------------------ binned linear marks
+    // Bytes of `words` linear recorders in the device layout.
+    uint64_t lin_bytes(uint64_t words) const { return nib ? words / 2 : words * wb; }
+
+    // Epoch stamps (epoch.cuh) for this config: tables of 16 GiB and more, or
+    // srla_config.flags / SRLA_EPOCH (setup_epoch may still decline).
+    bool epoch_wanted() const {
+        const char* env = std::getenv("SRLA_EPOCH");
+        bool want = uint64_t(cfg.rows) * lin_words * wb >= (16ull << 30);
+        if (cfg.flags & SRLA_FLAG_EPOCH) want = true;
+        if (cfg.flags & SRLA_FLAG_LITERAL) want = false;
+        if (env) want = env[0] == '1';
+        return want;
+    }
+
     void setup_bins() {
-        const uint64_t total_words = uint64_t(cfg.rows) * lin_words;
         const char* direct = std::getenv("SRLA_DIRECT_MARKS");  // A/B switch for measurements
+        if (cfg.rows > kBinRows || (direct && direct[0] == '1')) return;
+        // literal recorders of z <= 4 bits packed two per byte when the table
+        // geometry allows it (every slice whole and 16-byte aligned)
+        const char* ne = std::getenv("SRLA_NIBBLE");
+        nib = wb == 1 && cfg.recorder_bits <= 4 && !epoch_wanted() && !(ne && ne[0] == '0');
+        if (nib && !setup_bins_geometry()) nib = false;
+        if (!nib) setup_bins_geometry();
+    }
+
+    bool setup_bins_geometry() {
+        const uint64_t total_words = uint64_t(cfg.rows) * lin_words;
         const char* force = std::getenv("SRLA_FORCE_BINS");     // exercise the binned path on small tables (tests)
         const bool forced = force && force[0] == '1';
-        if (cfg.rows > kBinRows || (direct && direct[0] == '1')) return;
         const bool small = total_words * wb < (256ull << 20);
-        if (!forced && small) return;
+        if (!forced && small) return false;
         uint32_t shift = 0;
-        while ((1ull << (shift + 1)) * wb <= (32ull << 20)) ++shift;  // 32 MB coarse regions
+        while (lin_bytes(1ull << (shift + 1)) <= (32ull << 20)) ++shift;  // 32 MB coarse regions
         if (forced)
             while (shift > 4 && (total_words >> shift) < 8) --shift;  // ~8 regions even for tiny tables
         while (((total_words + (1ull << shift) - 1) >> shift) > kMaxRegions) ++shift;
@@ -551,11 +580,17 @@ struct Engine {
         uint32_t fs = 0;
         uint64_t fine_bytes = 32ull << 10;  // 32 KB: two buffers per block
         if (const char* fk = std::getenv("SRLA_FINE_KB")) fine_bytes = std::strtoull(fk, nullptr, 10) << 10;
-        while ((1ull << (fs + 1)) * wb <= fine_bytes) ++fs;
+        while (lin_bytes(1ull << (fs + 1)) <= fine_bytes) ++fs;
+        if (nib) fs = std::min<uint32_t>(fs, 16);  // u16 offsets within a slice
         fs = std::min(fs, shift);
         if (forced && small) fs = std::max<uint32_t>(std::min<uint32_t>(shift, 4), shift > 3 ? shift - 3 : 0);
         while (shift - fs > 12) ++fs;  // split fan-out <= 4096 slices per region
-        if ((1ull << fs) * wb > (64ull << 10)) return;  // slices must fit twice in shared memory
+        if (lin_bytes(1ull << fs) > (64ull << 10) || fs > 16) return false;  // slices fit twice in shared memory
+        if (nib) {  // nibble tables: whole, 16-byte slices; rows of whole 16-byte vectors (bulk kernel only)
+            const uint64_t slice_words = 1ull << fs;
+            if (lin_bytes(slice_words) % 16 || (lin_words % 32) || lin_words < slice_words || total_words % slice_words)
+                return false;
+        }
         bcfg.region_shift = shift;
         bcfg.nregions = static_cast<uint32_t>((total_words + (1ull << shift) - 1) >> shift);
         const uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);
@@ -586,7 +621,7 @@ struct Engine {
         CK(cudaMemsetAsync(d_streamed.p, 0, sizeof(unsigned long long), st));
         fcfg.streamed = d_streamed.p;
         CK(cudaMemsetAsync(fine_count.p, 0, fine_count.cap * sizeof(uint32_t), st));
-        const int smem = static_cast<int>((1ull << fs) * wb);
+        const int smem = static_cast<int>(lin_bytes(1ull << fs));
         split_smem = kSplitTile * 4 + fcfg.per_region * 16;
         with_w([&](auto w) {
             using W = decltype(w);
@@ -594,24 +629,22 @@ struct Engine {
             CK(cudaFuncSetAttribute(k_slice_apply<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(smem, 16)));
             CK(cudaFuncSetAttribute(k_slice_apply_bulk<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(2 * smem, 32)));
         });
+        CK(cudaFuncSetAttribute(k_slice_apply_nib, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(2 * smem, 32)));
         // bulk (TMA) slices need 16-byte slices and rows at least one slice long
         const uint64_t slice_words = 1ull << fs;
-        bulk_ok = (slice_words * wb) % 16 == 0 && (lin_words * wb) % 16 == 0 && lin_words >= slice_words;
-        bulk_end = (total_words % slice_words) * wb % 16 == 0 ? fcfg.nfine : fcfg.nfine - 1;
+        bulk_ok = lin_bytes(slice_words) % 16 == 0 && lin_bytes(lin_words) % 16 == 0 && lin_words >= slice_words;
+        bulk_end = lin_bytes(total_words % slice_words) % 16 == 0 ? fcfg.nfine : fcfg.nfine - 1;
         if (total_words % slice_words) bulk_end = fcfg.nfine - 1;  // partial last slice: plain kernel
+        bcfg.nib = fcfg.nib = nib ? 1u : 0u;
         use_bins = true;
+        return true;
     }
 
     // Epoch stamps replace the O(table) slide by O(1) + a 1/(255-expired)
     // sweep, at the price of a CAS per mark. Chosen for tables of 16 GiB and
     // more (the 2^24-column sketch), or by srla_config.flags / SRLA_EPOCH.
     void setup_epoch() {
-        const char* env = std::getenv("SRLA_EPOCH");
-        bool want = uint64_t(cfg.rows) * lin_words * wb >= (16ull << 30);
-        if (cfg.flags & SRLA_FLAG_EPOCH) want = true;
-        if (cfg.flags & SRLA_FLAG_LITERAL) want = false;
-        if (env) want = env[0] == '1';
-        if (!want || !use_bins || wb != 1 || dc.expired > 127) return;
+        if (!epoch_wanted() || nib || !use_bins || wb != 1 || dc.expired > 127) return;
         if (lin_words < (1ull << fcfg.shift)) return;  // a slice may span at most two rows
         epoch = true;
         cur_epoch = 0;
@@ -627,6 +660,26 @@ struct Engine {
         launched();
         CK(cudaFuncSetAttribute(k_slice_stamp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 std::max<int>(32, int(2u << fcfg.shift))));
+    }
+
+    // Unpack a nibble table to a byte per recorder (an import carried values
+    // above 15); the bin geometry is rebuilt for the byte layout.
+    void leave_nibble() {
+        if (!nib) return;
+        flush_linear();
+        const uint64_t words = uint64_t(cfg.rows) * lin_words;
+        void* wide = nullptr;
+        CK(cudaMalloc(&wide, words));
+        k_unpack_nib<<<blocks(words / 2, 256, 16), 256, 0, st>>>(static_cast<const uint8_t*>(d_lin), words / 2,
+                                                                 static_cast<uint8_t*>(wide));
+        check_launch();
+        launched();
+        CK(cudaStreamSynchronize(st));
+        CK(cudaFree(d_lin));
+        d_lin = wide;
+        nib = false;
+        if (!setup_bins_geometry()) use_bins = false;
+        CK(cudaStreamSynchronize(st));
     }
 
     // Literal recorder value of a stamp (recorders.hpp:84-87 applied cur - s times).
@@ -732,7 +785,12 @@ struct Engine {
             pending_entries = 0;
             return;
         }
-        with_w([&](auto w) {
+        if (nib) {
+            k_slice_apply_nib<<<std::min<uint32_t>(fcfg.nfine, sms * 3), 256, 2 * lin_bytes(1ull << fcfg.shift), st>>>(
+                static_cast<uint8_t*>(d_lin), lin_words, fcfg, fcfg.nfine, mode, cfg.window, dc.expired, d_counts.p);
+            check_launch();
+            launched();
+        } else with_w([&](auto w) {
             using W = decltype(w);
             const size_t smem = (1ull << fcfg.shift) * sizeof(W);
             uint32_t begin = 0;
@@ -1089,6 +1147,12 @@ struct Engine {
     }
     void union_linear(const uint32_t* d_hosts, uint32_t n, uint32_t* d_out, uint32_t kthr) {
         if (!n) return;
+        if (nib) {
+            k_union_linear_nib<4><<<blocks(uint64_t(n) * 32, 256, 16), 256, 0, st>>>(d_hosts, n, dc, static_cast<const uint8_t*>(d_lin), kthr, d_out);
+            check_launch();
+            launched();
+            return;
+        }
         if (epoch) {
             if (cfg.rows <= 4)
                 k_union_linear_epoch<4><<<blocks(uint64_t(n) * 32, 256, 16), 256, 0, st>>>(d_hosts, n, dc, static_cast<const uint8_t*>(d_lin), cur_epoch, d_out);
@@ -1108,7 +1172,10 @@ struct Engine {
     void row_active_async() {
         d_counts.ensure(cfg.rows);
         CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
-        with_w([&](auto w) {
+        if (nib) {
+            dim3 grid(blocks(lin_bytes(lin_words) / 4, 256, std::max(1u, 16u / std::min(16u, cfg.rows))), cfg.rows);
+            k_row_active_nib<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(d_lin), lin_words, cfg.window, d_counts.p);
+        } else with_w([&](auto w) {
             using W = decltype(w);
             const uint64_t vecs = lin_words * sizeof(W) / 16 + 1;
             dim3 grid(blocks(vecs, 256, std::max(1u, 16u / std::min(16u, cfg.rows))), cfg.rows);
@@ -1219,7 +1286,7 @@ struct Engine {
                 union_linear(sh + lo, hi - lo, weights.p + lo, kthr);
                 timer_stop(tg, kTimeGather);
                 timing.gather_kernel_launches += 1;
-                timing.gather_bytes += uint64_t(hi - lo) * cfg.rows * cfg.linear_slots * wb;
+                timing.gather_bytes += uint64_t(hi - lo) * cfg.rows * lin_bytes(cfg.linear_slots);
                 if (hdst) {
                     CK(cudaEventRecord(ev_part[c], st));
                     CK(cudaStreamWaitEvent(ds, ev_part[c], 0));
@@ -1574,7 +1641,13 @@ struct Engine {
             uint16_t s = 0;
             CK(cudaMemcpyAsync(&s, d_si + uint64_t(i) * cfg.cols + col, 2, cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(rb.data(), static_cast<uint8_t*>(d_rough) + (uint64_t(i) * rough_words + col * cfg.rough_slots) * wb, rb.size(), cudaMemcpyDeviceToHost, st));
-            if (linear)
+            if (linear && nib) {  // gl is a multiple of 32 in nibble mode: whole bytes
+                std::vector<uint8_t> pk(cfg.linear_slots / 2);
+                CK(cudaMemcpyAsync(pk.data(), static_cast<uint8_t*>(d_lin) + lin_bytes(uint64_t(i) * lin_words + col * cfg.linear_slots),
+                                   pk.size(), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                for (uint32_t j = 0; j < cfg.linear_slots; ++j) lb[j] = (pk[j >> 1] >> (4 * (j & 1))) & 0xF;
+            } else if (linear)
                 CK(cudaMemcpyAsync(lb.data(), static_cast<uint8_t*>(d_lin) + (uint64_t(i) * lin_words + col * cfg.linear_slots) * wb, lb.size(), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             acc &= s;
@@ -1598,13 +1671,24 @@ struct Engine {
         const uint64_t b = row_bytes(kind);
         if (kind == SRLA_INDICATOR) return reinterpret_cast<uint8_t*>(d_si) + row * b;
         if (kind == SRLA_ROUGH) return static_cast<uint8_t*>(d_rough) + row * b;
-        return static_cast<uint8_t*>(d_lin) + row * b;
+        return static_cast<uint8_t*>(d_lin) + lin_bytes(uint64_t(row) * lin_words);
     }
 
     void export_row(uint32_t row, int kind, void* buf, uint64_t bytes) {
         flush_linear();
         uint8_t* p = row_ptr(row, kind);
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
+        if (nib && kind == SRLA_LINEAR) {  // unpack to the reference's byte per recorder
+            std::vector<uint8_t> pk(lin_bytes(lin_words));
+            CK(cudaMemcpyAsync(pk.data(), p, pk.size(), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            uint8_t* b = static_cast<uint8_t*>(buf);
+            for (uint64_t j = 0; j < pk.size(); ++j) {
+                b[2 * j] = pk[j] & 0xF;
+                b[2 * j + 1] = pk[j] >> 4;
+            }
+            return;
+        }
         CK(cudaMemcpyAsync(buf, p, bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (epoch && kind == SRLA_LINEAR) {
@@ -1619,6 +1703,21 @@ struct Engine {
         flush_linear();
         uint8_t* p = row_ptr(row, kind);
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
+        if (nib && kind == SRLA_LINEAR) {
+            const uint8_t* v = static_cast<const uint8_t*>(buf);
+            bool in_model = true;
+            for (uint64_t j = 0; j < bytes && in_model; ++j) in_model = v[j] <= 0xF;
+            if (!in_model) {  // values a nibble cannot hold: back to a byte per recorder
+                leave_nibble();
+                import_row(row, kind, buf, bytes);
+                return;
+            }
+            std::vector<uint8_t> pk(bytes / 2);
+            for (uint64_t j = 0; j < pk.size(); ++j) pk[j] = static_cast<uint8_t>(v[2 * j] | (v[2 * j + 1] << 4));
+            CK(cudaMemcpyAsync(p, pk.data(), pk.size(), cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
+            return;
+        }
         if (epoch && kind == SRLA_LINEAR) {
             const uint8_t* v = static_cast<const uint8_t*>(buf);
             bool in_model = true;

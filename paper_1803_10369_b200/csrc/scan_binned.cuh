@@ -24,6 +24,7 @@ struct BinCfg {
     uint32_t nregions;
     uint32_t cap;
     uint32_t region_shift;  // log2(words per region)
+    uint32_t nib;           // linear recorders packed two per byte (nibble.cuh)
 };
 
 constexpr int kBinThreads = 256;
@@ -64,6 +65,11 @@ __device__ __forceinline__ void mark_epoch_global(uint8_t* lin, uint64_t word, u
         atomicAdd(h + old, ~0ull);  // -1
         atomicAdd(h + cur, 1ull);
     }
+}
+
+// "store 0" into packed recorder w (two per byte, low nibble for even w)
+__device__ __forceinline__ void mark_nibble_global(uint8_t* lin, uint64_t w) {
+    atomicAnd(reinterpret_cast<unsigned int*>(lin + ((w >> 1) & ~3ull)), ~(0xFu << (4u * static_cast<uint32_t>(w & 7u))));
 }
 
 // "store 0" into one recorder word (recorder_mark) as a 32-bit AND, which the
@@ -228,6 +234,8 @@ __global__ void __launch_bounds__(kBinThreads, 3) k_scan_bin(const uint32_t* __r
                 if (ep.on)
                     mark_epoch_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << b.region_shift) + s_off[idx],
                                       ep.row_words, ep.cur, ep.hist);
+                else if (b.nib)
+                    mark_nibble_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << b.region_shift) + s_off[idx]);
                 else
                     mark_word<W>(lin + (static_cast<uint64_t>(r) << b.region_shift), s_off[idx]);
             }
@@ -314,6 +322,7 @@ struct FineCfg {
     uint32_t per_region;  // fine slices per coarse region = 2^(region_shift - shift)
     uint32_t nfine;       // total fine slices covering the table
     unsigned long long* streamed;  // whole slices read + written by the apply kernels (statistics)
+    uint32_t nib;                  // linear recorders packed two per byte (nibble.cuh)
 };
 
 constexpr int kSplitThreads = 512;
@@ -430,6 +439,9 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
                                       (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift) +
                                           (v & 0xFFFFu),
                                       ep.row_words, ep.cur, ep.hist);
+                else if (f.nib)
+                    mark_nibble_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << region_shift) +
+                                                                            (static_cast<uint64_t>(b) << f.shift) + (v & 0xFFFFu));
                 else
                     mark_word<W>(lin + (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift),
                                  v & 0xFFFFu);

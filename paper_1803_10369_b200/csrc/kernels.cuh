@@ -419,9 +419,16 @@ __global__ void __launch_bounds__(256) k_union_linear(const uint32_t* __restrict
     for (uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < n; h += warps) {
         const uint32_t a = hosts[h];
         const W* cell[MAXR];
+        if (MAXR <= 4) {  // lane i hashes row i; the warp shares the columns
+            const uint32_t colv = lane < c.rows ? column_of(c, lane, a) : 0u;
 #pragma unroll
-        for (int i = 0; i < MAXR; ++i)
-            if (i < static_cast<int>(c.rows)) cell[i] = lin + i * lrow + static_cast<uint64_t>(column_of(c, i, a)) * c.gl;
+            for (int i = 0; i < MAXR; ++i)
+                cell[i] = lin + i * lrow + static_cast<uint64_t>(__shfl_sync(0xFFFFFFFFu, colv, i)) * c.gl;
+        } else {
+#pragma unroll
+            for (int i = 0; i < MAXR; ++i)
+                if (i < static_cast<int>(c.rows)) cell[i] = lin + i * lrow + static_cast<uint64_t>(column_of(c, i, a)) * c.gl;
+        }
         uint32_t acc = 0;
         if (vec && MAXR <= 4) {
             // all rows' vectors of two iterations issued before any use: 8

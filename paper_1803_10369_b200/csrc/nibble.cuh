@@ -22,13 +22,15 @@ __device__ __forceinline__ uint32_t nib_age(uint32_t x, uint32_t e8) {
     const uint32_t d = x ^ e8;
     return x + ((d | (d >> 1) | (d >> 2) | (d >> 3)) & kNibOne);
 }
+constexpr uint32_t kByteHi = 0x80808080u;
+// SWAR ">= k" on the even (low) nibbles of x, one per byte: bit 7 of byte j
+// is set iff recorder 2j >= k (x & kNibLo <= 15 and k <= 16: 0x80 | v - k
+// never borrows across bytes). Other bits are junk: mask with kByteHi.
+__device__ __forceinline__ uint32_t nib_ge_even(uint32_t x, uint32_t k4) { return ((x & kNibLo) | kByteHi) - k4; }
+__device__ __forceinline__ uint32_t nib_ge_odd(uint32_t x, uint32_t k4) { return (((x >> 4) & kNibLo) | kByteHi) - k4; }
 // number of the 8 packed recorders with value < k (k4 = k in every byte)
 __device__ __forceinline__ uint32_t nib_count_lt(uint32_t x, uint32_t k4) {
-    return (__popc(__vcmpltu4(x & kNibLo, k4)) + __popc(__vcmpltu4((x >> 4) & kNibLo, k4))) >> 3;
-}
-// per-recorder max of two packed words
-__device__ __forceinline__ uint32_t nib_max(uint32_t a, uint32_t b) {
-    return __vmaxu4(a & kNibLo, b & kNibLo) | (__vmaxu4((a >> 4) & kNibLo, (b >> 4) & kNibLo) << 4);
+    return 8u - __popc(nib_ge_even(x, k4) & kByteHi) - __popc(nib_ge_odd(x, k4) & kByteHi);
 }
 
 // k_slice_apply_bulk for nibble tables: fine slices of 2^f.shift recorders
@@ -162,10 +164,15 @@ __global__ void __launch_bounds__(256) k_union_linear_nib(const uint32_t* __rest
         const uint32_t nv = c.gl / 32;  // 16-byte vectors per cell
         for (uint64_t pair = warp0; pair * 2 < n; pair += warps) {
             const uint64_t h = pair * 2 + sub;
+            const uint32_t a = h < n ? hosts[h] : 0u;
+            // lane i of each half hashes row i; the half shares the columns
+            const uint32_t colv = sl < c.rows ? column_of(c, sl, a) : 0u;
+            const uint8_t* cell[MAXR];
+#pragma unroll
+            for (int i = 0; i < MAXR; ++i)
+                cell[i] = lin + ((i * lrow + static_cast<uint64_t>(__shfl_sync(0xFFFFFFFFu, colv, i, 16)) * c.gl) >> 1);
             uint32_t acc = 0;
             if (h < n) {
-                const uint8_t* cell[MAXR];
-                cells(hosts[h], cell);
                 for (uint32_t q0 = sl; q0 < nv; q0 += 32) {
                     uint4 x[2][MAXR];
 #pragma unroll
@@ -174,20 +181,23 @@ __global__ void __launch_bounds__(256) k_union_linear_nib(const uint32_t* __rest
                         for (int i = 0; i < MAXR; ++i)
                             x[u][i] = (i < static_cast<int>(c.rows) && q0 + 16u * u < nv)
                                           ? __ldcs(reinterpret_cast<const uint4*>(cell[i]) + q0 + 16u * u)
-                                          : make_uint4(0u, 0u, 0u, 0u);  // neutral for max
+                                          : make_uint4(0u, 0u, 0u, 0u);  // value 0: never >= k
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
                         if (q0 + 16u * u >= nv) break;
-                        uint4 m = x[u][0];
+                        // slot active in the union <=> no row has it >= k
+                        uint32_t ge[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-                        for (int i = 1; i < MAXR; ++i) {
-                            m.x = nib_max(m.x, x[u][i].x);
-                            m.y = nib_max(m.y, x[u][i].y);
-                            m.z = nib_max(m.z, x[u][i].z);
-                            m.w = nib_max(m.w, x[u][i].w);
+                        for (int i = 0; i < MAXR; ++i) {
+                            ge[0] |= nib_ge_even(x[u][i].x, k4); ge[1] |= nib_ge_odd(x[u][i].x, k4);
+                            ge[2] |= nib_ge_even(x[u][i].y, k4); ge[3] |= nib_ge_odd(x[u][i].y, k4);
+                            ge[4] |= nib_ge_even(x[u][i].z, k4); ge[5] |= nib_ge_odd(x[u][i].z, k4);
+                            ge[6] |= nib_ge_even(x[u][i].w, k4); ge[7] |= nib_ge_odd(x[u][i].w, k4);
                         }
-                        acc += nib_count_lt(m.x, k4) + nib_count_lt(m.y, k4) + nib_count_lt(m.z, k4) +
-                               nib_count_lt(m.w, k4);
+                        uint32_t g = 0;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) g += __popc(ge[j] & kByteHi);
+                        acc += 32u - g;
                     }
                 }
             }

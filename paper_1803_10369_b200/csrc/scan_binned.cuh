@@ -89,7 +89,7 @@ __device__ __forceinline__ void mark_word(W* base, uint32_t off) {
 // marks are binned by region; sampled packets stamp their rough entries and
 // append events exactly as k_scan does.
 template <typename W>
-__global__ void __launch_bounds__(kBinThreads, 3) k_scan_bin(const uint32_t* __restrict__ recs, uint32_t n, DevCfg c,
+__global__ void __launch_bounds__(kBinThreads, 4) k_scan_bin(const uint32_t* __restrict__ recs, uint32_t n, DevCfg c,
                                                          BinCfg b, EpochCfg ep, W* __restrict__ lin,
                                                          uint32_t* __restrict__ stamp, uint32_t* __restrict__ ev,
                                                          uint32_t ev_cap, uint32_t* __restrict__ ev_count, int vec) {

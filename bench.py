@@ -329,11 +329,40 @@ def run_engine(args):
                                              C.byref(nr)))
         return n.value, nr.value
 
+    # Overlapped pipeline (C2 default): srla_end_slice_async(s) returns at once and
+    # srla_scan_batch(s+1) bins its packets (K1) into the second bin set while
+    # slice s's end-of-slice still runs, then joins it; the report of slice s is
+    # collected with srla_end_slice_wait. Same work per step, pipelined.
+    abufs = [pinned_entries(rep_cap) for _ in range(2)] if args.overlap else None
+    pend = {"slot": None}
+
+    def collect():
+        if pend["slot"] is None:
+            return None
+        n, _ = eng.end_slice_wait()
+        rep = abufs[pend["slot"]][:n]
+        pend["slot"] = None
+        if world > 1:
+            allgather_report(rep)
+        return n
+
+    def step_overlapped(sid):
+        eng.scan(slices[sid % nres])  # joins the pending end-of-slice after its K1
+        n = collect()
+        eng.end_slice_async(sid, abufs[sid % 2])
+        pend["slot"] = sid % 2
+        return n
+
     sid = 0
     prefill = max(0, cfg.window - 1 - args.warmup)
     for _ in range(prefill + args.warmup):
-        step(sid)
+        if args.overlap:
+            step_overlapped(sid)
+        else:
+            step(sid)
         sid += 1
+    if args.overlap:
+        collect()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -347,13 +376,24 @@ def run_engine(args):
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(st)
     eos_dev, eos_wall, entries = [], [], []
-    for _ in range(args.steps):
-        _, n = step(sid)
+
+    def eos_sample(n):
         tm = eng.timing()
         eos_dev.append(tm["last_end_slice_device_ms"])
         eos_wall.append(tm["last_end_slice_wall_ms"])
         entries.append(n)
+
+    for _ in range(args.steps):
+        if args.overlap:
+            n = step_overlapped(sid)
+            if n is not None:
+                eos_sample(n)
+        else:
+            _, n = step(sid)
+            eos_sample(n)
         sid += 1
+    if args.overlap:
+        eos_sample(collect())
     t_end.record(st)
     t_end.synchronize()
     if dist:
@@ -435,7 +475,9 @@ def run_engine(args):
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference generator C2 spec, device port)",
             "config": {"workload": WORKLOADS[args.workload],
                        "packets_per_slice_per_gpu": n_per_gpu, "resident_slices": nres,
-                       "report_handoff": "srla_end_slice_compact: host+weight per entry and the Eq. 9 table"
+                       "report_handoff": "srla_end_slice_async/wait: 24-byte srla_entry per entry (pinned), "
+                                         "next slice's K1 overlapped" if args.overlap else
+                       "srla_end_slice_compact: host+weight per entry and the Eq. 9 table"
                        if args.handoff == "compact" else "srla_end_slice: 24-byte srla_entry per entry",
                        "l2": "inputs larger than L2 (1.2 GB per slice); no flush",
                        "parallelism": f"owner-partitioned x{world}" if world > 1 else "1 GPU"},
@@ -452,6 +494,7 @@ def run_engine(args):
                                        "sync_wait_ms", "syncs", "alloc_ms", "allocs")},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "overlapped_chunks": int(st1["overlapped_chunks"] - st0["overlapped_chunks"]),
             "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
             "library_launches": int(st1["library_launches"] - st0["library_launches"]),
             "clocks": clk,
@@ -476,11 +519,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi clock sampling period in the timed region")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--overlap", action="store_true",
+                    help="pipeline slice s+1's K1 under slice s's asynchronous end-of-slice (SRLA_OVERLAP=1; "
+                         "measured slower on C2, kept as an option)")
     ap.add_argument("--handoff", default="compact", choices=["compact", "entries"],
                     help="report hand-off of the device-resident steps (e2e always returns srla_entry)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.overlap:
+        os.environ["SRLA_OVERLAP"] = "1"
     if not args.resident:
         args.resident = 10 if args.workload == "c3" else 12
     if args.impl == "reference":

@@ -88,6 +88,7 @@ typedef struct srla_stats {
     uint64_t library_launches;/* CUB sort/scan/select launches (approximate) */
     uint64_t chunks;
     uint64_t slides;
+    uint64_t overlapped_chunks; /* K1 run under a pending asynchronous end-of-slice */
 } srla_stats;
 
 /* Last failure message on this thread ("" if none). */

@@ -9,6 +9,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -211,6 +212,23 @@ struct Engine {
     EpochCfg ecfg() const { return EpochCfg{epoch ? 1u : 0u, cur_epoch, hist.p, lin_words}; }
     PinBuf<uint32_t> pin_bc;
     uint64_t pending_entries = 0;
+    // Second region-bin set: a slice's K1 bins into it on stream sk while the
+    // previous slice's asynchronous end-of-slice still flushes the first
+    // (srla_end_slice_async followed by srla_scan_batch of device records).
+    DevBuf<uint32_t> bins_alt, bin_count_alt, ctr_k1;
+    PinBuf<uint32_t> pin_k1;
+    cudaStream_t sk = nullptr;
+    cudaEvent_t ev_scan_done = nullptr;
+    // the overlapped K1 starts once the end-of-slice has queued its split
+    // (K1 and the split are both SM-bound; the apply and gather that follow
+    // are HBM-bound and co-run with K1)
+    cudaEvent_t ev_k1_gate = nullptr;
+    std::atomic<bool> k1_gate{false};
+    bool in_async_eos = false;
+    // Measured on B200 (C2): K1 co-running with the end-of-slice slows both
+    // (K1 and the split are SM-bound; K1's shared memory and the apply's
+    // slices cannot co-reside), 6.4 vs 6.1 ms per slice, so it is opt-in.
+    bool overlap_on = [] { const char* v = std::getenv("SRLA_OVERLAP"); return v && v[0] == '1'; }();
     bool prefetch_next = false;  // bulk-prefetch region r+1 while applying r (measured slower; off)
 
     // ------------------------------------------------------------ kernel timers
@@ -301,6 +319,12 @@ struct Engine {
             CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         for (cudaEvent_t& e : ev_part) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&sk, cudaStreamNonBlocking, prio_low));
+        CK(cudaEventCreateWithFlags(&ev_scan_done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_k1_gate, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_scan_done, st));
+        ctr_k1.ensure(4);
+        pin_k1.ensure(4);
         for (int b = 0; b < 2; ++b) {
             CK(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ev_scanned[b], cudaEventDisableTiming));
@@ -389,6 +413,12 @@ struct Engine {
             cudaStreamSynchronize(ds);
             cudaStreamDestroy(ds);
         }
+        if (sk) {
+            cudaStreamSynchronize(sk);
+            cudaStreamDestroy(sk);
+        }
+        if (ev_scan_done) cudaEventDestroy(ev_scan_done);
+        if (ev_k1_gate) cudaEventDestroy(ev_k1_gate);
         if (st) cudaStreamDestroy(st);
     }
 
@@ -593,10 +623,17 @@ struct Engine {
         }
         bcfg.region_shift = shift;
         bcfg.nregions = static_cast<uint32_t>((total_words + (1ull << shift) - 1) >> shift);
-        const uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);
+        // forced-binned small tables (tests): tiny bins, so the overflow paths run
+        uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);
+        if (const char* be = std::getenv("SRLA_SMALL_BIN_ENTRIES"); be && small) coarse_total = std::strtoull(be, nullptr, 10);
         bcfg.cap = static_cast<uint32_t>(std::min<uint64_t>(coarse_total / bcfg.nregions, 0xFFFFFFF0ull)) & ~3u;
         bins.ensure(uint64_t(bcfg.cap) * bcfg.nregions);
         bin_count.ensure(bcfg.nregions);
+        if (overlap_on) {
+            bins_alt.ensure(uint64_t(bcfg.cap) * bcfg.nregions);
+            bin_count_alt.ensure(bcfg.nregions);
+            CK(cudaMemsetAsync(bin_count_alt.p, 0, bcfg.nregions * sizeof(uint32_t), st));
+        }
         pin_bc.ensure(2 * bcfg.nregions + 2);
         tile_prefix.ensure(2 * bcfg.nregions + 2);
         CK(cudaMemsetAsync(bin_count.p, 0, bcfg.nregions * sizeof(uint32_t), st));
@@ -765,6 +802,7 @@ struct Engine {
                 timing.split_entries += pending_entries;
             }
         }
+        open_k1_gate();
         const cudaEvent_t t_apply = timer_start();
         timing.apply_entries += pending_entries;
         if (epoch) {
@@ -817,8 +855,81 @@ struct Engine {
     }
 
     // ------------------------------------------------------------ scan
+    void open_k1_gate_final() {  // end-of-slice over without a split: gate on its end
+        if (k1_gate.load(std::memory_order_relaxed)) return;
+        cudaEventRecord(ev_k1_gate, st);
+        k1_gate.store(true, std::memory_order_release);
+    }
+    void open_k1_gate() {
+        if (!in_async_eos || k1_gate.load(std::memory_order_relaxed)) return;
+        CK(cudaEventRecord(ev_k1_gate, st));
+        k1_gate.store(true, std::memory_order_release);
+    }
+
+    // current <-> alternate region-bin set
+    void swap_bin_sets() {
+        std::swap(bins.p, bins_alt.p);
+        std::swap(bins.cap, bins_alt.cap);
+        std::swap(bin_count.p, bin_count_alt.p);
+        std::swap(bin_count.cap, bin_count_alt.cap);
+        bcfg.bins = bins.p;
+        bcfg.count = bin_count.p;
+    }
+
+    // K1 of the first chunk of a slice while the previous slice's
+    // end-of-slice runs on its worker thread: bins into the alternate set on
+    // stream sk (never marking the table directly), then joins the
+    // end-of-slice and makes that set current. Returns false (after joining)
+    // when the chunk has to be scanned the ordinary way.
+    template <typename W>
+    bool scan_k1_overlapped(const uint32_t* d_recs, uint32_t n, int vec, uint32_t& n_ev) {
+        BinCfg b2 = bcfg;
+        b2.bins = bins_alt.p;
+        b2.count = bin_count_alt.p;
+        b2.no_direct = 1;
+        b2.overflow = ctr_k1.p + 1;
+        const uint64_t add = uint64_t(n) * cfg.rows;
+        if (add / bcfg.nregions * 13 / 10 + 8192 > bcfg.cap) {
+            join_eos();
+            return false;
+        }
+        // the alternate set was zeroed, and the stamps reset, before the last scan ended
+        CK(cudaStreamWaitEvent(sk, ev_scan_done, 0));
+        if (!std::getenv("SRLA_K1_EARLY")) {
+            while (!k1_gate.load(std::memory_order_acquire)) std::this_thread::yield();
+            CK(cudaStreamWaitEvent(sk, ev_k1_gate, 0));
+        }
+        CK(cudaMemsetAsync(ctr_k1.p, 0, 4 * sizeof(uint32_t), sk));
+        CK(cudaEventRecord(t_scan0, sk));
+        const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
+        k_scan_bin<W><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, sk>>>(
+            d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(t_scan1, sk));
+        CK(cudaMemcpyAsync(pin_k1.p, ctr_k1.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, sk));
+        join_eos();  // the end-of-slice has flushed (and zeroed) the current set
+        CK(cudaStreamSynchronize(sk));
+        launched();
+        swap_bin_sets();
+        pending_entries = add;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, t_scan0, t_scan1));
+        timing.scan_kernel_ms += ms;
+        timing.scan_kernel_launches += 1;
+        timing.scan_kernel_records += n;
+        n_ev = pin_k1.p[0];
+        if (pin_k1.p[1] || n_ev > ev_cap) {  // a bin or the event list overflowed: drop and rescan
+            CK(cudaMemsetAsync(bin_count.p, 0, bcfg.nregions * sizeof(uint32_t), st));
+            pending_entries = 0;
+            return false;
+        }
+        CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
+        ++stats.overlapped_chunks;
+        return true;
+    }
+
     template <typename W, int MAXR>
-    void scan_chunk_t(const uint32_t* d_recs, uint32_t n) {
+    void scan_chunk_t(const uint32_t* d_recs, uint32_t n, bool overlap) {
         W* lin = static_cast<W*>(d_lin);
         W* rough = static_cast<W*>(d_rough);
         const int vec = (reinterpret_cast<uintptr_t>(d_recs) & 15) == 0;
@@ -837,8 +948,13 @@ struct Engine {
             tkey.ensure(t); skey.ensure(t); tval.ensure(t); sval.ensure(t); towner.ensure(t); posof.ensure(t);
         }
         uint32_t n_ev = 0;
+        bool k1_done = false;
+        if (overlap) {
+            if (use_bins && MAXR <= kBinRows && bins_alt.p) k1_done = scan_k1_overlapped<W>(d_recs, n, vec, n_ev);
+            else join_eos();
+        }
         join_maint_lin();  // K1 may stamp the linear table directly (bin overflow)
-        for (;;) {
+        while (!k1_done) {
             CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
             if (use_bins) {
                 const uint64_t add = uint64_t(n) * cfg.rows;
@@ -982,15 +1098,18 @@ struct Engine {
         trace("scan: append");
     }
 
-    void scan_chunk(const uint32_t* d_recs, uint32_t n) {
-        if (!n) return;
+    void scan_chunk(const uint32_t* d_recs, uint32_t n, bool overlap = false) {
+        if (!n) {
+            if (overlap) join_eos();
+            return;
+        }
         trace(nullptr);
         stats.chunks++;
         stats.packets += n;
         with_w([&](auto w) {
             using W = decltype(w);
-            if (cfg.rows <= 4) scan_chunk_t<W, 4>(d_recs, n);
-            else scan_chunk_t<W, 64>(d_recs, n);
+            if (cfg.rows <= 4) scan_chunk_t<W, 4>(d_recs, n, overlap);
+            else scan_chunk_t<W, 64>(d_recs, n, overlap);
         });
     }
 
@@ -1051,17 +1170,23 @@ struct Engine {
         eos = EosResult{};
         eos.pending = true;
         eos.n = due ? ncsip : 0;
+        k1_gate.store(false);
         eos_thread = std::thread([this, slice_id, want_report, out] {
             try {
                 CK(cudaSetDevice(device));
+                in_async_eos = true;
                 timed_end_slice(slice_id, want_report, out);
+                in_async_eos = false;
+                open_k1_gate_final();
                 eos.nret = ncsip;
             } catch (const Error& x) {
                 eos.code = x.code;
                 eos.msg = x.what();
+                open_k1_gate_final();
             } catch (const std::exception& x) {
                 eos.code = SRLA_E_INTERNAL;
                 eos.msg = x.what();
+                open_k1_gate_final();
             }
         });
     }
@@ -1088,16 +1213,19 @@ struct Engine {
             return;
         }
         if (on_device) {
-            join_eos();
+            // a pending asynchronous end-of-slice overlaps this batch's first K1
+            const bool overlap = overlap_on && eos_thread.joinable() && ev_cap != 0;
+            if (!overlap) join_eos();
             const uint32_t* base = reinterpret_cast<const uint32_t*>(recs);
             for (uint64_t o = 0; o < n; o += kChunk)
-                scan_chunk(base + 3 * o, static_cast<uint32_t>(std::min<uint64_t>(kChunk, n - o)));
+                scan_chunk(base + 3 * o, static_cast<uint32_t>(std::min<uint64_t>(kChunk, n - o)), overlap && o == 0);
         } else {
             scan_host(reinterpret_cast<const uint32_t*>(recs), n);
         }
         // epoch stamps: apply this batch's marks now, so end-of-slice only
         // reads histograms and the candidates' cells
         if (epoch) flush_linear();
+        CK(cudaEventRecord(ev_scan_done, st));
     }
 
     // Host records: double-buffered H2D on a copy stream overlapping the scan

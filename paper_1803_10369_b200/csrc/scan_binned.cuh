@@ -25,6 +25,8 @@ struct BinCfg {
     uint32_t cap;
     uint32_t region_shift;  // log2(words per region)
     uint32_t nib;           // linear recorders packed two per byte (nibble.cuh)
+    uint32_t no_direct;     // a bin overflow sets *overflow instead of marking the table directly
+    uint32_t* overflow;
 };
 
 constexpr int kBinThreads = 256;
@@ -228,6 +230,11 @@ __global__ void __launch_bounds__(kBinThreads, 4) k_scan_bin(const uint32_t* __r
             else ovf = true;
         }
         if (__syncthreads_or(ovf)) {  // a bin is full: mark the rest directly (marks commute)
+            if (b.no_direct) {  // the table is busy elsewhere: the caller reruns this scan
+                if (tid == 0) atomicOr(b.overflow, 1u);
+                __syncthreads();
+                continue;
+            }
             for (uint32_t idx = tid; idx < total; idx += kBinThreads) {
                 const uint32_t r = s_reg[idx];
                 if (idx < s_win[r].y) continue;

@@ -51,7 +51,7 @@ assert ENTRY_DTYPE.itemsize == 24
 class CStats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "packets", "sampled_events", "crossings", "first_crossings", "flagged", "pushed",
-        "kernel_launches", "library_launches", "chunks", "slides")]
+        "kernel_launches", "library_launches", "chunks", "slides", "overlapped_chunks")]
 
 
 class CTiming(C.Structure):

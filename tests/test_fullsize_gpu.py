@@ -125,3 +125,42 @@ def test_c2_fullsize_epoch_and_literal_paths_agree(gpu, monkeypatch):
         assert len(x) > 1000
     for (r1, l1), (r2, l2) in zip(sa, sb):
         assert np.array_equal(r1, r2) and np.array_equal(l1, l2)
+
+
+@pytest.mark.slow
+def test_c2_fullsize_overlapped_pipeline_matches_sync(gpu, monkeypatch):
+    """The bench's overlapped pipeline (srla_end_slice_async, next slice's K1
+    binned under it) against synchronous end-of-slice on the same full C2
+    slices: identical report entries and recorders."""
+    import torch
+    from paper_1803_10369_b200.srla import ENTRY_DTYPE
+    slices = _c2_slices(11)
+    cfg = S.Cfg(cols=1 << 20, **C2_SKETCH)
+    sync = _engine(cfg)
+    want = []
+    for sid, t in enumerate(slices):
+        sync.scan(t)
+        r, _ = sync.end_slice(sid, want_report=True)
+        want.append(None if r is None else r.copy())
+    want_rows = [(sync.export_row(i, 1), sync.export_row(i, 2)) for i in range(cfg.rows)]
+    del sync
+    monkeypatch.setenv("SRLA_OVERLAP", "1")
+    e = _engine(cfg)
+    bufs = [torch.empty((2 << 20) * ENTRY_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True).numpy().view(ENTRY_DTYPE)
+            for _ in range(2)]
+    got = []
+    for sid, t in enumerate(slices):
+        e.scan(t)
+        if sid:
+            n, _ = e.end_slice_wait()
+            got.append(bufs[(sid - 1) % 2][:n].copy() if sid >= cfg.window else None)
+        e.end_slice_async(sid, bufs[sid % 2])
+    n, _ = e.end_slice_wait()
+    got.append(bufs[(len(slices) - 1) % 2][:n].copy())
+    assert e.stats()["overlapped_chunks"] >= 9
+    for g, w in zip(got, want):
+        assert (g is None) == (w is None)
+        if w is not None:
+            assert g.tobytes() == w.tobytes()
+    for (r1, l1), (r2, l2) in zip(want_rows, [(e.export_row(i, 1), e.export_row(i, 2)) for i in range(cfg.rows)]):
+        assert np.array_equal(r1, r2) and np.array_equal(l1, l2)

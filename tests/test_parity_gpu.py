@@ -314,6 +314,51 @@ def test_async_end_slice_matches_sync(gpu, oracle, name, pinned):
     assert np.array_equal(e.candidates(), pipe.candidates())
 
 
+@pytest.mark.parametrize("epoch", ["0", "1"])
+@pytest.mark.parametrize("name", ["contended", "drift_evict", "c1_shape"])
+def test_async_end_slice_overlaps_next_device_scan(gpu, oracle, name, epoch, monkeypatch):
+    """srla_end_slice_async + the next slice's DEVICE scan: K1 bins into the
+    second bin set while the end-of-slice runs (binned marks forced on), and
+    the reports, candidate list and recorders stay the reference's."""
+    import torch
+    from oracle.pyoracle import SeaConfig as OCfg
+    from paper_1803_10369_b200.srla import ENTRY_DTYPE
+    monkeypatch.setenv("SRLA_FORCE_BINS", "1")
+    monkeypatch.setenv("SRLA_EPOCH", epoch)
+    monkeypatch.setenv("SRLA_OVERLAP", "1")
+    monkeypatch.setenv("SRLA_SMALL_BIN_ENTRIES", str(1 << 20))  # room for a whole slice per bin set
+    cfg, _ = S.SCENARIOS[name]
+    slices = GF.scenario_slices(name, oracle)
+    pipe = oracle.pipeline(OCfg(**cfg.as_dict()))
+    want = [pipe.process_slice(s, r, True) for s, r in enumerate(slices)]
+    e = engine(cfg)
+    bufs = [np.zeros(200000, ENTRY_DTYPE) for _ in range(2)]
+    dev = [torch.from_numpy(r.astype(np.int32)).cuda() for r in slices]
+    torch.cuda.synchronize()
+    got = []
+    for s in range(len(slices)):
+        e.scan(dev[s])
+        if s:
+            n, _ = e.end_slice_wait()
+            got.append(bufs[(s - 1) % 2][:n].copy() if s >= cfg.window else None)
+        e.end_slice_async(s, bufs[s % 2])
+    n, _ = e.end_slice_wait()
+    got.append(bufs[(len(slices) - 1) % 2][:n].copy() if len(slices) >= cfg.window else None)
+    assert e.stats()["overlapped_chunks"] > 0
+    for s, (g, w) in enumerate(zip(got, want)):
+        if w is None:
+            assert g is None or len(g) == 0
+            continue
+        assert np.array_equal(g["host"], w["host"]), s
+        assert np.array_equal(g["union_weight"], w["weight"]), s
+        assert np.array_equal(g["estimate"].view(np.uint64)[w["has_estimate"] == 1],
+                              w["estimate"].view(np.uint64)[w["has_estimate"] == 1]), s
+    assert np.array_equal(e.candidates(), pipe.candidates())
+    for i in range(cfg.rows):
+        for kind in (1, 2):
+            assert np.array_equal(e.export_row(i, kind), pipe.sketch.export_row(i, kind)), (i, kind)
+
+
 @pytest.mark.parametrize("bits,window", [(4, 5), (7, 100), (3, 7)])
 def test_epoch_stamps_survive_counter_wrap(gpu, oracle, bits, window, monkeypatch):
     """600 slides (the u8 epoch counter wraps twice): hosts fall silent for

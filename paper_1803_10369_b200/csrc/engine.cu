@@ -207,8 +207,6 @@ struct Engine {
     DevBuf<unsigned long long> hist;  // rows x 256
     PinBuf<unsigned long long> pin_hist;
     uint64_t sweep_pos = 0;
-    // slices with at most this many marks are stamped in place (epoch.cuh)
-    uint32_t sparse_max = 0;
     EpochCfg ecfg() const { return EpochCfg{epoch ? 1u : 0u, cur_epoch, hist.p, lin_words}; }
     PinBuf<uint32_t> pin_bc;
     uint64_t pending_entries = 0;
@@ -290,7 +288,7 @@ struct Engine {
         *out = timing;
         out->alloc_ms = g_alloc_ms;
         out->allocs = g_allocs;
-        if (pin_streamed.p) out->apply_stream_bytes = 2ull * pin_streamed.p[0] * lin_bytes(1ull << fcfg.shift);
+        if (pin_streamed.p) out->apply_stream_bytes = 2ull * pin_streamed.p[0];
     }
     void timing_clear() {
         resolve_timers(true);
@@ -685,8 +683,6 @@ struct Engine {
         if (lin_words < (1ull << fcfg.shift)) return;  // a slice may span at most two rows
         epoch = true;
         cur_epoch = 0;
-        sparse_max = (1u << fcfg.shift) / 128;
-        if (const char* sm = std::getenv("SRLA_SPARSE_MAX")) sparse_max = static_cast<uint32_t>(std::strtoul(sm, nullptr, 10));
         hist.ensure(uint64_t(cfg.rows) * 256);
         pin_hist.ensure(uint64_t(cfg.rows) * 256);
         CK(cudaMemsetAsync(hist.p, 0, uint64_t(cfg.rows) * 256 * sizeof(unsigned long long), st));
@@ -808,8 +804,7 @@ struct Engine {
         if (epoch) {
             if (pending_entries) {
                 k_slice_stamp<<<std::min<uint32_t>(fcfg.nfine, sms * 3), 256, 2u << fcfg.shift, st>>>(
-                    static_cast<uint8_t*>(d_lin), total, lin_words, fcfg, 0, bulk_ok ? 1 : 0, cur_epoch, cfg.window, hist.p,
-                    sparse_max);
+                    static_cast<uint8_t*>(d_lin), total, lin_words, fcfg, 0, bulk_ok ? 1 : 0, cur_epoch, cfg.window, hist.p);
                 check_launch();
                 launched();
                 timer_stop(t_apply, kTimeApply);

@@ -36,119 +36,138 @@ __device__ __forceinline__ uint32_t stamp_byte_shared(uint8_t* base, uint32_t of
     return (old >> sh) & 0xFFu;
 }
 
-// Apply pending marks of slices [f_begin, nfine) as epoch stamps (only slices
-// with marks; bulk-loaded, double-buffered like k_slice_apply_bulk) and
-// account the transitions in the per-row histograms.
+// Apply pending marks of slices [f_begin, nfine) as epoch stamps and account
+// the transitions in the per-row histograms. Only the touched 1 KB pieces of
+// a slice move (a stamp pass leaves every other byte as it is): the block ORs
+// its marks into a piece mask, bulk-loads those pieces into shared memory,
+// stamps them there and bulk-stores them back; the next slice's pieces load
+// while the current one is stamped. A tail slice (not a whole 16-byte
+// multiple) goes through shared memory with plain loads.
 __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, uint64_t total_words,
                                                      uint64_t row_words, FineCfg f, uint32_t f_begin, int bulk,
-                                                     uint32_t cur, uint32_t k, unsigned long long* __restrict__ hist,
-                                                     uint32_t sparse_max) {
+                                                     uint32_t cur, uint32_t k, unsigned long long* __restrict__ hist) {
     extern __shared__ __align__(128) uint8_t s_raw[];
     __shared__ __align__(8) uint64_t s_bar[2];
-    __shared__ uint32_t s_hist[2][256];
-    const uint32_t tid = threadIdx.x;
+    // per row of the slice (a slice spans at most two rows): net transitions
+    // by age (cur - stamp) in [0, k): age 0 gains, older stamps in the window lose
+    __shared__ uint32_t s_hist[2][128];
+    __shared__ uint32_t s_mask[2];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
     const uint32_t slice_bytes = 1u << f.shift;
+    const uint32_t cs = f.shift > 15 ? f.shift - 5 : min(10u, f.shift);  // piece = 2^cs bytes, <= 32 per slice
     uint8_t* buf[2] = {s_raw, s_raw + slice_bytes};
     auto next_slice = [&](uint32_t from) -> uint32_t {
         for (uint32_t fb = from; fb < f.nfine; fb += gridDim.x)
             if (f.count[fb] != 0) return fb;
         return f.nfine;
     };
-    // sparse slices (few marks for their size) are stamped in place with a
-    // CAS per mark: only the touched sectors move, instead of the slice twice
-    auto dense = [&](uint32_t fb) { return min(f.count[fb], f.cap) > sparse_max; };
+    auto slice_len = [&](uint32_t fb) {
+        return static_cast<uint32_t>(min(static_cast<uint64_t>(slice_bytes), total_words - (static_cast<uint64_t>(fb) << f.shift)));
+    };
+    auto marks = [&](uint32_t fb) { return f.bins + static_cast<uint64_t>(fb) * f.cap; };
+    // pieces of slice fb holding marks (block-uniform call)
+    auto piece_mask = [&](uint32_t fb, uint32_t slot) -> uint32_t {
+        if (tid == 0) s_mask[slot] = 0;
+        __syncthreads();
+        const uint32_t n = min(f.count[fb], f.cap);
+        const uint16_t* e = marks(fb);
+        uint32_t m = 0;
+        for (uint32_t q = tid; q < n; q += blockDim.x) m |= 1u << (static_cast<uint32_t>(e[q]) >> cs);
+        m = __reduce_or_sync(0xFFFFFFFFu, m);
+        if (lane == 0 && m) atomicOr(&s_mask[slot], m);
+        __syncthreads();
+        return s_mask[slot];
+    };
+    auto issue = [&](uint32_t fb, uint32_t b, uint32_t mask) -> bool {
+        if (!bulk || slice_len(fb) != slice_bytes) return false;
+        if (tid == 0) {
+            uint8_t* g = lin + (static_cast<uint64_t>(fb) << f.shift);
+            mbar_expect_tx(&s_bar[b], static_cast<uint32_t>(__popc(mask)) << cs);
+            for (uint32_t m = mask; m; m &= m - 1) {
+                const uint32_t c = __ffs(m) - 1;
+                bulk_load(buf[b] + (c << cs), g + (static_cast<uint64_t>(c) << cs), 1u << cs, &s_bar[b]);
+            }
+        }
+        return true;
+    };
     if (tid == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
     }
     __syncthreads();
-    uint32_t cur_fb = next_slice(f_begin + blockIdx.x);
-    auto slice_len = [&](uint32_t fb) {
-        return static_cast<uint32_t>(min(static_cast<uint64_t>(slice_bytes), total_words - (static_cast<uint64_t>(fb) << f.shift)));
-    };
-    auto load = [&](uint32_t fb, uint32_t b) {
-        // bulk path: whole 16-byte multiple slices; plain path for the tail slice
-        const uint32_t len = slice_len(fb);
-        uint8_t* g = lin + (static_cast<uint64_t>(fb) << f.shift);
-        if (!dense(fb)) return false;
-        if (bulk && (len & 15) == 0) {
-            if (tid == 0) {
-                mbar_expect_tx(&s_bar[b], len);
-                bulk_load(buf[b], g, len, &s_bar[b]);
-            }
-            return true;
-        }
-        return false;
-    };
     uint32_t phase[2] = {0u, 0u};  // parity of each barrier's next completion
-    bool bulk_cur = cur_fb < f.nfine ? load(cur_fb, 0) : false;
+    uint32_t cur_fb = next_slice(f_begin + blockIdx.x);
+    uint32_t mcur = cur_fb < f.nfine ? piece_mask(cur_fb, 0) : 0u;
+    bool bulk_cur = cur_fb < f.nfine && issue(cur_fb, 0, mcur);
     for (uint32_t i = 0; cur_fb < f.nfine; ++i) {
         const uint32_t b = i & 1u;
         const uint32_t nxt = next_slice(cur_fb + gridDim.x);
+        uint32_t mnxt = 0;
         bool bulk_nxt = false;
         if (nxt < f.nfine) {
-            if (tid == 0) bulk_wait_read_all();
-            bulk_nxt = load(nxt, b ^ 1u);
+            mnxt = piece_mask(nxt, b ^ 1u);
+            if (tid == 0) bulk_wait_read_all();  // the stores out of buf[b ^ 1] have left shared memory
+            bulk_nxt = issue(nxt, b ^ 1u, mnxt);
         }
         const uint32_t len = slice_len(cur_fb);
         uint8_t* g = lin + (static_cast<uint64_t>(cur_fb) << f.shift);
-        const bool in_smem = dense(cur_fb);
-        if (in_smem && tid == 0) atomicAdd(f.streamed, 1ull);
-        for (uint32_t q = tid; q < 512; q += blockDim.x) (&s_hist[0][0])[q] = 0;
+        for (uint32_t q = tid; q < 2 * k; q += blockDim.x) s_hist[q / k][q % k] = 0;
         if (bulk_cur) {
             mbar_wait(&s_bar[b], phase[b]);
             phase[b] ^= 1u;
-        } else if (in_smem) {
+        } else {
             for (uint32_t q = tid; q < len; q += blockDim.x) buf[b][q] = g[q];
         }
         __syncthreads();
+        if (tid == 0) atomicAdd(f.streamed, bulk_cur ? static_cast<unsigned long long>(__popc(mcur)) << cs : len);
         const uint32_t n = min(f.count[cur_fb], f.cap);
-        const uint16_t* e = f.bins + static_cast<uint64_t>(cur_fb) * f.cap;
+        const uint16_t* e = marks(cur_fb);
         const uint64_t w0 = static_cast<uint64_t>(cur_fb) << f.shift;
         const uint64_t row_a = w0 / row_words;
         const uint32_t split = static_cast<uint32_t>(min(static_cast<uint64_t>(len), (row_a + 1) * row_words - w0));
         // transitions onto `cur` are counted per warp (one shared atomic per
         // warp and row); decrements only matter for stamps inside the window
         // (stale bins are zeroed when the counter returns to them)
-        const uint32_t lane = tid & 31u;
         for (uint32_t q0 = 0; q0 < n; q0 += blockDim.x) {
             const uint32_t q = q0 + tid;
             uint32_t old = cur, h = 0;
             if (q < n) {
                 const uint32_t off = e[q];
-                // one block owns a slice: the CAS only races with this block
-                old = in_smem ? stamp_byte_shared(buf[b], off, cur) : stamp_byte_global(g, off, cur);
+                old = stamp_byte_shared(buf[b], off, cur);
                 h = off < split ? 0u : 1u;
-                if (old != cur && ((cur - old) & 0xFFu) < k) atomicSub(&s_hist[h][old], 1u);
+                const uint32_t age = (cur - old) & 0xFFu;
+                if (old != cur && age < k) atomicSub(&s_hist[h][age], 1u);
             }
             const unsigned moved = __ballot_sync(0xFFFFFFFFu, old != cur);
             const unsigned row_b = __ballot_sync(0xFFFFFFFFu, h == 1u);
             if (lane == 0) {
                 const uint32_t c1 = __popc(moved & row_b), c0 = __popc(moved) - c1;
-                if (c0) atomicAdd(&s_hist[0][cur], c0);
-                if (c1) atomicAdd(&s_hist[1][cur], c1);
+                if (c0) atomicAdd(&s_hist[0][0], c0);
+                if (c1) atomicAdd(&s_hist[1][0], c1);
             }
         }
         __syncthreads();
-        for (uint32_t q = tid; q < 512; q += blockDim.x) {
-            const uint32_t v = (&s_hist[0][0])[q];
-            if (v) {
-                const uint32_t h = q >> 8;
-                atomicAdd(hist + (row_a + h) * 256 + (q & 255u),
+        for (uint32_t q = tid; q < 2 * k; q += blockDim.x) {
+            const uint32_t h = q / k, age = q % k;
+            const uint32_t v = s_hist[h][age];
+            if (v)
+                atomicAdd(hist + (row_a + h) * 256 + ((cur - age) & 0xFFu),
                           static_cast<unsigned long long>(static_cast<long long>(static_cast<int32_t>(v))));
-            }
         }
         if (bulk_cur) {
             fence_proxy_async_smem();
             __syncthreads();
-            if (tid == 0) bulk_store(g, buf[b], len);
-        } else if (in_smem) {
-            for (uint32_t q = tid; q < len; q += blockDim.x) g[q] = buf[b][q];
-            __syncthreads();
+            if (tid == 0)
+                for (uint32_t m = mcur; m; m &= m - 1) {
+                    const uint32_t c = __ffs(m) - 1;
+                    bulk_store(g + (static_cast<uint64_t>(c) << cs), buf[b] + (c << cs), 1u << cs);
+                }
         } else {
+            for (uint32_t q = tid; q < len; q += blockDim.x) g[q] = buf[b][q];
             __syncthreads();
         }
         cur_fb = nxt;
+        mcur = mnxt;
         bulk_cur = bulk_nxt;
     }
     if (tid == 0) bulk_wait_all();

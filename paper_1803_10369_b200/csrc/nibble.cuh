@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) k_slice_apply_nib(uint8_t* __restrict__ l
             bulk_load(buf[b ^ 1u], gaddr(nxt), slice_bytes, &s_bar[b ^ 1u]);
         }
         mbar_wait(&s_bar[b], (i >> 1) & 1u);
-        if (tid == 0) atomicAdd(f.streamed, 1ull);
+        if (tid == 0) atomicAdd(f.streamed, static_cast<unsigned long long>(slice_bytes));
         unsigned int* s32 = reinterpret_cast<unsigned int*>(buf[b]);
         const uint32_t n = min(f.count[cur], f.cap);
         const uint16_t* e = f.bins + static_cast<uint64_t>(cur) * f.cap;

@@ -328,7 +328,7 @@ struct FineCfg {
     uint32_t shift;       // log2(words per fine slice)
     uint32_t per_region;  // fine slices per coarse region = 2^(region_shift - shift)
     uint32_t nfine;       // total fine slices covering the table
-    unsigned long long* streamed;  // whole slices read + written by the apply kernels (statistics)
+    unsigned long long* streamed;  // table bytes read (= written) by the apply kernels (statistics)
     uint32_t nib;                  // linear recorders packed two per byte (nibble.cuh)
 };
 
@@ -481,9 +481,9 @@ __global__ void __launch_bounds__(256) k_slice_apply(W* __restrict__ lin, uint64
     for (uint32_t fb = f_begin + blockIdx.x; fb < f.nfine; fb += gridDim.x) {
         const uint32_t n = min(f.count[fb], f.cap);
         if (mode == 0 && n == 0) continue;
-        if (tid == 0) atomicAdd(f.streamed, 1ull);
         const uint64_t w0 = static_cast<uint64_t>(fb) << f.shift;
         const uint32_t nw = static_cast<uint32_t>(min(static_cast<uint64_t>(1u << f.shift), total_words - w0));
+        if (tid == 0) atomicAdd(f.streamed, static_cast<unsigned long long>(nw) * sizeof(W));
         const uint32_t nv = vec ? static_cast<uint32_t>((static_cast<uint64_t>(nw) * sizeof(W)) / 16) : 0u;
         const uint32_t tail0 = nv * 16 / sizeof(W);
         uint4* g = reinterpret_cast<uint4*>(lin + w0);
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(256) k_slice_apply_bulk(W* __restrict__ lin, u
             bulk_load(buf[b ^ 1u], lin + (static_cast<uint64_t>(nxt) << f.shift), slice_bytes, &s_bar[b ^ 1u]);
         }
         mbar_wait(&s_bar[b], (i >> 1) & 1u);
-        if (tid == 0) atomicAdd(f.streamed, 1ull);
+        if (tid == 0) atomicAdd(f.streamed, static_cast<unsigned long long>(slice_bytes));
         W* sw = reinterpret_cast<W*>(buf[b]);
         const uint32_t n = min(f.count[cur], f.cap);
         const uint16_t* e = f.bins + static_cast<uint64_t>(cur) * f.cap;

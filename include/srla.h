@@ -32,7 +32,8 @@ typedef enum srla_status {
     SRLA_E_RANGE = 2,    /* row index out of range (std::out_of_range) */
     SRLA_E_CAPACITY = 3, /* output buffer too small; *n_out holds the size needed */
     SRLA_E_CUDA = 4,     /* CUDA runtime / device failure */
-    SRLA_E_INTERNAL = 5
+    SRLA_E_INTERNAL = 5,
+    SRLA_E_INPUT = 6     /* malformed trace input (sspread::InputError) */
 } srla_status;
 
 /* sspread::SeaConfig (sea.hpp:33-52), field for field. */
@@ -266,6 +267,39 @@ srla_status srla_partition_records(const srla_record* d_in, uint64_t n, uint64_t
                                    uint32_t part, srla_record* d_out, uint64_t* n_out, void* stream);
 /* Host-side owner of one address (same function). */
 uint32_t srla_owner_of(uint64_t seed, uint32_t aip, uint32_t nparts);
+
+/* Device memory for callers without CUDA headers (the drop-in C++ API). */
+srla_status srla_device_alloc(int device, uint64_t bytes, void** out);
+srla_status srla_device_free(int device, void* p);
+srla_status srla_copy_to_device(int device, void* dst, const void* src, uint64_t bytes);
+
+/* ---- ingest front end on the device (trace.hpp) ----
+ * All buffers are device memory; `stream` is a cudaStream_t (NULL: default). */
+
+/* for_each_record's binary branch (trace.hpp:109-170, replaces
+ * read_trace/for_each_record for SRLT files): `d_bytes` is the whole file
+ * ("SRLT", version 1, packed little-endian u32 ts/src/dst). Bad magic or
+ * version, a truncated last record and a timestamp regression return
+ * SRLA_E_INPUT with the reference's message; *n_out = the records before the
+ * failure, as the reference delivers them. d_out has room for
+ * (nbytes - 5) / 12 records. */
+srla_status srla_parse_srlt(const void* d_bytes, uint64_t nbytes, srla_record* d_out, uint64_t* n_out, void* stream);
+
+/* orient_record over a batch (trace.hpp:223-238, OrientStats :212-221): src in
+ * the prefix and dst outside -> kept; the reverse -> flipped (src <-> dst);
+ * both / neither -> dropped and counted. Output in input order. */
+typedef struct srla_orient_stats {
+    uint64_t kept, flipped, dropped_both, dropped_neither;
+} srla_orient_stats;
+srla_status srla_orient_records(const srla_record* d_in, uint64_t n, uint32_t prefix_addr, uint32_t prefix_bits,
+                                srla_record* d_out, uint64_t* n_out, srla_orient_stats* stats, void* stream);
+
+/* SlicePartitioner (trace.hpp:243-281) over an ordered batch: the origin is
+ * the first record's ts; offsets[s] (host memory, n_slices + 1 entries) is the
+ * first record of slice s, empty slices included. offsets == NULL queries
+ * *n_slices. A timestamp regression returns SRLA_E_INPUT. */
+srla_status srla_slice_bounds(const srla_record* d_recs, uint64_t n, uint32_t slice_seconds, uint64_t* offsets,
+                              uint64_t cap, uint64_t* n_slices, void* stream);
 
 #ifdef __cplusplus
 }

@@ -13,6 +13,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <fstream>
 #include <functional>
 #include <span>
 #include <stdexcept>
@@ -84,7 +85,16 @@ class DetectPipeline {
     double total_scan_ms() const noexcept { return total_scan_ms_; }
     double total_estimate_ms() const noexcept { return total_estimate_ms_; }
 
-    void run(const std::string& trace_path, const ReportSink& sink) {  // pipeline.hpp:96-106
+    // pipeline.hpp:96-106. Binary (SRLT) traces take the device front end:
+    // the file crosses to HBM once; parsing, orientation and the slice
+    // boundaries run on the GPU (srla_parse_srlt / srla_orient_records /
+    // srla_slice_bounds) and every slice is scanned where it lies. CSV traces
+    // take the host path.
+    void run(const std::string& trace_path, const ReportSink& sink) {
+        if (sniff_trace_format(trace_path) == TraceFormat::binary) {
+            run_device(trace_path, sink);
+            return;
+        }
         SlicePartitioner partitioner(cfg_.slice_seconds);
         const auto on_slice = [&](uint64_t id, std::vector<TraceRecord>&& records) {
             process_slice(id, records, sink);
@@ -117,6 +127,55 @@ class DetectPipeline {
     }
 
   private:
+    void run_device(const std::string& path, const ReportSink& sink) {
+        std::ifstream in(path, std::ios::binary | std::ios::ate);
+        if (!in) throw InputError("cannot open trace: " + path);
+        const uint64_t nbytes = static_cast<uint64_t>(in.tellg());
+        std::vector<char> bytes(nbytes);
+        in.seekg(0);
+        in.read(bytes.data(), static_cast<std::streamsize>(nbytes));
+        const int dev = cfg_.device;
+        struct DevMem {
+            int dev;
+            void* p = nullptr;
+            ~DevMem() { if (p) srla_device_free(dev, p); }
+        } d_bytes{dev}, d_raw{dev}, d_recs{dev};
+        const uint64_t cap = nbytes >= 5 ? (nbytes - 5) / 12 + 1 : 1;
+        detail::check(srla_device_alloc(dev, std::max<uint64_t>(nbytes, 1), &d_bytes.p), "srla_device_alloc");
+        detail::check(srla_device_alloc(dev, cap * sizeof(srla_record), &d_raw.p), "srla_device_alloc");
+        detail::check(srla_device_alloc(dev, cap * sizeof(srla_record), &d_recs.p), "srla_device_alloc");
+        detail::check(srla_copy_to_device(dev, d_bytes.p, bytes.data(), nbytes), "srla_copy_to_device");
+        uint64_t n = 0;
+        const srla_status ps = srla_parse_srlt(d_bytes.p, nbytes, static_cast<srla_record*>(d_raw.p), &n, nullptr);
+        std::string input_error;
+        if (ps == SRLA_E_INPUT) input_error = std::string(srla_last_error()) + " in " + path;
+        else detail::check(ps, "srla_parse_srlt");
+        uint64_t m = 0;
+        srla_orient_stats os{};
+        detail::check(srla_orient_records(static_cast<const srla_record*>(d_raw.p), n, cfg_.a_network.addr,
+                                          cfg_.a_network.bits, static_cast<srla_record*>(d_recs.p), &m, &os, nullptr),
+                      "srla_orient_records");
+        stats_.kept += os.kept;
+        stats_.flipped += os.flipped;
+        stats_.dropped_both += os.dropped_both;
+        stats_.dropped_neither += os.dropped_neither;
+        uint64_t ns = 0;
+        detail::check(srla_slice_bounds(static_cast<const srla_record*>(d_recs.p), m, cfg_.slice_seconds, nullptr, 0,
+                                        &ns, nullptr),
+                      "srla_slice_bounds");
+        std::vector<uint64_t> off(ns + 1);
+        if (ns)
+            detail::check(srla_slice_bounds(static_cast<const srla_record*>(d_recs.p), m, cfg_.slice_seconds,
+                                            off.data(), off.size(), &ns, nullptr),
+                          "srla_slice_bounds");
+        // a failed read leaves the last, unfinished slice unprocessed (the
+        // partitioner is never finished), as for_each_record's throw does
+        const uint64_t done = input_error.empty() ? ns : (ns ? ns - 1 : 0);
+        const auto* d = static_cast<const TraceRecord*>(d_recs.p);
+        for (uint64_t sid = 0; sid < done; ++sid) process_slice_device(sid, d + off[sid], off[sid + 1] - off[sid], sink);
+        if (!input_error.empty()) throw InputError(input_error);
+    }
+
     void process(uint64_t slice_id, const TraceRecord* recs, uint64_t n, int on_device, const ReportSink& sink) {
         sea_.pipeline_mode();
         sea_.to_device();

@@ -144,6 +144,9 @@ class Checker:
             "pipeline_scan_ms": (dbl, [vp]),
             "pipeline_estimate_ms": (dbl, [vp]),
             "generate": (u64, [C.POINTER(OrcSpec), vp, C.c_char_p, C.c_size_t]),
+            "orient": (u64, [vp, u64, u32, u32, vp, vp]),
+            "slice_bounds": (u64, [vp, u64, u32, vp]),
+            "parse_srlt": (u64, [vp, u64, vp, C.POINTER(i32), C.POINTER(u64)]),
         }
         for name, (res, args) in sigs.items():
             fn = self.f(name)
@@ -160,6 +163,33 @@ class Checker:
     def linear_estimate(self, w, slots):
         out = C.c_double()
         return out.value if self.f("linear_estimate")(w, slots, C.byref(out)) else None
+
+    # ---- ingest front end (trace.hpp)
+    def orient(self, recs, prefix_addr, prefix_bits):
+        """orient_record over a batch -> (records kept/flipped in order, [kept, flipped, both, neither])."""
+        recs = np.ascontiguousarray(recs, dtype=np.uint32).reshape(-1, 3)
+        out = np.empty((max(1, len(recs)), 3), np.uint32)
+        st = np.zeros(4, np.uint64)
+        m = self.f("orient")(_ptr(recs), len(recs), prefix_addr, prefix_bits, _ptr(out), _ptr(st))
+        return out[:m].copy(), st
+
+    def slice_bounds(self, recs, slice_seconds):
+        """SlicePartitioner -> offsets (nslices + 1) of an ordered batch."""
+        recs = np.ascontiguousarray(recs, dtype=np.uint32).reshape(-1, 3)
+        ns = self.f("slice_bounds")(_ptr(recs), len(recs), slice_seconds, None)
+        off = np.zeros(ns + 1, np.uint64)
+        if ns:
+            self.f("slice_bounds")(_ptr(recs), len(recs), slice_seconds, _ptr(off))
+        return off
+
+    def parse_srlt(self, data: bytes):
+        """SRLT v1 file bytes -> (records, err, err_index)."""
+        buf = np.frombuffer(data, np.uint8)
+        err, idx = C.c_int(), C.c_uint64()
+        n = self.f("parse_srlt")(_ptr(buf), len(buf), None, C.byref(err), C.byref(idx))
+        out = np.empty((max(1, n), 3), np.uint32)
+        n = self.f("parse_srlt")(_ptr(buf), len(buf), _ptr(out), C.byref(err), C.byref(idx))
+        return out[:n].copy(), err.value, idx.value
 
     def config(self, cfg: SeaConfig) -> OrcConfig:
         fr = self.super_test_ratio if cfg.fill_ratio is None else cfg.fill_ratio

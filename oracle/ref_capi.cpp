@@ -7,6 +7,8 @@
 // reference's public API with the same entry points as srla_oracle.h
 // (prefix `ref_` instead of `orc_`).
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -16,6 +18,7 @@
 #include "sspread/generator.hpp"
 #include "sspread/pipeline.hpp"
 #include "sspread/sea.hpp"
+#include "sspread/trace.hpp"
 
 #include "srla_oracle.h"  // shared struct layouts (orc_config, orc_spec, kinds)
 
@@ -301,6 +304,69 @@ uint64_t ref_generate(const orc_spec* s, uint32_t* out, char* err, size_t errlen
         set_err(err, errlen, e.what());
         return UINT64_MAX;
     }
+}
+
+// ---- ingest front end: the reference's own orient_record / SlicePartitioner / for_each_record
+uint64_t ref_orient(const uint32_t* recs, uint64_t n, uint32_t prefix_addr, uint32_t prefix_bits, uint32_t* out,
+                    uint64_t* stats) {
+    const CidrPrefix net{prefix_addr & CidrPrefix::mask_of(prefix_bits), prefix_bits};
+    OrientStats st;
+    uint64_t m = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (const auto o = orient_record(TraceRecord{recs[3 * i], recs[3 * i + 1], recs[3 * i + 2]}, net, st)) {
+            out[3 * m] = o->ts;
+            out[3 * m + 1] = o->src;
+            out[3 * m + 2] = o->dst;
+            ++m;
+        }
+    }
+    stats[0] = st.kept;
+    stats[1] = st.flipped;
+    stats[2] = st.dropped_both;
+    stats[3] = st.dropped_neither;
+    return m;
+}
+
+uint64_t ref_slice_bounds(const uint32_t* recs, uint64_t n, uint32_t slice_seconds, uint64_t* offsets) {
+    SlicePartitioner part(slice_seconds);
+    uint64_t slices = 0, at = 0;
+    const auto sink = [&](uint64_t id, std::vector<TraceRecord>&& batch) {
+        if (offsets) offsets[id] = at;
+        at += batch.size();
+        slices = id + 1;
+    };
+    for (uint64_t i = 0; i < n; ++i) part.push(TraceRecord{recs[3 * i], recs[3 * i + 1], recs[3 * i + 2]}, sink);
+    part.finish(sink);
+    if (offsets && slices) offsets[slices] = at;
+    return slices;
+}
+
+uint64_t ref_parse_srlt(const uint8_t* bytes, uint64_t nbytes, uint32_t* out, int* err, uint64_t* err_index) {
+    *err = 0;
+    *err_index = 0;
+    char path[] = "/tmp/srla_ref_srlt_XXXXXX";
+    const int fd = mkstemp(path);
+    if (fd < 0) throw std::runtime_error("mkstemp");
+    FILE* f = fdopen(fd, "wb");
+    fwrite(bytes, 1, nbytes, f);
+    fclose(f);
+    uint64_t n = 0;
+    try {
+        for_each_record(path, TraceFormat::binary, [&](const TraceRecord& r) {
+            if (out) {
+                out[3 * n] = r.ts;
+                out[3 * n + 1] = r.src;
+                out[3 * n + 2] = r.dst;
+            }
+            ++n;
+        });
+    } catch (const InputError& e) {
+        const std::string m = e.what();
+        *err = m.find("truncated") != std::string::npos ? 2 : m.find("regression") != std::string::npos ? 3 : 1;
+        *err_index = n;
+    }
+    std::remove(path);
+    return n;
 }
 
 }  // extern "C"

@@ -652,3 +652,86 @@ uint64_t orc_generate(const orc_spec* spec, uint32_t* out, char* err, size_t err
     free(cdf);
     return n;
 }
+
+/* ------------------------------------------------------------------ ingest (trace.hpp) */
+
+/* CidrPrefix::mask_of (trace.hpp:73-75) */
+static uint32_t cidr_mask(uint32_t bits) { return bits == 0 ? 0u : 0xFFFFFFFFu << (32 - bits); }
+
+/* orient_record (trace.hpp:223-238) applied to a batch */
+uint64_t orc_orient(const uint32_t* recs, uint64_t n, uint32_t prefix_addr, uint32_t prefix_bits, uint32_t* out,
+                    uint64_t* stats) {
+    const uint32_t mask = cidr_mask(prefix_bits), addr = prefix_addr & mask; /* CidrPrefix::parse */
+    uint64_t m = 0;
+    stats[0] = stats[1] = stats[2] = stats[3] = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t ts = recs[3 * i], src = recs[3 * i + 1], dst = recs[3 * i + 2];
+        const int src_in = (src & mask) == addr, dst_in = (dst & mask) == addr; /* contains, :77 */
+        if (src_in && !dst_in) {
+            ++stats[0];
+            out[3 * m] = ts; out[3 * m + 1] = src; out[3 * m + 2] = dst;
+            ++m;
+        } else if (!src_in && dst_in) {
+            ++stats[1];
+            out[3 * m] = ts; out[3 * m + 1] = dst; out[3 * m + 2] = src;
+            ++m;
+        } else if (src_in) {
+            ++stats[2];
+        } else {
+            ++stats[3];
+        }
+    }
+    return m;
+}
+
+/* SlicePartitioner::push / finish (trace.hpp:248-271): id = (ts - origin) /
+   seconds with the first record's ts as origin; every id up to the last is a
+   slice, empty or not */
+uint64_t orc_slice_bounds(const uint32_t* recs, uint64_t n, uint32_t slice_seconds, uint64_t* offsets) {
+    if (n == 0) return 0;
+    const uint64_t origin = recs[0];
+    uint64_t current = 0;
+    if (offsets) offsets[0] = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t id = ((uint64_t)recs[3 * i] - origin) / slice_seconds;
+        while (current < id) {
+            ++current;
+            if (offsets) offsets[current] = i;
+        }
+    }
+    if (offsets) offsets[current + 1] = n;
+    return current + 1;
+}
+
+/* for_each_record, binary branch (trace.hpp:148-170): magic "SRLT", version 1,
+   packed little-endian (u32 ts, u32 src, u32 dst), non-decreasing ts */
+uint64_t orc_parse_srlt(const uint8_t* bytes, uint64_t nbytes, uint32_t* out, int* err, uint64_t* err_index) {
+    *err = 0;
+    *err_index = 0;
+    if (nbytes < 5 || memcmp(bytes, "SRLT", 4) != 0 || bytes[4] != 1) {
+        *err = 1;
+        return 0;
+    }
+    const uint8_t* p = bytes + 5;
+    const uint64_t body = nbytes - 5, n = body / 12;
+    uint32_t last = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint32_t v[3];
+        for (int k = 0; k < 3; ++k) {
+            const uint8_t* q = p + 12 * i + 4 * k;
+            v[k] = (uint32_t)q[0] | (uint32_t)q[1] << 8 | (uint32_t)q[2] << 16 | (uint32_t)q[3] << 24;
+        }
+        if (i > 0 && v[0] < last) { /* check_order, trace.hpp:113-119 */
+            *err = 3;
+            *err_index = i;
+            return i;
+        }
+        last = v[0];
+        if (out) { out[3 * i] = v[0]; out[3 * i + 1] = v[1]; out[3 * i + 2] = v[2]; }
+    }
+    if (body % 12) {
+        *err = 2;
+        *err_index = n;
+    }
+    return n;
+}

@@ -131,6 +131,24 @@ double orc_pipeline_estimate_ms(void* p);
  * triples into out when out != NULL (capacity must be >= the count). */
 uint64_t orc_generate(const orc_spec* spec, uint32_t* out, char* err, size_t errlen);
 
+/* Ingest front end (trace.hpp), records as (ts, src, dst) u32 triples.
+ * orient: orient_record over a batch (trace.hpp:223-238) against the prefix
+ * addr/bits (CidrPrefix, addr masked as CidrPrefix::parse does); kept/flipped
+ * records to `out` in input order; stats = {kept, flipped, dropped_both,
+ * dropped_neither}; returns the records written. */
+uint64_t orc_orient(const uint32_t* recs, uint64_t n, uint32_t prefix_addr, uint32_t prefix_bits, uint32_t* out,
+                    uint64_t* stats);
+/* SlicePartitioner over an ordered batch (trace.hpp:243-281): offsets[s] =
+ * first record of slice s for s in [0, nslices], origin = the first record's
+ * ts, empty slices included. Returns nslices (0 for an empty batch);
+ * offsets == NULL only counts. */
+uint64_t orc_slice_bounds(const uint32_t* recs, uint64_t n, uint32_t slice_seconds, uint64_t* offsets);
+/* SRLT v1 file bytes (for_each_record binary branch, trace.hpp:148-170):
+ * returns the records parsed into `out` (NULL: count only); *err = 0 ok,
+ * 1 bad magic/version, 2 truncated record, 3 timestamp regression, with the
+ * record index in *err_index. */
+uint64_t orc_parse_srlt(const uint8_t* bytes, uint64_t nbytes, uint32_t* out, int* err, uint64_t* err_index);
+
 #ifdef __cplusplus
 }
 #endif

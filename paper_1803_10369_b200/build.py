@@ -12,7 +12,7 @@ LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsrla_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["engine.cu", "generator.cu", "shard.cu"]
+CU_SOURCES = ["engine.cu", "generator.cu", "shard.cu", "ingest.cu"]
 CXX_SOURCES = ["host_math.cpp"]
 
 

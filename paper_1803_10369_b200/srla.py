@@ -22,7 +22,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libsrla_b200.so")
 
 INDICATOR, ROUGH, LINEAR = 0, 1, 2
-OK, E_INVALID, E_RANGE, E_CAPACITY, E_CUDA, E_INTERNAL = range(6)
+OK, E_INVALID, E_RANGE, E_CAPACITY, E_CUDA, E_INTERNAL, E_INPUT = range(7)
 
 # estimators.hpp:19 — evaluated by the library on first load (host glibc)
 KSUPER_TEST_RATIO = 0.99 * (1.0 - math.exp(-1.0 / 3.0))
@@ -32,6 +32,10 @@ class SrlaError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(msg)
         self.code = code
+
+
+class InputError(SrlaError):
+    """sspread::InputError (trace.hpp / snapshot.hpp): malformed trace input."""
 
 
 class CConfig(C.Structure):
@@ -84,6 +88,10 @@ class CSpec(C.Structure):
     ]
 
 
+class COrientStats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("kept", "flipped", "dropped_both", "dropped_neither")]
+
+
 _lib = None
 
 
@@ -129,6 +137,9 @@ def load_library(path: str = LIB_PATH):
         "srla_generator_create": (i32, [C.POINTER(CSpec), i32, C.POINTER(vp)]),
         "srla_generator_destroy": (i32, [vp]),
         "srla_generate_slice": (i32, [vp, u64, vp, u64, C.POINTER(u64), vp]),
+        "srla_parse_srlt": (i32, [vp, u64, vp, C.POINTER(u64), vp]),
+        "srla_orient_records": (i32, [vp, u64, u32, u32, vp, C.POINTER(u64), C.POINTER(COrientStats), vp]),
+        "srla_slice_bounds": (i32, [vp, u64, u32, vp, u64, C.POINTER(u64), vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -145,6 +156,8 @@ EXPORTED_SYMBOLS = (
     "srla_stream", "srla_generator_create", "srla_generator_destroy", "srla_generate_slice",
     "srla_timing_get", "srla_timing_reset", "srla_partition_records", "srla_owner_of",
     "srla_end_slice_async", "srla_end_slice_wait", "srla_end_slice_compact",
+    "srla_parse_srlt", "srla_orient_records", "srla_slice_bounds", "srla_device_alloc", "srla_device_free",
+    "srla_copy_to_device",
 )
 
 
@@ -155,6 +168,8 @@ def _check(rc):
             raise ValueError(msg)  # std::invalid_argument
         if rc == E_RANGE:
             raise IndexError(msg)  # std::out_of_range
+        if rc == E_INPUT:
+            raise InputError(rc, msg)
         raise SrlaError(rc, msg)
 
 
@@ -506,3 +521,56 @@ def partition_records(d_in_ptr: int, n: int, seed: int, nparts: int, part: int, 
 
 def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+# ---------------------------------------------------------------- ingest front end (trace.hpp)
+
+def _stream_of(t):
+    import torch
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def parse_srlt(data_dev):
+    """SRLT v1 file bytes (uint8 CUDA tensor) -> (n, 3) int32 CUDA tensor of records.
+    Raises InputError like for_each_record; the records before the failure are in
+    the exception's `records` attribute."""
+    import torch
+    nbytes = data_dev.numel()
+    cap = max(1, (nbytes - 5) // 12) if nbytes >= 5 else 1
+    out = torch.empty((cap, 3), dtype=torch.int32, device=data_dev.device)
+    n = C.c_uint64()
+    rc = load_library().srla_parse_srlt(C.c_void_p(data_dev.data_ptr()), nbytes, C.c_void_p(out.data_ptr()),
+                                        C.byref(n), C.c_void_p(_stream_of(data_dev)))
+    if rc != OK:
+        try:
+            _check(rc)
+        except InputError as e:
+            e.records = out[: n.value]
+            raise
+    return out[: n.value]
+
+
+def orient_records(recs_dev, prefix_addr: int, prefix_bits: int):
+    """orient_record over a CUDA (n, 3) int32 batch -> (oriented records, stats dict)."""
+    import torch
+    n = recs_dev.shape[0]
+    out = torch.empty((max(1, n), 3), dtype=torch.int32, device=recs_dev.device)
+    m, st = C.c_uint64(), COrientStats()
+    _check(load_library().srla_orient_records(C.c_void_p(recs_dev.data_ptr()), n, prefix_addr & 0xFFFFFFFF,
+                                              prefix_bits, C.c_void_p(out.data_ptr()), C.byref(m), C.byref(st),
+                                              C.c_void_p(_stream_of(recs_dev))))
+    return out[: m.value], {k: getattr(st, k) for k, _ in COrientStats._fields_}
+
+
+def slice_bounds(recs_dev, slice_seconds: int):
+    """SlicePartitioner over an ordered CUDA batch -> numpy offsets (n_slices + 1)."""
+    n = recs_dev.shape[0]
+    lib = load_library()
+    ns = C.c_uint64()
+    st = C.c_void_p(_stream_of(recs_dev))
+    _check(lib.srla_slice_bounds(C.c_void_p(recs_dev.data_ptr()), n, slice_seconds, None, 0, C.byref(ns), st))
+    off = np.zeros(ns.value + 1, np.uint64)
+    if ns.value:
+        _check(lib.srla_slice_bounds(C.c_void_p(recs_dev.data_ptr()), n, slice_seconds,
+                                     off.ctypes.data_as(C.c_void_p), len(off), C.byref(ns), st))
+    return off

@@ -338,8 +338,48 @@ static int replay(int argc, char** argv) {
     });
 }
 
+// test_dropin run <trace.bin> <out.txt> rows cols g gl bits k theta seed:
+// DetectPipeline::run (pipeline.hpp:96-106) — for a binary trace the device
+// front end parses, orients (against 10.0.0.0/8) and slices it in HBM; dumps
+// every report and the final candidate list.
+static int run_mode(int argc, char** argv) {
+    if (argc != 12) return 2;
+    RunConfig rc;
+    rc.sea.rows = std::stoul(argv[4]);
+    rc.sea.cols = std::stoul(argv[5]);
+    rc.sea.rough_slots = std::stoul(argv[6]);
+    rc.sea.linear_slots = std::stoul(argv[7]);
+    rc.sea.recorder_bits = std::stoul(argv[8]);
+    rc.sea.window = std::stoul(argv[9]);
+    rc.sea.theta = std::stoul(argv[10]);
+    rc.sea.seed = std::stoull(argv[11], nullptr, 0);
+    rc.slice_seconds = 1;
+    rc.a_network = CidrPrefix::parse("10.0.0.0/8");
+    std::ofstream out(argv[3]);
+    return with_recorder_word(rc.sea.recorder_bits, [&](auto word) {
+        using Word = decltype(word);
+        DetectPipeline<Word> pipe(rc);
+        pipe.run(argv[2], [&](const WindowReport& r) {
+            out << "report " << r.window_start << " " << r.entries.size() << "\n";
+            for (const auto& e : r.entries) {
+                uint64_t bits = 0;
+                if (e.estimate) std::memcpy(&bits, &*e.estimate, 8);
+                out << e.host << " " << e.union_weight << " " << bits << " " << e.estimate.has_value() << " "
+                    << e.is_super << "\n";
+            }
+        });
+        const auto& c = pipe.candidates();
+        out << "csip " << c.size() << "\n";
+        for (uint32_t h : c.hosts()) out << h << "\n";
+        const auto& st = pipe.orient_stats();
+        out << "orient " << st.kept << " " << st.flipped << " " << st.dropped_both << " " << st.dropped_neither << "\n";
+        return 0;
+    });
+}
+
 int main(int argc, char** argv) {
     if (argc > 1 && std::string(argv[1]) == "replay") return replay(argc, argv);
+    if (argc > 1 && std::string(argv[1]) == "run") return run_mode(argc, argv);
     test_single_pair();
     test_indicator_suppression();
     test_union_view();

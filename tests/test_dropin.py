@@ -90,3 +90,56 @@ def test_dropin_pipeline_replay_matches_oracle(gpu, oracle, dropin_bin, tmp_path
         want = [[int(h), int(w), int(b) if has else 0, int(has), int(sup)]
                 for h, w, b, has, sup in zip(rep["host"], rep["weight"], bits, rep["has_estimate"], rep["is_super"])]
         assert got[s]["report"] == want, f"slice {s}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["pipeline_small", "c1_shape"])
+def test_dropin_run_device_front_end_matches_oracle(gpu, oracle, dropin_bin, tmp_path, name):
+    """DetectPipeline::run on a raw SRLT file with far-side (flipped) and
+    off-network records: the device front end (parse, orient, slice in HBM)
+    gives the reports and candidates of the reference pipeline fed the
+    host-oriented, partitioned records."""
+    from oracle.pyoracle import SeaConfig as OCfg
+    cfg, _ = S.SCENARIOS[name]
+    slices = GF.scenario_slices(name, oracle)
+    recs = np.concatenate(slices)
+    rng = np.random.default_rng(5)
+    raw = recs.copy()
+    flip = rng.random(len(raw)) < 0.25
+    raw[flip, 1], raw[flip, 2] = recs[flip, 2], recs[flip, 1]
+    off = rng.random(len(raw)) < 0.05  # neither side in 10/8: dropped
+    raw[off, 1] = 0xC0A80001
+    raw[off, 2] = 0xC0A80002
+    trace = tmp_path / "raw.bin"
+    _write_srlt(trace, raw)
+    out = tmp_path / "run.txt"
+    c = cfg
+    subprocess.run([dropin_bin, "run", str(trace), str(out), str(c.rows), str(c.cols), str(c.rough_slots),
+                    str(c.linear_slots), str(c.recorder_bits), str(c.window), str(c.theta), hex(c.seed)],
+                   check=True, timeout=600)
+    lines = open(out).read().split("\n")
+    ori, st = oracle.orient(raw, 0x0A000000, 8)
+    assert lines[-2] == "orient " + " ".join(str(int(x)) for x in st)
+    bounds = oracle.slice_bounds(ori, 1)
+    pipe = oracle.pipeline(OCfg(**c.as_dict()))
+    want = []
+    for s in range(len(bounds) - 1):
+        rep = pipe.process_slice(s, ori[bounds[s]:bounds[s + 1]], True)
+        if rep is None:
+            continue
+        bits = rep["estimate"].view(np.uint64)
+        want.append([[int(h), int(w), int(b) if has else 0, int(has), int(sup)]
+                     for h, w, b, has, sup in zip(rep["host"], rep["weight"], bits, rep["has_estimate"],
+                                                  rep["is_super"])])
+    got, i = [], 0
+    while i < len(lines):
+        if lines[i].startswith("report "):
+            n = int(lines[i].split()[2])
+            got.append([list(map(int, lines[i + 1 + j].split())) for j in range(n)])
+            i += 1 + n
+            continue
+        i += 1
+    assert got == want
+    k = lines.index(next(l for l in lines if l.startswith("csip ")))
+    n = int(lines[k].split()[1])
+    assert [int(x) for x in lines[k + 1:k + 1 + n]] == pipe.candidates().tolist()

@@ -897,8 +897,12 @@ struct Engine {
         CK(cudaMemsetAsync(ctr_k1.p, 0, 4 * sizeof(uint32_t), sk));
         CK(cudaEventRecord(t_scan0, sk));
         const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
-        k_scan_bin<W><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, sk>>>(
-            d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
+        if (cfg.rows == 4)
+            k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, sk>>>(
+                d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
+        else
+            k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, sk>>>(
+                d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
         CK(cudaGetLastError());
         CK(cudaEventRecord(t_scan1, sk));
         CK(cudaMemcpyAsync(pin_k1.p, ctr_k1.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, sk));
@@ -958,7 +962,10 @@ struct Engine {
             CK(cudaEventRecord(t_scan0, st));
             if (use_bins && MAXR <= kBinRows) {
                 const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
-                k_scan_bin<W><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                if (cfg.rows == 4)
+                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                else
+                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             } else {
                 k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             }

@@ -14,6 +14,8 @@
 // (Engine::flush_linear).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace srla {
@@ -90,7 +92,11 @@ __device__ __forceinline__ void mark_word(W* base, uint32_t off) {
 // K1 (binned): per record the u column hashes and the sample hash; linear
 // marks are binned by region; sampled packets stamp their rough entries and
 // append events exactly as k_scan does.
-template <typename W>
+//
+// ROWS = 4 (the configs of BASELINE.json) fixes the row loop at compile time;
+// ROWS = 0 reads c.rows (<= kBinRows). Tiles where every thread has its four
+// records take a path without per-record liveness tests.
+template <typename W, int ROWS>
 __global__ void __launch_bounds__(kBinThreads, 4) k_scan_bin(const uint32_t* __restrict__ recs, uint32_t n, DevCfg c,
                                                          BinCfg b, EpochCfg ep, W* __restrict__ lin,
                                                          uint32_t* __restrict__ stamp, uint32_t* __restrict__ ev,
@@ -135,36 +141,44 @@ __global__ void __launch_bounds__(kBinThreads, 4) k_scan_bin(const uint32_t* __r
                 }
             }
         }
-        uint32_t off[kBinPerThread][kBinRows], rank[kBinPerThread][kBinRows];
-        uint16_t reg[kBinPerThread][kBinRows];
+        // per mark: offset in its region, and (region << 16 | rank in the tile's
+        // region bucket); 0xFFFFFFFF = no mark (dead record or row)
+        uint32_t off[kBinPerThread][kBinRows], rr[kBinPerThread][kBinRows];
         uint32_t smask = 0, rsl[kBinPerThread];
+        const uint32_t nrows = ROWS ? static_cast<uint32_t>(ROWS) : c.rows;
+        auto place = [&](auto full_tag) {
+            constexpr bool kFull = decltype(full_tag)::value;
 #pragma unroll
-        for (uint32_t q = 0; q < kBinPerThread; ++q) {
-            rsl[q] = 0;
-            const bool live = q < valid;
-            const uint32_t sample = hash_u32(c.sub_sample, dst[q]);
-            const uint32_t lslot = c.gl_mask ? (sample & c.gl_mask) : (sample % c.gl);
-            const bool smp = live && (sample & c.tau_mask) == 0u;
-            const uint32_t rslot = smp ? reduce32(hash_u32(c.sub_rslot, dst[q]), c.g) : 0u;
+            for (uint32_t q = 0; q < kBinPerThread; ++q) {
+                rsl[q] = 0;
+                const bool live = kFull || q < valid;
+                const uint32_t sample = hash_u32(c.sub_sample, dst[q]);
+                const uint32_t lslot = c.gl_mask ? (sample & c.gl_mask) : (sample % c.gl);
+                uint32_t cols[kBinRows];
 #pragma unroll
-            for (int i = 0; i < kBinRows; ++i) {
-                reg[q][i] = 0xFFFF;
-                const bool on = live && i < static_cast<int>(c.rows);
-                if (on) {
-                    const uint32_t col = column_of(c, i, src[q]);
-                    const uint64_t w = i * lrow + static_cast<uint64_t>(col) * c.gl + lslot;
-                    const uint32_t r = static_cast<uint32_t>(w >> b.region_shift);
-                    reg[q][i] = static_cast<uint16_t>(r);
-                    off[q][i] = static_cast<uint32_t>(w) & rmask;
-                    rank[q][i] = atomicAdd(&s_cnt[r], 1u);  // slot within the tile's region bucket
-                    if (smp) atomicMin(stamp + i * rrow + static_cast<uint64_t>(col) * c.g + rslot, base + q);
+                for (int i = 0; i < kBinRows; ++i) {
+                    rr[q][i] = 0xFFFFFFFFu;
+                    if (live && (ROWS ? i < ROWS : static_cast<uint32_t>(i) < nrows)) {
+                        const uint32_t col = column_of(c, i, src[q]);
+                        cols[i] = col;
+                        const uint64_t w = i * lrow + static_cast<uint64_t>(col) * c.gl + lslot;
+                        const uint32_t r = static_cast<uint32_t>(w >> b.region_shift);
+                        off[q][i] = static_cast<uint32_t>(w) & rmask;
+                        rr[q][i] = (r << 16) | atomicAdd(&s_cnt[r], 1u);
+                    }
+                }
+                if (live && (sample & c.tau_mask) == 0u) {  // sampled (1 in 2^tau): rough stamps
+                    const uint32_t rslot = reduce32(hash_u32(c.sub_rslot, dst[q]), c.g);
+                    for (uint32_t i = 0; i < nrows; ++i)
+                        atomicMin(stamp + i * rrow + static_cast<uint64_t>(cols[i < kBinRows ? i : 0]) * c.g + rslot,
+                                  base + q);
+                    smask |= 1u << q;
+                    rsl[q] = rslot;
                 }
             }
-            if (smp) {
-                smask |= 1u << q;
-                rsl[q] = rslot;
-            }
-        }
+        };
+        if (valid == kBinPerThread) place(std::true_type{});
+        else place(std::false_type{});
         if (__any_sync(0xFFFFFFFFu, smask != 0)) {
             uint32_t pos = warp_append(ev_count, __popc(smask));
 #pragma unroll
@@ -214,10 +228,11 @@ __global__ void __launch_bounds__(kBinThreads, 4) k_scan_bin(const uint32_t* __r
         for (uint32_t q = 0; q < kBinPerThread; ++q)
 #pragma unroll
             for (int i = 0; i < kBinRows; ++i)
-                if (reg[q][i] != 0xFFFF) {
-                    const uint32_t p = s_lbase[reg[q][i]] + rank[q][i];
+                if (rr[q][i] != 0xFFFFFFFFu) {
+                    const uint32_t reg = rr[q][i] >> 16;
+                    const uint32_t p = s_lbase[reg] + (rr[q][i] & 0xFFFFu);
                     s_off[p] = off[q][i];
-                    s_reg[p] = reg[q][i];
+                    s_reg[p] = static_cast<uint16_t>(reg);
                 }
         __syncthreads();
 

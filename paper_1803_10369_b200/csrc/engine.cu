@@ -568,6 +568,9 @@ struct Engine {
     }
 
     // ------------------------------------------------------------ binned linear marks
+    // k_slice_apply_nib: two stages of (packed slice + its mark list)
+    uint64_t nib_apply_smem() const { return 2 * (lin_bytes(1ull << fcfg.shift) + uint64_t(fcfg.cap) * 2); }
+
     // Bytes of `words` linear recorders in the device layout.
     uint64_t lin_bytes(uint64_t words) const { return nib ? words / 2 : words * wb; }
 
@@ -664,7 +667,10 @@ struct Engine {
             CK(cudaFuncSetAttribute(k_slice_apply<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(smem, 16)));
             CK(cudaFuncSetAttribute(k_slice_apply_bulk<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(2 * smem, 32)));
         });
-        CK(cudaFuncSetAttribute(k_slice_apply_nib, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(2 * smem, 32)));
+        if (nib) {
+            if (nib_apply_smem() > 200 * 1024) return false;  // two stages must fit in shared memory
+            CK(cudaFuncSetAttribute(k_slice_apply_nib, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(nib_apply_smem())));
+        }
         // bulk (TMA) slices need 16-byte slices and rows at least one slice long
         const uint64_t slice_words = 1ull << fs;
         bulk_ok = lin_bytes(slice_words) % 16 == 0 && lin_bytes(lin_words) % 16 == 0 && lin_words >= slice_words;
@@ -819,7 +825,7 @@ struct Engine {
             return;
         }
         if (nib) {
-            k_slice_apply_nib<<<std::min<uint32_t>(fcfg.nfine, sms * 3), 256, 2 * lin_bytes(1ull << fcfg.shift), st>>>(
+            k_slice_apply_nib<<<std::min<uint32_t>(fcfg.nfine, sms * 3), 256, nib_apply_smem(), st>>>(
                 static_cast<uint8_t*>(d_lin), lin_words, fcfg, fcfg.nfine, mode, cfg.window, dc.expired, d_counts.p);
             check_launch();
             launched();

@@ -34,18 +34,22 @@ __device__ __forceinline__ uint32_t nib_count_lt(uint32_t x, uint32_t k4) {
 }
 
 // k_slice_apply_bulk for nibble tables: fine slices of 2^f.shift recorders
-// (2^(f.shift-1) bytes, a multiple of 16), double-buffered bulk loads, marks
-// as shared-memory ANDs (two recorders share a byte), mode 0 apply / 1 apply +
-// age / 2 apply + count active (pre-age) + age.
+// (2^(f.shift-1) bytes, a multiple of 16). Each stage bulk-loads a slice AND
+// its mark list into shared memory on one mbarrier (the marks' global-load
+// latency was the stall), double-buffered; marks are shared-memory ANDs (two
+// recorders share a byte); mode 0 apply / 1 apply + age / 2 apply + count
+// active (pre-age) + age; the slice is bulk-stored back.
+// Shared memory: 2 x (slice bytes + f.cap x 2 B).
 __global__ void __launch_bounds__(256) k_slice_apply_nib(uint8_t* __restrict__ lin, uint64_t row_words, FineCfg f,
                                                          uint32_t f_end, int mode, uint32_t k, uint32_t expired,
                                                          unsigned long long* __restrict__ counts) {
     extern __shared__ __align__(128) uint8_t s_raw[];
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ unsigned long long s_part[2][8];
+    __shared__ uint32_t s_n[2];
     const uint32_t tid = threadIdx.x;
     const uint32_t slice_bytes = (1u << f.shift) >> 1;
-    uint8_t* buf[2] = {s_raw, s_raw + slice_bytes};
+    const uint32_t stage = slice_bytes + f.cap * 2u;  // slice | marks (f.cap is a multiple of 8)
     const uint32_t k4 = k * 0x01010101u, e8 = expired * kNibOne;
     auto next_slice = [&](uint32_t from) -> uint32_t {
         for (uint32_t fb = from; fb < f_end; fb += gridDim.x)
@@ -53,33 +57,38 @@ __global__ void __launch_bounds__(256) k_slice_apply_nib(uint8_t* __restrict__ l
         return f_end;
     };
     auto gaddr = [&](uint32_t fb) { return lin + ((static_cast<uint64_t>(fb) << f.shift) >> 1); };
+    auto issue = [&](uint32_t fb, uint32_t b) {  // thread 0
+        const uint32_t n = min(f.count[fb], f.cap);
+        const uint32_t mb = (n * 2u + 15u) & ~15u;
+        s_n[b] = n;
+        mbar_expect_tx(&s_bar[b], slice_bytes + mb);
+        bulk_load(s_raw + b * stage, gaddr(fb), slice_bytes, &s_bar[b]);
+        if (mb) bulk_load(s_raw + b * stage + slice_bytes, f.bins + static_cast<uint64_t>(fb) * f.cap, mb, &s_bar[b]);
+    };
     if (tid == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
     }
     __syncthreads();
     uint32_t cur = next_slice(blockIdx.x);
-    if (tid == 0 && cur < f_end) {
-        mbar_expect_tx(&s_bar[0], slice_bytes);
-        bulk_load(buf[0], gaddr(cur), slice_bytes, &s_bar[0]);
-    }
+    if (tid == 0 && cur < f_end) issue(cur, 0);
     for (uint32_t i = 0; cur < f_end; ++i) {
         const uint32_t b = i & 1u;
         const uint32_t nxt = next_slice(cur + gridDim.x);
         if (tid == 0 && nxt < f_end) {
-            bulk_wait_read_all();
-            mbar_expect_tx(&s_bar[b ^ 1u], slice_bytes);
-            bulk_load(buf[b ^ 1u], gaddr(nxt), slice_bytes, &s_bar[b ^ 1u]);
+            bulk_wait_read_all();  // the other buffer's store (slice i-1) has left shared memory
+            issue(nxt, b ^ 1u);
         }
         mbar_wait(&s_bar[b], (i >> 1) & 1u);
         if (tid == 0) atomicAdd(f.streamed, static_cast<unsigned long long>(slice_bytes));
-        unsigned int* s32 = reinterpret_cast<unsigned int*>(buf[b]);
-        const uint32_t n = min(f.count[cur], f.cap);
-        const uint16_t* e = f.bins + static_cast<uint64_t>(cur) * f.cap;
+        uint8_t* sb = s_raw + b * stage;
+        unsigned int* s32 = reinterpret_cast<unsigned int*>(sb);
+        const uint32_t n = s_n[b];
+        const uint16_t* e = reinterpret_cast<const uint16_t*>(sb + slice_bytes);
         const uint4* ev = reinterpret_cast<const uint4*>(e);
         auto mark = [&](uint32_t o) { atomicAnd(s32 + (o >> 3), ~(0xFu << (4u * (o & 7u)))); };
         for (uint32_t q = tid; q < n / 8; q += blockDim.x) {
-            const uint4 x = __ldcs(ev + q);
+            const uint4 x = ev[q];
             mark(x.x & 0xFFFF); mark(x.x >> 16);
             mark(x.y & 0xFFFF); mark(x.y >> 16);
             mark(x.z & 0xFFFF); mark(x.z >> 16);
@@ -92,7 +101,7 @@ __global__ void __launch_bounds__(256) k_slice_apply_nib(uint8_t* __restrict__ l
             const uint64_t row_a = w0 / row_words;
             const uint64_t split = (row_a + 1) * row_words;  // first word of the next row
             unsigned long long acc_a = 0, acc_b = 0;
-            uint4* sv = reinterpret_cast<uint4*>(buf[b]);
+            uint4* sv = reinterpret_cast<uint4*>(sb);
             const uint32_t nv = slice_bytes / 16;
             for (uint32_t q = tid; q < nv; q += blockDim.x) {
                 uint4 x = sv[q];
@@ -122,19 +131,19 @@ __global__ void __launch_bounds__(256) k_slice_apply_nib(uint8_t* __restrict__ l
             fence_proxy_async_smem();
             __syncthreads();
             if (mode == 2 && tid == 0) {
-                unsigned long long sa = 0, sb = 0;
+                unsigned long long sa = 0, sb2 = 0;
                 for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
                     sa += s_part[0][w];
-                    sb += s_part[1][w];
+                    sb2 += s_part[1][w];
                 }
                 if (sa) atomicAdd(counts + row_a, sa);
-                if (sb) atomicAdd(counts + row_a + 1, sb);
+                if (sb2) atomicAdd(counts + row_a + 1, sb2);
             }
         } else {
             fence_proxy_async_smem();
             __syncthreads();
         }
-        if (tid == 0) bulk_store(gaddr(cur), buf[b], slice_bytes);
+        if (tid == 0) bulk_store(gaddr(cur), sb, slice_bytes);
         cur = nxt;
     }
     if (tid == 0) bulk_wait_all();

@@ -132,7 +132,7 @@ def ncu_traffic(workload):
     if not os.path.exists(p):
         return {}
     wl = json.load(open(p)).get("workloads", {}).get(workload, {})
-    return {k: v.get("dram_bytes_per_launch") for k, v in wl.items()}
+    return {k: v for k, v in wl.items()}
 
 
 def kernel_rooflines(tm, step_ms_total, cfg, peak, peak_src, packets, steps, workload):
@@ -164,9 +164,12 @@ def kernel_rooflines(tm, step_ms_total, cfg, peak, peak_src, packets, steps, wor
         if n == 0 or kms <= 0:
             continue
         ach = byts / (kms * 1e-3) / 1e9
+        nc = traffic.get(name) or {}
         kernels[name] = {"ms_per_launch": kms / n, "launches": n, "algorithmic_bytes_per_launch": byts / n,
                          "achieved": ach, "frac": ach / peak, "share_of_step": kms / step_ms_total,
-                         "traffic": traffic.get(name)}
+                         "traffic": nc.get("dram_bytes_per_launch"),
+                         "ncu": {k: nc[k] for k in ("dram_pct", "sm_pct", "warps_active_pct", "warp_inst") if k in nc}
+                         or None}
     dom = max(kernels, key=lambda k: kernels[k]["share_of_step"])
     d = kernels[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": d["achieved"], "peak": peak, "unit": "GB/s",

@@ -36,10 +36,14 @@ def main(workload, reps):
             ent["launches"].append({"kernel": kname.split("(")[0], "dram_bytes": b, "ms": ms,
                                     "dram_pct": float(d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]),
                                     "sm_pct": float(d["sm__throughput.avg.pct_of_peak_sustained_elapsed"]),
+                                    "warp_inst": float(d["smsp__inst_executed.sum"]),
+                                    "warps_active_pct": float(d["sm__warps_active.avg.pct_of_peak_sustained_active"]),
                                     "source": os.path.basename(rep)})
     for ent in wl.values():
         ls = ent["launches"]
         ent["dram_bytes_per_launch"] = sum(x["dram_bytes"] for x in ls) / len(ls)
+        for key in ("dram_pct", "sm_pct", "warp_inst", "warps_active_pct", "ms"):
+            ent[key] = sum(x[key] for x in ls) / len(ls)
     json.dump(out, open(path, "w"), indent=1)
     print(json.dumps({k: v["dram_bytes_per_launch"] for k, v in wl.items()}, indent=1))
 

@@ -209,7 +209,15 @@ struct Engine {
     uint64_t sweep_pos = 0;
     EpochCfg ecfg() const { return EpochCfg{epoch ? 1u : 0u, cur_epoch, hist.p, lin_words}; }
     PinBuf<uint32_t> pin_bc;
-    uint64_t pending_entries = 0;
+    uint64_t pending_entries = 0;  // marks in the region bins
+    uint64_t fine_pending = 0;     // marks split into the fine bins, not yet applied
+    // Early split: right after K1 the region bins are split on stream ssplit,
+    // concurrent with the scan's ordering phase (K2..K5, latency-bound); the
+    // apply waits for it (flush_linear), as does the next K1.
+    cudaStream_t ssplit = nullptr;
+    cudaEvent_t ev_split_done = nullptr, ev_k1_done = nullptr;
+    bool split_in_flight = false;
+    bool early_split = [] { const char* v = std::getenv("SRLA_EARLY_SPLIT"); return !(v && v[0] == '0'); }();
     // Second region-bin set: a slice's K1 bins into it on stream sk while the
     // previous slice's asynchronous end-of-slice still flushes the first
     // (srla_end_slice_async followed by srla_scan_batch of device records).
@@ -251,14 +259,14 @@ struct Engine {
         ev_pool.pop_back();
         return e;
     }
-    cudaEvent_t timer_start() {
+    cudaEvent_t timer_start(cudaStream_t s = nullptr) {
         cudaEvent_t a = take_event();
-        CK(cudaEventRecord(a, st));
+        CK(cudaEventRecord(a, s ? s : st));
         return a;
     }
-    void timer_stop(cudaEvent_t a, int kind) {
+    void timer_stop(cudaEvent_t a, int kind, cudaStream_t s = nullptr) {
         cudaEvent_t b = take_event();
-        CK(cudaEventRecord(b, st));
+        CK(cudaEventRecord(b, s ? s : st));
         timers.push_back({a, b, kind});
         if (timers.size() > 256) resolve_timers(true);
     }
@@ -320,6 +328,9 @@ struct Engine {
         CK(cudaStreamCreateWithPriority(&sk, cudaStreamNonBlocking, prio_low));
         CK(cudaEventCreateWithFlags(&ev_scan_done, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_k1_gate, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_split_done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_k1_done, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&ssplit, cudaStreamNonBlocking));
         CK(cudaEventRecord(ev_scan_done, st));
         ctr_k1.ensure(4);
         pin_k1.ensure(4);
@@ -417,6 +428,12 @@ struct Engine {
         }
         if (ev_scan_done) cudaEventDestroy(ev_scan_done);
         if (ev_k1_gate) cudaEventDestroy(ev_k1_gate);
+        if (ssplit) {
+            cudaStreamSynchronize(ssplit);
+            cudaStreamDestroy(ssplit);
+        }
+        for (cudaEvent_t e : {ev_split_done, ev_k1_done})
+            if (e) cudaEventDestroy(e);
         if (st) cudaStreamDestroy(st);
     }
 
@@ -768,47 +785,74 @@ struct Engine {
     // Apply pending linear marks. mode 0: apply only (slices without marks
     // untouched); 1: apply + age the whole table; 2: apply + count active per
     // row into d_counts (pre-age) + age. One streaming pass over the table.
+    // Split the region bins into the fine bins on stream `s` (the region bins
+    // and their counts are free again when ev_split_done fires).
+    void split_now(cudaStream_t s) {
+        if (!pending_entries) return;
+        const uint32_t R = bcfg.nregions;
+        if (split_in_flight) CK(cudaEventSynchronize(ev_split_done));  // pin_bc / tile_prefix reuse
+        split_in_flight = false;
+        CK(cudaMemcpyAsync(pin_bc.p, bin_count.p, R * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        // per-region entry counts (clamped: overflow was applied directly) and tile prefix
+        uint32_t* n_r = pin_bc.p + R + 1;
+        uint32_t* prefix = pin_bc.p;  // reuse: prefix[0..R]
+        std::vector<uint32_t> cnt(pin_bc.p, pin_bc.p + R);
+        uint32_t run = 0;
+        for (uint32_t r = 0; r < R; ++r) {
+            prefix[r] = run;
+            n_r[r] = std::min(cnt[r], bcfg.cap);
+            run += (n_r[r] + kSplitTile - 1) / kSplitTile;
+        }
+        prefix[R] = run;
+        if (s != st) {
+            CK(cudaEventRecord(ev_k1_done, st));
+            CK(cudaStreamWaitEvent(s, ev_k1_done, 0));
+        }
+        CK(cudaMemcpyAsync(tile_prefix.p, pin_bc.p, (2 * R + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        if (run) {
+            const cudaEvent_t t0 = timer_start(s);
+            with_w([&](auto w) {
+                using W = decltype(w);
+                // an early split leaves room for the ordering phase's kernels
+                static const uint32_t waves = [] { const char* v = std::getenv("SRLA_SPLIT_WAVES"); return v ? static_cast<uint32_t>(std::atoi(v)) : 2u; }();
+                k_split<W><<<std::min<uint32_t>(run, sms * (s == st ? 8u : waves)), kSplitThreads, split_smem, s>>>(
+                    bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg, ecfg(),
+                    static_cast<W*>(d_lin));
+            });
+            check_launch();
+            launched();
+            timer_stop(t0, kTimeSplit, s);
+            timing.split_kernel_launches += 1;
+            timing.split_entries += pending_entries;
+        }
+        CK(cudaMemsetAsync(bin_count.p, 0, R * sizeof(uint32_t), s));
+        if (s != st) {
+            CK(cudaEventRecord(ev_split_done, s));
+            split_in_flight = true;
+        }
+        fine_pending += pending_entries;
+        pending_entries = 0;
+    }
+    // the engine stream waits for an early split (device-side)
+    void join_split() {
+        if (!split_in_flight) return;
+        CK(cudaStreamWaitEvent(st, ev_split_done, 0));
+        split_in_flight = false;
+    }
+
     void flush_linear(int mode = 0) {
         if (!use_bins) return;
         join_maint_lin();
-        if (pending_entries == 0 && mode == 0) return;
+        split_now(st);
+        join_split();
+        if (fine_pending == 0 && mode == 0) return;
         const uint64_t total = uint64_t(cfg.rows) * lin_words;
-        const uint32_t R = bcfg.nregions;
-        if (pending_entries) {
-            CK(cudaMemcpyAsync(pin_bc.p, bin_count.p, R * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            // per-region entry counts (clamped: overflow was applied directly) and tile prefix
-            uint32_t* n_r = pin_bc.p + R + 1;
-            uint32_t* prefix = pin_bc.p;  // reuse: prefix[0..R]
-            std::vector<uint32_t> cnt(pin_bc.p, pin_bc.p + R);
-            uint32_t run = 0;
-            for (uint32_t r = 0; r < R; ++r) {
-                prefix[r] = run;
-                n_r[r] = std::min(cnt[r], bcfg.cap);
-                run += (n_r[r] + kSplitTile - 1) / kSplitTile;
-            }
-            prefix[R] = run;
-            CK(cudaMemcpyAsync(tile_prefix.p, pin_bc.p, (2 * R + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-            if (run) {
-                const cudaEvent_t t0 = timer_start();
-                with_w([&](auto w) {
-                    using W = decltype(w);
-                    k_split<W><<<std::min<uint32_t>(run, sms * 8), kSplitThreads, split_smem, st>>>(
-                        bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg, ecfg(),
-                        static_cast<W*>(d_lin));
-                });
-                check_launch();
-                launched();
-                timer_stop(t0, kTimeSplit);
-                timing.split_kernel_launches += 1;
-                timing.split_entries += pending_entries;
-            }
-        }
         open_k1_gate();
         const cudaEvent_t t_apply = timer_start();
-        timing.apply_entries += pending_entries;
+        timing.apply_entries += fine_pending;
         if (epoch) {
-            if (pending_entries) {
+            if (fine_pending) {
                 k_slice_stamp<<<std::min<uint32_t>(fcfg.nfine, sms * 3), 256, 2u << fcfg.shift, st>>>(
                     static_cast<uint8_t*>(d_lin), total, lin_words, fcfg, 0, bulk_ok ? 1 : 0, cur_epoch, cfg.window, hist.p);
                 check_launch();
@@ -817,11 +861,10 @@ struct Engine {
                 timing.apply_kernel_launches += 1;
                 CK(cudaMemcpyAsync(pin_streamed.p, d_streamed.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
                 CK(cudaMemsetAsync(fine_count.p, 0, fcfg.nfine * sizeof(uint32_t), st));
-                CK(cudaMemsetAsync(bin_count.p, 0, R * sizeof(uint32_t), st));
             } else {
                 ev_pool.push_back(t_apply);
             }
-            pending_entries = 0;
+            fine_pending = 0;
             return;
         }
         if (nib) {
@@ -851,8 +894,7 @@ struct Engine {
         timing.apply_kernel_launches += 1;
         CK(cudaMemcpyAsync(pin_streamed.p, d_streamed.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         CK(cudaMemsetAsync(fine_count.p, 0, fcfg.nfine * sizeof(uint32_t), st));
-        if (pending_entries) CK(cudaMemsetAsync(bin_count.p, 0, R * sizeof(uint32_t), st));
-        pending_entries = 0;
+        fine_pending = 0;
     }
 
     // ------------------------------------------------------------ scan
@@ -959,6 +1001,7 @@ struct Engine {
             else join_eos();
         }
         join_maint_lin();  // K1 may stamp the linear table directly (bin overflow)
+        join_split();      // the region bins must have been split and zeroed
         while (!k1_done) {
             CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
             if (use_bins) {
@@ -991,6 +1034,8 @@ struct Engine {
             ev.ensure(3ull * ev_cap);
         }
         stats.sampled_events += n_ev;
+        // split the region bins now, concurrent with the ordering phase below
+        if (use_bins && early_split && !overlap_on) split_now(ssplit);
         trace("scan: K1");
         if (!n_ev) return;
         const auto w_order = std::chrono::steady_clock::now();

@@ -645,10 +645,10 @@ struct Engine {
         uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);
         if (const char* be = std::getenv("SRLA_SMALL_BIN_ENTRIES"); be && small) coarse_total = std::strtoull(be, nullptr, 10);
         bcfg.cap = static_cast<uint32_t>(std::min<uint64_t>(coarse_total / bcfg.nregions, 0xFFFFFFF0ull)) & ~3u;
-        bins.ensure(uint64_t(bcfg.cap) * bcfg.nregions);
+        bins.ensure(uint64_t(bcfg.cap) * bcfg.nregions + 4);  // + 16 bytes: k_split bulk-loads whole 16-byte units
         bin_count.ensure(bcfg.nregions);
         if (overlap_on) {
-            bins_alt.ensure(uint64_t(bcfg.cap) * bcfg.nregions);
+            bins_alt.ensure(uint64_t(bcfg.cap) * bcfg.nregions + 4);
             bin_count_alt.ensure(bcfg.nregions);
             CK(cudaMemsetAsync(bin_count_alt.p, 0, bcfg.nregions * sizeof(uint32_t), st));
         }
@@ -677,7 +677,7 @@ struct Engine {
         fcfg.streamed = d_streamed.p;
         CK(cudaMemsetAsync(fine_count.p, 0, fine_count.cap * sizeof(uint32_t), st));
         const int smem = static_cast<int>(lin_bytes(1ull << fs));
-        split_smem = kSplitTile * 4 + fcfg.per_region * 16;
+        split_smem = 2 * kSplitTile * 4 + fcfg.per_region * 16;  // two tile stages + per-slice tables
         with_w([&](auto w) {
             using W = decltype(w);
             CK(cudaFuncSetAttribute(k_split<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(split_smem)));

@@ -20,6 +20,43 @@
 
 namespace srla {
 
+// ---- bulk-copy (TMA engine) + mbarrier helpers, sm_90+/sm_100a PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// global -> shared, completion counted on the mbarrier in bytes
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst_smem)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// shared -> global, tracked by the issuing thread's bulk groups
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 struct BinCfg {
     uint32_t* bins;         // nregions x cap offsets (words within the region)
     uint32_t* count;        // reserved entries per region (may exceed cap: overflow applied directly)
@@ -361,51 +398,67 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
                                                          uint32_t region_shift, FineCfg f, EpochCfg ep,
                                                          W* __restrict__ lin) {
     // dynamic shared memory, sized by the fan-out f.per_region (<= 4096):
-    //   sorted[kSplitTile] | cnt[P] | lbase[P] | win[P] (uint2)
-    extern __shared__ uint32_t s_dyn[];
-    uint32_t* s_sorted = s_dyn;  // (slice << 16) | offset within slice
-    uint32_t* s_cnt = s_sorted + kSplitTile;
+    //   stage[2][kSplitTile] | cnt[P] | lbase[P] | win[P] (uint2)
+    // A tile's entries are bulk-loaded into its stage while the block sorts
+    // the previous tile (the coarse bins have >= 16 bytes of slack at the end);
+    // once read into registers, the stage holds the tile's sorted entries.
+    extern __shared__ __align__(128) uint32_t s_dyn[];
+    uint32_t* s_stage = s_dyn;
+    uint32_t* s_cnt = s_dyn + 2 * kSplitTile;
     uint32_t* s_lbase = s_cnt + f.per_region;
     // per fine slice: {bin slot of sorted entry i = x + i (mod 2^32; nfine * cap < 2^32 by
     // construction, Engine::setup_bins), first sorted index that no longer fits its bin}
     uint2* s_win = reinterpret_cast<uint2*>(s_lbase + f.per_region);
     __shared__ uint32_t s_warp[kSplitThreads / 32];
-    __shared__ uint32_t s_region;
+    __shared__ uint32_t s_region[2], s_n[2];
+    __shared__ __align__(8) uint64_t s_bar[2];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t total_tiles = tile_prefix[nregions];
     const uint32_t fmask = (1u << f.shift) - 1u;
     const uint32_t per_thread = (f.per_region + kSplitThreads - 1) / kSplitThreads;
-    for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        if (tid == 0) {  // region r with tile_prefix[r] <= t < tile_prefix[r+1]
-            uint32_t lo = 0, hi = nregions;
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) / 2;
-                if (tile_prefix[mid] <= t) lo = mid;
-                else hi = mid;
-            }
-            s_region = lo;
+    // thread 0: locate tile t (region r with tile_prefix[r] <= t < tile_prefix[r+1]) and load it
+    auto issue = [&](uint32_t t, uint32_t b) {
+        uint32_t lo = 0, hi = nregions;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (tile_prefix[mid] <= t) lo = mid;
+            else hi = mid;
         }
+        const uint32_t begin = (t - tile_prefix[lo]) * kSplitTile;
+        const uint32_t n = min(coarse_n[lo] - begin, static_cast<uint32_t>(kSplitTile));
+        s_region[b] = lo;
+        s_n[b] = n;
+        const uint32_t bytes = (n * 4u + 15u) & ~15u;
+        mbar_expect_tx(&s_bar[b], bytes);
+        bulk_load(s_stage + b * kSplitTile, coarse + static_cast<uint64_t>(lo) * coarse_cap + begin, bytes, &s_bar[b]);
+    };
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+    }
+    __syncthreads();
+    if (tid == 0 && blockIdx.x < total_tiles) issue(blockIdx.x, 0);
+    uint32_t it = 0;
+    for (uint32_t t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+        const uint32_t sb = it & 1u;
+        // the other stage was last read by the previous tile, finished at its final barrier
+        if (tid == 0 && t + gridDim.x < total_tiles) issue(t + gridDim.x, sb ^ 1u);
         for (uint32_t i = tid; i < f.per_region; i += kSplitThreads) s_cnt[i] = 0;
+        mbar_wait(&s_bar[sb], (it >> 1) & 1u);
         __syncthreads();
-        const uint32_t r = s_region;
-        const uint32_t begin = (t - tile_prefix[r]) * kSplitTile;
-        const uint32_t n = min(coarse_n[r] - begin, static_cast<uint32_t>(kSplitTile));
-        const uint32_t* src = coarse + static_cast<uint64_t>(r) * coarse_cap + begin;
+        const uint32_t r = s_region[sb];
+        const uint32_t n = s_n[sb];
+        uint32_t* s_sorted = s_stage + sb * kSplitTile;  // (slice << 16) | offset within slice
         uint32_t off[kSplitPerThread];
         const uint32_t e0 = tid * kSplitPerThread;
-        if (e0 + kSplitPerThread <= n) {
-            const uint4* v = reinterpret_cast<const uint4*>(src + e0);
+        const uint4* v = reinterpret_cast<const uint4*>(s_stage + sb * kSplitTile + e0);
 #pragma unroll
-            for (int q = 0; q < kSplitPerThread / 4; ++q) {
-                const uint4 x = __ldcs(v + q);
-                off[4 * q] = x.x;
-                off[4 * q + 1] = x.y;
-                off[4 * q + 2] = x.z;
-                off[4 * q + 3] = x.w;
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < kSplitPerThread; ++k) off[k] = e0 + k < n ? __ldcs(src + e0 + k) : 0xFFFFFFFFu;
+        for (int q = 0; q < kSplitPerThread / 4; ++q) {
+            const uint4 x = v[q];
+            off[4 * q] = e0 + 4 * q < n ? x.x : 0xFFFFFFFFu;
+            off[4 * q + 1] = e0 + 4 * q + 1 < n ? x.y : 0xFFFFFFFFu;
+            off[4 * q + 2] = e0 + 4 * q + 2 < n ? x.z : 0xFFFFFFFFu;
+            off[4 * q + 3] = e0 + 4 * q + 3 < n ? x.w : 0xFFFFFFFFu;
         }
         uint32_t rank[kSplitPerThread];
 #pragma unroll
@@ -571,43 +624,6 @@ __global__ void __launch_bounds__(256) k_slice_apply(W* __restrict__ lin, uint64
 }  // namespace srla
 
 namespace srla {
-
-// ---- bulk-copy (TMA engine) + mbarrier helpers, sm_90+/sm_100a PTX
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-// global -> shared, completion counted on the mbarrier in bytes
-__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst_smem)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-// shared -> global, tracked by the issuing thread's bulk groups
-__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Same contract as k_slice_apply for slices [f_begin, f_end) whose bytes are
 // a multiple of 16 and 16-byte aligned (and rows are 16-byte multiples):

@@ -1855,68 +1855,71 @@ struct Engine {
         return static_cast<uint8_t*>(d_lin) + lin_bytes(uint64_t(row) * lin_words);
     }
 
+    // Row export/import (the raw spans of sea.hpp:341-346; snapshot.hpp
+    // writes and reads them). Epoch-stamp and nibble tables convert to and
+    // from the reference's layout on the device, chunk by chunk through a
+    // staging buffer, so a 16 GiB row moves at copy speed.
+    static constexpr uint64_t kXferChunk = 1ull << 28;  // reference-layout bytes per hop
+    DevBuf<uint8_t> xfer;
+
     void export_row(uint32_t row, int kind, void* buf, uint64_t bytes) {
         flush_linear();
         uint8_t* p = row_ptr(row, kind);
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
-        if (nib && kind == SRLA_LINEAR) {  // unpack to the reference's byte per recorder
-            std::vector<uint8_t> pk(lin_bytes(lin_words));
-            CK(cudaMemcpyAsync(pk.data(), p, pk.size(), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+        if (kind == SRLA_LINEAR && (nib || epoch)) {
+            xfer.ensure(std::min(bytes, kXferChunk));
             uint8_t* b = static_cast<uint8_t*>(buf);
-            for (uint64_t j = 0; j < pk.size(); ++j) {
-                b[2 * j] = pk[j] & 0xF;
-                b[2 * j + 1] = pk[j] >> 4;
+            for (uint64_t j0 = 0; j0 < bytes; j0 += kXferChunk) {
+                const uint64_t m = std::min(kXferChunk, bytes - j0);  // recorders (= output bytes)
+                if (nib)
+                    k_unpack_nib<<<blocks(m / 2, 256, 16), 256, 0, st>>>(p + j0 / 2, m / 2, xfer.p);
+                else
+                    k_stamps_to_values<<<blocks(m, 256, 16), 256, 0, st>>>(p + j0, m, cur_epoch, dc.expired, xfer.p);
+                check_launch();
+                launched();
+                CK(cudaMemcpyAsync(b + j0, xfer.p, m, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
             }
             return;
         }
         CK(cudaMemcpyAsync(buf, p, bytes, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        if (epoch && kind == SRLA_LINEAR) {
-            uint8_t* b = static_cast<uint8_t*>(buf);
-            uint8_t lut[256];
-            for (uint32_t s = 0; s < 256; ++s) lut[s] = static_cast<uint8_t>(stamp_value(s));
-            for (uint64_t j = 0; j < bytes; ++j) b[j] = lut[b[j]];
-        }
     }
 
     void import_row(uint32_t row, int kind, const void* buf, uint64_t bytes) {
         flush_linear();
         uint8_t* p = row_ptr(row, kind);
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
-        if (nib && kind == SRLA_LINEAR) {
+        if (kind == SRLA_LINEAR && (nib || epoch)) {
             const uint8_t* v = static_cast<const uint8_t*>(buf);
-            bool in_model = true;
-            for (uint64_t j = 0; j < bytes && in_model; ++j) in_model = v[j] <= 0xF;
-            if (!in_model) {  // values a nibble cannot hold: back to a byte per recorder
-                leave_nibble();
+            uint8_t vmax = 0;  // vectorisable reduction (no early exit)
+            for (uint64_t j = 0; j < bytes; ++j) vmax = std::max(vmax, v[j]);
+            if (vmax > (nib ? 0xFu : dc.expired)) {  // beyond the packed / stamp model: a byte per value
+                if (nib) leave_nibble();
+                else leave_epoch();
                 import_row(row, kind, buf, bytes);
                 return;
             }
-            std::vector<uint8_t> pk(bytes / 2);
-            for (uint64_t j = 0; j < pk.size(); ++j) pk[j] = static_cast<uint8_t>(v[2 * j] | (v[2 * j + 1] << 4));
-            CK(cudaMemcpyAsync(p, pk.data(), pk.size(), cudaMemcpyHostToDevice, st));
-            CK(cudaStreamSynchronize(st));
-            return;
-        }
-        if (epoch && kind == SRLA_LINEAR) {
-            const uint8_t* v = static_cast<const uint8_t*>(buf);
-            bool in_model = true;
-            for (uint64_t j = 0; j < bytes && in_model; ++j) in_model = v[j] <= dc.expired;
-            if (!in_model) {
-                leave_epoch();  // values beyond `expired` need literal recorders
-            } else {
-                std::vector<uint8_t> s(bytes);
-                for (uint64_t j = 0; j < bytes; ++j)
-                    s[j] = static_cast<uint8_t>((cur_epoch - std::min<uint32_t>(v[j], dc.expired)) & 0xFFu);
-                CK(cudaMemcpyAsync(p, s.data(), bytes, cudaMemcpyHostToDevice, st));
+            xfer.ensure(std::min(bytes, kXferChunk));
+            for (uint64_t j0 = 0; j0 < bytes; j0 += kXferChunk) {
+                const uint64_t m = std::min(kXferChunk, bytes - j0);
+                CK(cudaMemcpyAsync(xfer.p, v + j0, m, cudaMemcpyHostToDevice, st));
+                if (nib)
+                    k_pack_nib<<<blocks(m / 2, 256, 16), 256, 0, st>>>(xfer.p, m / 2, p + j0 / 2);
+                else
+                    k_values_to_stamps<<<blocks(m, 256, 16), 256, 0, st>>>(xfer.p, m, cur_epoch, p + j0);
+                check_launch();
+                launched();
+                CK(cudaStreamSynchronize(st));  // the staging buffer is reused
+            }
+            if (epoch) {
                 CK(cudaMemsetAsync(hist.p + uint64_t(row) * 256, 0, 256 * sizeof(unsigned long long), st));
                 k_row_hist<<<blocks(bytes, 256, 4), 256, 0, st>>>(p, bytes, hist.p + uint64_t(row) * 256);
                 check_launch();
                 launched();
                 CK(cudaStreamSynchronize(st));
-                return;
             }
+            return;
         }
         CK(cudaMemcpyAsync(p, buf, bytes, cudaMemcpyHostToDevice, st));
         CK(cudaStreamSynchronize(st));

@@ -234,6 +234,25 @@ __global__ void __launch_bounds__(256) k_epoch_to_literal(uint8_t* __restrict__ 
     }
 }
 
+// Row export/import through a device staging buffer (a snapshot of a 64 GiB
+// table converts at HBM speed instead of in a host loop):
+// stamps -> literal values min((cur - s) mod 256, expired), and back
+// (s = cur - v, values already checked to be <= expired).
+__global__ void __launch_bounds__(256) k_stamps_to_values(const uint8_t* __restrict__ s, uint64_t n, uint32_t cur,
+                                                          uint32_t expired, uint8_t* __restrict__ v) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t a = (cur - s[q]) & 0xFFu;
+        v[q] = static_cast<uint8_t>(a < expired ? a : expired);
+    }
+}
+__global__ void __launch_bounds__(256) k_values_to_stamps(const uint8_t* __restrict__ v, uint64_t n, uint32_t cur,
+                                                          uint8_t* __restrict__ s) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        s[q] = static_cast<uint8_t>((cur - v[q]) & 0xFFu);
+}
+
 // Histogram of one row's stamps (after an import). grid-stride, 256 bins.
 __global__ void __launch_bounds__(256) k_row_hist(const uint8_t* __restrict__ row, uint64_t n,
                                                   unsigned long long* __restrict__ hist) {

@@ -270,4 +270,12 @@ __global__ void __launch_bounds__(256) k_unpack_nib(const uint8_t* __restrict__ 
     }
 }
 
+// a byte per recorder (values <= 15, checked by the caller) -> packed
+__global__ void __launch_bounds__(256) k_pack_nib(const uint8_t* __restrict__ wide, uint64_t nbytes,
+                                                  uint8_t* __restrict__ packed) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < nbytes;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        packed[q] = static_cast<uint8_t>(wide[2 * q] | (wide[2 * q + 1] << 4));
+}
+
 }  // namespace srla

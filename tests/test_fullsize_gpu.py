@@ -164,3 +164,33 @@ def test_c2_fullsize_overlapped_pipeline_matches_sync(gpu, monkeypatch):
             assert g.tobytes() == w.tobytes()
     for (r1, l1), (r2, l2) in zip(want_rows, [(e.export_row(i, 1), e.export_row(i, 2)) for i in range(cfg.rows)]):
         assert np.array_equal(r1, r2) and np.array_equal(l1, l2)
+
+
+@pytest.mark.slow
+def test_c3_row_export_import_on_device(gpu):
+    """Snapshot rows at the 2^24-column scale (§8f rank 3): a 16 GiB
+    epoch-stamp linear row exports as the reference's literal values (converted
+    on the device), its active count equals count_active, and an import of a
+    modified row round-trips exactly."""
+    import time
+    from paper_1803_10369_b200.srla import DeviceTraceGenerator, EstimatorArray, PlantSpec, SeaConfig
+    cfg = SeaConfig(rows=4, cols=1 << 24, **{k: v for k, v in C2_SKETCH.items() if k != "rows"})
+    e = EstimatorArray(cfg)
+    gen = DeviceTraceGenerator(PlantSpec(seed=3, slices=2, window=10, a_hosts=1 << 20, b_hosts=1 << 24,
+                                         pairs_per_slice=10_000_000, skew=0.0, plants=[]))
+    for sid in range(2):
+        e.scan(gen.slice_tensor(sid))
+        e.end_slice(sid, want_report=True)
+    t0 = time.perf_counter()
+    row = e.export_row(1, 2)
+    t_export = time.perf_counter() - t0
+    assert row.nbytes == (1 << 24) * 1024 and int(row.max()) <= 15
+    assert int(np.count_nonzero(row < cfg.window)) == int(e.row_active()[1])
+    row[::4096] = 3
+    t0 = time.perf_counter()
+    e.import_row(1, 2, row)
+    t_import = time.perf_counter() - t0
+    back = e.export_row(1, 2)
+    assert np.array_equal(back, row)
+    assert int(e.row_active()[1]) == int(np.count_nonzero(row < cfg.window))
+    print(f"16 GiB row: export {t_export:.2f} s, import {t_import:.2f} s")

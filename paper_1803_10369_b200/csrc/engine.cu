@@ -853,8 +853,18 @@ struct Engine {
         timing.apply_entries += fine_pending;
         if (epoch) {
             if (fine_pending) {
+                // sparse slices warp by warp in place, dense ones through shared memory
+                static const uint32_t sparse_max = [] { const char* v = std::getenv("SRLA_STAMP_SPARSE"); return v ? static_cast<uint32_t>(std::atoi(v)) : 512u; }();
+                const uint32_t sp = cfg.rows <= kStampWarpRows && lin_words % 4 == 0 ? sparse_max : 0u;
+                if (sp) {
+                    k_stamp_warp<<<sms * 8, 256, 0, st>>>(static_cast<uint8_t*>(d_lin), lin_words, fcfg, sp, cur_epoch,
+                                                         cfg.window, cfg.rows, hist.p);
+                    check_launch();
+                    launched();
+                }
                 k_slice_stamp<<<std::min<uint32_t>(fcfg.nfine, sms * 3), 256, 2u << fcfg.shift, st>>>(
-                    static_cast<uint8_t*>(d_lin), total, lin_words, fcfg, 0, bulk_ok ? 1 : 0, cur_epoch, cfg.window, hist.p);
+                    static_cast<uint8_t*>(d_lin), total, lin_words, fcfg, 0, bulk_ok ? 1 : 0, cur_epoch, cfg.window, hist.p,
+                    sp);
                 check_launch();
                 launched();
                 timer_stop(t_apply, kTimeApply);

@@ -45,7 +45,8 @@ __device__ __forceinline__ uint32_t stamp_byte_shared(uint8_t* base, uint32_t of
 // multiple) goes through shared memory with plain loads.
 __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, uint64_t total_words,
                                                      uint64_t row_words, FineCfg f, uint32_t f_begin, int bulk,
-                                                     uint32_t cur, uint32_t k, unsigned long long* __restrict__ hist) {
+                                                     uint32_t cur, uint32_t k, unsigned long long* __restrict__ hist,
+                                                     uint32_t sparse_max) {
     extern __shared__ __align__(128) uint8_t s_raw[];
     __shared__ __align__(8) uint64_t s_bar[2];
     // per row of the slice (a slice spans at most two rows): net transitions
@@ -56,9 +57,21 @@ __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, 
     const uint32_t slice_bytes = 1u << f.shift;
     const uint32_t cs = f.shift > 15 ? f.shift - 5 : min(10u, f.shift);  // piece = 2^cs bytes, <= 32 per slice
     uint8_t* buf[2] = {s_raw, s_raw + slice_bytes};
+    // next slice of this block (from, from + gridDim.x, ...) with more than
+    // sparse_max marks (the rest is k_stamp_warp's): the block tests 256
+    // candidates at a time (block-uniform call)
+    __shared__ uint32_t s_next;
     auto next_slice = [&](uint32_t from) -> uint32_t {
-        for (uint32_t fb = from; fb < f.nfine; fb += gridDim.x)
-            if (f.count[fb] != 0) return fb;
+        for (uint64_t base = from; base < f.nfine; base += static_cast<uint64_t>(blockDim.x) * gridDim.x) {
+            if (threadIdx.x == 0) s_next = 0xFFFFFFFFu;
+            __syncthreads();
+            const uint64_t fb = base + static_cast<uint64_t>(threadIdx.x) * gridDim.x;
+            if (fb < f.nfine && f.count[fb] > sparse_max) atomicMin(&s_next, static_cast<uint32_t>(fb));
+            __syncthreads();
+            const uint32_t r = s_next;
+            __syncthreads();
+            if (r != 0xFFFFFFFFu) return r;
+        }
         return f.nfine;
     };
     auto slice_len = [&](uint32_t fb) {
@@ -171,6 +184,73 @@ __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, 
         bulk_cur = bulk_nxt;
     }
     if (tid == 0) bulk_wait_all();
+}
+
+// Sparse slices (at most sparse_max marks; C3's 2^24-column table has ~200
+// per 32 KB slice, clustered on the active sources' cells): one WARP per
+// slice stamps in place in global memory, no shared-memory staging and no
+// block barriers — the block-per-slice kernel above is bound by its
+// per-slice fixed cost there. Each mark is a CAS on its 32-bit word; the
+// histogram deltas accumulate per warp by (row, age) and are flushed at the
+// end.
+constexpr int kStampWarpRows = 4;  // binned tables have <= kBinRows rows
+__global__ void __launch_bounds__(256) k_stamp_warp(uint8_t* __restrict__ lin, uint64_t row_words, FineCfg f,
+                                                    uint32_t sparse_max, uint32_t cur, uint32_t k, uint32_t rows,
+                                                    unsigned long long* __restrict__ hist) {
+    __shared__ int32_t s_h[8][kStampWarpRows][128];  // per warp: net transitions by (row, age)
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    for (uint32_t q = lane; q < kStampWarpRows * 128; q += 32) (&s_h[warp][0][0])[q] = 0;
+    __syncwarp();
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t fb = blockIdx.x * (blockDim.x >> 5) + warp; fb < f.nfine; fb += nwarps) {
+        const uint32_t n = min(f.count[fb], f.cap);
+        if (n == 0 || n > sparse_max) continue;
+        const uint16_t* e = f.bins + static_cast<uint64_t>(fb) * f.cap;
+        const uint64_t w0 = static_cast<uint64_t>(fb) << f.shift;
+        const uint32_t row_a = static_cast<uint32_t>(w0 / row_words);
+        const uint64_t split = (static_cast<uint64_t>(row_a) + 1) * row_words - w0;  // offsets >= split: next row
+        unsigned int* g = reinterpret_cast<unsigned int*>(lin + w0);
+        // four marks per lane in flight: load the words, then CAS each
+        // (exact under duplicates: the loser of a same-recorder race re-reads
+        // `cur` and records nothing)
+        constexpr int kU = 4;
+        for (uint32_t q0 = 0; q0 < n; q0 += 32 * kU) {
+            uint32_t off[kU], wv[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const uint32_t q = q0 + lane + 32u * u;
+                off[u] = q < n ? static_cast<uint32_t>(e[q]) : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) wv[u] = off[u] != 0xFFFFFFFFu ? __ldcg(g + (off[u] >> 2)) : 0u;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (off[u] == 0xFFFFFFFFu) continue;
+                const uint32_t sh = 8u * (off[u] & 3u);
+                unsigned int assumed, cur_w = wv[u];
+                uint32_t old;
+                for (;;) {
+                    old = (cur_w >> sh) & 0xFFu;
+                    if (old == cur) break;
+                    assumed = cur_w;
+                    cur_w = atomicCAS(g + (off[u] >> 2), assumed, (assumed & ~(0xFFu << sh)) | (cur << sh));
+                    if (cur_w == assumed) break;
+                }
+                if (old != cur) {
+                    const uint32_t h = row_a + (off[u] >= split ? 1u : 0u);
+                    const uint32_t age = (cur - old) & 0xFFu;
+                    if (age < k) atomicSub(&s_h[warp][h & 3u][age], 1);
+                    atomicAdd(&s_h[warp][h & 3u][0], 1);
+                }
+            }
+        }
+    }
+    __syncwarp();
+    for (uint32_t q = lane; q < rows * k; q += 32) {
+        const uint32_t h = q / k, age = q % k;
+        const int32_t v = s_h[warp][h][age];
+        if (v) atomicAdd(hist + h * 256ull + ((cur - age) & 0xFFu), static_cast<unsigned long long>(static_cast<long long>(v)));
+    }
 }
 
 // Sweep [w0, w0+n) of the table: stamps with age >= expired become age

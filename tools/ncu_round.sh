@@ -20,6 +20,6 @@ if [ "$W" != "c3" ]; then
 fi
 if [ "$W" != "c2" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv $B --workload c3 > $O/launches_c3.log 2>&1
-  for k in k_scan_bin k_split k_slice_stamp k_union_linear_epoch; do cap c3 $k; done
+  for k in k_scan_bin k_split k_stamp_warp k_union_linear_epoch; do cap c3 $k; done
 fi
 ls -la $O

@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_table import rows  # noqa: E402
 
 NAMES = [("k_scan_bin", "k_scan_bin"), ("k_split", "k_split"), ("k_slice_apply", "k_slice_apply"),
-         ("k_slice_stamp", "k_slice_apply"), ("k_union_linear", "k_union_linear"), ("k_scan<", "k_scan")]
+         ("k_slice_stamp", "k_slice_apply"), ("k_stamp_warp", "k_slice_apply"), ("k_union_linear", "k_union_linear"), ("k_scan<", "k_scan")]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 TSCALE = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3, "s": 1e3}
 

@@ -1711,7 +1711,12 @@ struct Engine {
         eos_mark("start");
         join_maint();
         stats.slides++;
-        slide_begin();
+        // the candidate re-validation reads only the rough table: with a
+        // streamed apply in this end-of-slice it starts after the apply
+        // (overlapping the gather) instead of competing with it
+        static const bool retain_late = [] { const char* v = std::getenv("SRLA_RETAIN_LATE"); return !(v && v[0] == '0'); }();
+        const bool late = retain_late && !epoch && use_bins && due && dc.k < dc.expired;
+        if (!late) slide_begin();
         eos_mark("begin");
         const auto w0 = std::chrono::steady_clock::now();
         bool age_linear = false, finished = false;
@@ -1730,6 +1735,7 @@ struct Engine {
             d_counts.ensure(cfg.rows);
             CK(cudaMemsetAsync(d_counts.p, 0, cfg.rows * sizeof(unsigned long long), st));
             flush_linear(2);
+            if (late) slide_begin();
             trace("eos: split+apply+count+age");
             report(out, nullptr, true, compact, finish);
             trace("eos: report");

@@ -620,7 +620,11 @@ struct Engine {
         const bool small = total_words * wb < (256ull << 20);
         if (!forced && small) return false;
         uint32_t shift = 0;
-        while (lin_bytes(1ull << (shift + 1)) <= (32ull << 20)) ++shift;  // 32 MB coarse regions
+        // 16 MB coarse regions: K1's fan-out (regions per tile) against the
+        // split's (fine slices per region); measured best on C2 (8-64 MB swept)
+        uint64_t region_bytes = 16ull << 20;
+        if (const char* rm = std::getenv("SRLA_REGION_MB")) region_bytes = std::strtoull(rm, nullptr, 10) << 20;
+        while (lin_bytes(1ull << (shift + 1)) <= region_bytes) ++shift;
         if (forced)
             while (shift > 4 && (total_words >> shift) < 8) --shift;  // ~8 regions even for tiny tables
         while (((total_words + (1ull << shift) - 1) >> shift) > kMaxRegions) ++shift;

@@ -1086,7 +1086,8 @@ struct Engine {
         stats.first_crossings += Hn;
         hps.ensure(Hn);
         cub_call([&](void* t, size_t& b) {
-            return cub::DeviceRadixSort::SortKeys(t, b, hp.p, hps.p, static_cast<int>(Hn), 0, 64, st);
+            // by P alone (bits 32..): P (< kChunk) is distinct per host
+            return cub::DeviceRadixSort::SortKeys(t, b, hp.p, hps.p, static_cast<int>(Hn), 32, 32 + bit_length(kChunk - 1), st);
         });
 
         // K4: ordered indicator resolution

@@ -692,6 +692,11 @@ struct Engine {
             if (nib_apply_smem() > 200 * 1024) return false;  // two stages must fit in shared memory
             CK(cudaFuncSetAttribute(k_slice_apply_nib, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(nib_apply_smem())));
         }
+        with_w([&](auto w) {
+            using W = decltype(w);
+            CK(cudaFuncSetAttribute(k_scan_bin<W, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmem));
+            CK(cudaFuncSetAttribute(k_scan_bin<W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmem));
+        });
         // bulk (TMA) slices need 16-byte slices and rows at least one slice long
         const uint64_t slice_words = 1ull << fs;
         bulk_ok = lin_bytes(slice_words) % 16 == 0 && lin_bytes(lin_words) % 16 == 0 && lin_words >= slice_words;
@@ -960,10 +965,10 @@ struct Engine {
         CK(cudaEventRecord(t_scan0, sk));
         const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
         if (cfg.rows == 4)
-            k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, sk>>>(
+            k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, sk>>>(
                 d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
         else
-            k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, sk>>>(
+            k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, sk>>>(
                 d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
         CK(cudaGetLastError());
         CK(cudaEventRecord(t_scan1, sk));
@@ -1026,9 +1031,9 @@ struct Engine {
             if (use_bins && MAXR <= kBinRows) {
                 const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
                 if (cfg.rows == 4)
-                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
                 else
-                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 4), kBinThreads, 0, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             } else {
                 k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             }

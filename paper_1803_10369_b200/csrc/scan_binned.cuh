@@ -68,12 +68,13 @@ struct BinCfg {
     uint32_t* overflow;
 };
 
-constexpr int kBinThreads = 256;
+constexpr int kBinThreads = 512;
 constexpr int kBinPerThread = 4;                            // packets per thread per tile
 constexpr int kBinTile = kBinThreads * kBinPerThread;       // packets per tile
 constexpr int kBinRows = 4;                                 // rows handled by the binned path
 constexpr int kBinEntries = kBinTile * kBinRows;
 constexpr int kMaxRegions = 1024;
+constexpr int kBinSmem = kMaxRegions * 16 + kBinEntries * 6;  // k_scan_bin dynamic shared memory
 
 // Epoch-stamp mode of the linear table (epoch.cuh): marks write the current
 // epoch instead of 0 and keep per-row stamp histograms.
@@ -134,17 +135,20 @@ __device__ __forceinline__ void mark_word(W* base, uint32_t off) {
 // ROWS = 0 reads c.rows (<= kBinRows). Tiles where every thread has its four
 // records take a path without per-record liveness tests.
 template <typename W, int ROWS>
-__global__ void __launch_bounds__(kBinThreads, 4) k_scan_bin(const uint32_t* __restrict__ recs, uint32_t n, DevCfg c,
+__global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __restrict__ recs, uint32_t n, DevCfg c,
                                                          BinCfg b, EpochCfg ep, W* __restrict__ lin,
                                                          uint32_t* __restrict__ stamp, uint32_t* __restrict__ ev,
                                                          uint32_t ev_cap, uint32_t* __restrict__ ev_count, int vec) {
-    __shared__ uint32_t s_cnt[kMaxRegions];
-    __shared__ uint32_t s_lbase[kMaxRegions];
-    // per region: {bin slot of staging entry idx = x + idx (mod 2^32; nregions * cap < 2^32),
-    //              first staging index that no longer fits the region's bin}
-    __shared__ uint2 s_win[kMaxRegions];
-    __shared__ uint32_t s_off[kBinEntries];
-    __shared__ uint16_t s_reg[kBinEntries];
+    // dynamic shared memory (kBinSmem bytes):
+    //   win[kMaxRegions] (uint2) | cnt | lbase | off[kBinEntries] | reg[kBinEntries] (u16)
+    // win: per region {bin slot of staging entry idx = x + idx (mod 2^32; nregions * cap < 2^32),
+    //                  first staging index that no longer fits the region's bin}
+    extern __shared__ __align__(16) uint8_t s_bin_raw[];
+    uint2* s_win = reinterpret_cast<uint2*>(s_bin_raw);
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_win + kMaxRegions);
+    uint32_t* s_lbase = s_cnt + kMaxRegions;
+    uint32_t* s_off = s_lbase + kMaxRegions;
+    uint16_t* s_reg = reinterpret_cast<uint16_t*>(s_off + kBinEntries);
     __shared__ uint32_t s_warp[kBinThreads / 32];
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;

@@ -165,15 +165,19 @@ def kernel_rooflines(tm, step_ms_total, cfg, peak, peak_src, packets, steps, wor
             continue
         ach = byts / (kms * 1e-3) / 1e9
         nc = traffic.get(name) or {}
+        ncu = {k: nc[k] for k in ("dram_pct", "sm_pct", "warps_active_pct", "warp_inst") if k in nc} or None
+        if ncu and nc.get("ms"):
+            # instruction-issue roofline: warp instructions per second against
+            # 148 SMs x 4 schedulers x 1 warp-instruction per clock at the max SM clock
+            ncu["issue_frac"] = nc["warp_inst"] / (nc["ms"] * 1e-3) / (148 * 4 * 1.965e9)
         kernels[name] = {"ms_per_launch": kms / n, "launches": n, "algorithmic_bytes_per_launch": byts / n,
                          "achieved": ach, "frac": ach / peak, "share_of_step": kms / step_ms_total,
-                         "traffic": nc.get("dram_bytes_per_launch"),
-                         "ncu": {k: nc[k] for k in ("dram_pct", "sm_pct", "warps_active_pct", "warp_inst") if k in nc}
-                         or None}
+                         "traffic": nc.get("dram_bytes_per_launch"), "ncu": ncu}
     dom = max(kernels, key=lambda k: kernels[k]["share_of_step"])
     d = kernels[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": d["achieved"], "peak": peak, "unit": "GB/s",
                 "frac": d["frac"], "traffic": d["traffic"], "peak_source": peak_src,
+                "issue_frac": (d["ncu"] or {}).get("issue_frac"),
                 "algorithmic_bytes_per_launch": d["algorithmic_bytes_per_launch"],
                 "ms_per_launch": d["ms_per_launch"], "share_of_step": d["share_of_step"]}
     path_ms = sum(ks[k][0] for k in ks if k != "k_union_linear")

@@ -265,11 +265,19 @@ def run_engine(args):
     from paper_1803_10369_b200 import srla
 
     rank, world, local = env_rank()
+    # one process per GPU; SRLA_BENCH_BACKEND=gloo lets several ranks share a
+    # GPU to exercise the N > 1 path on a one-GPU box (timings then contend)
+    backend = os.environ.get("SRLA_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    comm_dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     cols = args.cols if args.cols else (1 << 24 if args.workload == "c3" else 1 << 20)
     cfg = srla.SeaConfig(**sketch_cfg(cols))
     n_per_gpu = args.packets
@@ -305,18 +313,20 @@ def run_engine(args):
     from paper_1803_10369_b200.shard import allgather_report as _allgather
 
     def allgather_report(entries):
-        return entries if world == 1 else _allgather(entries, dist, torch.device("cuda", local))
+        return entries if world == 1 else _allgather(entries, dist, comm_dev if backend == "nccl" else None)
 
     def step(sid):
         eng.scan(slices[sid % nres])
         n, nr = _end_slice(eng, sid, rep_buf)
         if world > 1:
-            if args.handoff == "compact":  # rebuild entries for the all-gather
-                ent = np.zeros(n, srla.ENTRY_DTYPE)
-                ent["host"], ent["union_weight"] = comp_hosts[:n], comp_w[:n]
-                ent["estimate"] = comp_est[comp_w[:n]]
-                ent["has_estimate"], ent["is_super"] = comp_flags[comp_w[:n]] & 1, comp_flags[comp_w[:n]] >> 1
-                return allgather_report(ent), n
+            if args.handoff == "compact":  # (host, weight) words + this shard's Eq. 9 table, merged on the device
+                from paper_1803_10369_b200.shard import allgather_report_compact
+                h = torch.from_numpy(comp_hosts[:n].view(np.int32)).to(comm_dev, non_blocking=True)
+                w = torch.from_numpy(comp_w[:n].view(np.int32)).to(comm_dev, non_blocking=True)
+                mask = 0xFFFFFFFF
+                return allgather_report_compact(h.to(torch.int64) & mask, w.to(torch.int64) & mask,
+                                                torch.from_numpy(comp_est).to(comm_dev),
+                                                torch.from_numpy(comp_flags).to(comm_dev), dist), n
             return allgather_report(rep_buf[:n]), n
         return None, n
 
@@ -410,7 +420,7 @@ def run_engine(args):
     ms = t_start.elapsed_time(t_end)
     tm = eng.timing()
     st1 = eng.stats()
-    pk = torch.tensor([float(st1["packets"] - st0["packets"]), ms], dtype=torch.float64, device="cuda")
+    pk = torch.tensor([float(st1["packets"] - st0["packets"]), ms], dtype=torch.float64, device=comm_dev)
     if dist:
         tot = pk[:1].clone()
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
@@ -457,7 +467,7 @@ def run_engine(args):
             dist.barrier()
         el = time.perf_counter() - t0
         if dist:
-            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            t = torch.tensor([el], dtype=torch.float64, device=comm_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = t.item()
         e2e = {"value": packets / el, "unit": "packets/s", "h2d_bytes_per_step": int(h2d),

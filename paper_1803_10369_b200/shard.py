@@ -92,3 +92,41 @@ class ShardedPipeline:
         if report is None:
             return None
         return allgather_report(report, self.dist, self.device) if self.dist else merge_reports([report])
+
+
+def allgather_report_compact(hosts, weights, est_lut, flag_lut, dist):
+    """Device-resident report all-gather for the bench's N-GPU path.
+
+    hosts, weights: this rank's report (ascending hosts) as 1-D tensors on the
+    collective's device; est_lut (float64) and flag_lut (uint8: bit 0
+    has_estimate, bit 1 is_super) this shard's Eq. 9 table over the g'+1
+    weights (each shard has its own fill product). Returns the merged report
+    (hosts ascending) as device tensors (host, weight, estimate, flags) — one
+    all-gather of 8-byte (host, weight) words plus the tables, a merge on the
+    device, nothing back to the host."""
+    import torch
+    world = dist.get_world_size()
+    dev = hosts.device
+    n = torch.tensor([hosts.numel()], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n)
+    counts = [int(c.item()) for c in counts]
+    mx = max(counts + [1])
+    word = torch.zeros(mx, dtype=torch.int64, device=dev)
+    word[: hosts.numel()] = (hosts.to(torch.int64) << 32) | weights.to(torch.int64)
+    words = [torch.empty_like(word) for _ in range(world)]
+    dist.all_gather(words, word)
+    luts = [torch.empty_like(est_lut) for _ in range(world)]
+    dist.all_gather(luts, est_lut)
+    flags = [torch.empty_like(flag_lut) for _ in range(world)]
+    dist.all_gather(flags, flag_lut)
+    # shards own disjoint hosts: the merged order is a sort by host
+    allw = torch.cat([w[:c] for w, c in zip(words, counts)])
+    shard = torch.cat([torch.full((c,), r, dtype=torch.int64, device=dev) for r, c in enumerate(counts)])
+    host = (allw >> 32) & 0xFFFFFFFF  # int64 words: undo the sign of hosts >= 2^31
+    order = torch.argsort(host)
+    host, weight, shard = host[order], (allw & 0xFFFFFFFF)[order], shard[order]
+    L = est_lut.numel()
+    est = torch.stack(luts).reshape(-1)[shard * L + weight]
+    flg = torch.stack(flags).reshape(-1)[shard * L + weight]
+    return host, weight, est, flg

@@ -93,3 +93,42 @@ def test_two_rank_gloo_sharded_reports(oracle):
             else:
                 assert np.array_equal(g, want), f"slice {s} rank {r}"
     assert any(x is not None and len(x) for x in got[0])
+
+
+def _compact_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    from paper_1803_10369_b200.shard import allgather_report_compact, merge_reports
+    from paper_1803_10369_b200.srla import ENTRY_DTYPE
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(10 + rank)
+    L = 65
+    est = rng.random(L) * 1000
+    flg = rng.integers(0, 4, L).astype(np.uint8)
+    hosts = np.sort(rng.choice(2**31, 500 + 100 * rank, replace=False).astype(np.uint32) * 2 + rank)  # disjoint
+    w = rng.integers(0, L, len(hosts)).astype(np.uint32)
+    ent = np.zeros(len(hosts), ENTRY_DTYPE)
+    ent["host"], ent["union_weight"], ent["estimate"] = hosts, w, est[w]
+    ent["has_estimate"], ent["is_super"] = flg[w] & 1, flg[w] >> 1
+    h, wt, e, f = allgather_report_compact(torch.from_numpy(hosts.astype(np.int64)), torch.from_numpy(w.astype(np.int64)),
+                                           torch.from_numpy(est), torch.from_numpy(flg), dist)
+    parts = [None] * world
+    dist.all_gather_object(parts, ent)
+    want = merge_reports(parts)
+    ok = (np.array_equal(h.numpy(), want["host"].astype(np.int64)) and np.array_equal(wt.numpy(), want["union_weight"])
+          and np.array_equal(e.numpy(), want["estimate"]) and np.array_equal(f.numpy() & 1, want["has_estimate"])
+          and np.array_equal(f.numpy() >> 1, want["is_super"]))
+    open(os.path.join(out_dir, f"ok{rank}"), "w").write("1" if ok else "0")
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_compact_report_allgather():
+    """The bench's device-resident report all-gather (hosts + weights + each
+    shard's Eq. 9 table, merged by host) equals the entry-level merge."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_compact_worker, args=(2, port, d), nprocs=2, join=True)
+        assert open(os.path.join(d, "ok0")).read() == "1" and open(os.path.join(d, "ok1")).read() == "1"

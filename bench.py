@@ -310,10 +310,10 @@ def run_engine(args):
 
     rep_buf = pinned_entries(rep_cap)
 
-    from paper_1803_10369_b200.shard import allgather_report as _allgather
+    from paper_1803_10369_b200.shard import allgather_report_entries as _allgather_dev
 
-    def allgather_report(entries):
-        return entries if world == 1 else _allgather(entries, dist, comm_dev if backend == "nccl" else None)
+    def allgather_report(entries):  # merged on the device (N > 1)
+        return entries if world == 1 else _allgather_dev(entries, dist, comm_dev)
 
     def step(sid):
         eng.scan(slices[sid % nres])

@@ -130,3 +130,26 @@ def allgather_report_compact(hosts, weights, est_lut, flag_lut, dist):
     est = torch.stack(luts).reshape(-1)[shard * L + weight]
     flg = torch.stack(flags).reshape(-1)[shard * L + weight]
     return host, weight, est, flg
+
+
+def allgather_report_entries(entries: np.ndarray, dist, device):
+    """allgather_report with the merge on the device: this rank's srla_entry
+    array (24 bytes each, hosts ascending) is gathered from every rank and
+    merged by host on `device`; returns the merged entries as a (n, 24)
+    uint8 tensor on `device` (nothing copied back to the host)."""
+    import torch
+    world = dist.get_world_size()
+    entries = np.ascontiguousarray(entries, dtype=ENTRY_DTYPE)
+    n = torch.tensor([len(entries)], dtype=torch.int64, device=device)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n)
+    counts = [int(c.item()) for c in counts]
+    mx = max(counts + [1])
+    rows = torch.zeros((mx, ENTRY_DTYPE.itemsize), dtype=torch.uint8, device=device)
+    if len(entries):
+        rows[: len(entries)] = torch.from_numpy(entries.view(np.uint8).reshape(-1, ENTRY_DTYPE.itemsize)).to(device)
+    outs = [torch.empty_like(rows) for _ in range(world)]
+    dist.all_gather(outs, rows)
+    merged = torch.cat([o[:c] for o, c in zip(outs, counts)])
+    host = merged[:, :4].contiguous().view(torch.int32).reshape(-1).to(torch.int64) & 0xFFFFFFFF
+    return merged[torch.argsort(host)]

@@ -116,9 +116,12 @@ def _compact_worker(rank, world, port, out_dir):
     parts = [None] * world
     dist.all_gather_object(parts, ent)
     want = merge_reports(parts)
+    from paper_1803_10369_b200.shard import allgather_report_entries
+    dev_rows = allgather_report_entries(ent, dist, torch.device("cpu"))
+    ok_rows = dev_rows.numpy().tobytes() == want.tobytes()
     ok = (np.array_equal(h.numpy(), want["host"].astype(np.int64)) and np.array_equal(wt.numpy(), want["union_weight"])
           and np.array_equal(e.numpy(), want["estimate"]) and np.array_equal(f.numpy() & 1, want["has_estimate"])
-          and np.array_equal(f.numpy() >> 1, want["is_super"]))
+          and np.array_equal(f.numpy() >> 1, want["is_super"]) and ok_rows)
     open(os.path.join(out_dir, f"ok{rank}"), "w").write("1" if ok else "0")
     dist.destroy_process_group()
 

@@ -688,6 +688,8 @@ struct Engine {
             CK(cudaFuncSetAttribute(k_slice_apply<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(smem, 16)));
             CK(cudaFuncSetAttribute(k_slice_apply_bulk<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(2 * smem, 32)));
         });
+        CK(cudaFuncSetAttribute(k_stamp_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(stamp_claim_bytes(fs))));
         if (nib) {
             if (nib_apply_smem() > 200 * 1024) return false;  // two stages must fit in shared memory
             CK(cudaFuncSetAttribute(k_slice_apply_nib, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(nib_apply_smem())));
@@ -863,10 +865,10 @@ struct Engine {
         if (epoch) {
             if (fine_pending) {
                 // sparse slices warp by warp in place, dense ones through shared memory
-                static const uint32_t sparse_max = [] { const char* v = std::getenv("SRLA_STAMP_SPARSE"); return v ? static_cast<uint32_t>(std::atoi(v)) : 512u; }();
+                static const uint32_t sparse_max = [] { const char* v = std::getenv("SRLA_STAMP_SPARSE"); return v ? static_cast<uint32_t>(std::atoi(v)) : 1024u; }();
                 const uint32_t sp = cfg.rows <= kStampWarpRows && lin_words % 4 == 0 ? sparse_max : 0u;
                 if (sp) {
-                    k_stamp_warp<<<sms * 8, 256, 0, st>>>(static_cast<uint8_t*>(d_lin), lin_words, fcfg, sp, cur_epoch,
+                    k_stamp_warp<<<sms * 5, 256, stamp_claim_bytes(fcfg.shift), st>>>(static_cast<uint8_t*>(d_lin), lin_words, fcfg, sp, cur_epoch,
                                                          cfg.window, cfg.rows, hist.p);
                     check_launch();
                     launched();

@@ -188,67 +188,108 @@ __global__ void __launch_bounds__(256) k_slice_stamp(uint8_t* __restrict__ lin, 
 
 // Sparse slices (at most sparse_max marks; C3's 2^24-column table has ~200
 // per 32 KB slice, clustered on the active sources' cells): one WARP per
-// slice stamps in place in global memory, no shared-memory staging and no
-// block barriers — the block-per-slice kernel above is bound by its
-// per-slice fixed cost there. Each mark is a CAS on its 32-bit word; the
-// histogram deltas accumulate per warp by (row, age) and are flushed at the
-// end.
+// slice stamps in place in global memory, no shared-memory staging of the
+// slice and no block barriers — the block-per-slice kernel above is bound by
+// its per-slice fixed cost there. The warp owns its slice, so no global
+// atomics are needed: a per-warp shared bitmap (one bit per recorder of the
+// slice, claimed with a shared atomicOr) elects one lane per distinct
+// recorder, which loads the stamp and stores `cur` with plain byte accesses;
+// eight marks per lane are in flight. The histogram deltas accumulate per
+// block by (row, age) and are flushed at the end. Dynamic shared memory:
+// 8 warps x 2^(shift-3) bytes of bitmap.
 constexpr int kStampWarpRows = 4;  // binned tables have <= kBinRows rows
-__global__ void __launch_bounds__(256) k_stamp_warp(uint8_t* __restrict__ lin, uint64_t row_words, FineCfg f,
+inline uint32_t stamp_claim_words(uint32_t shift) { return ((1u << shift) + 31u) >> 5; }
+inline uint32_t stamp_claim_bytes(uint32_t shift) { return 8u * 4u * stamp_claim_words(shift); }
+__global__ void __launch_bounds__(256, 5) k_stamp_warp(uint8_t* __restrict__ lin, uint64_t row_words, FineCfg f,
                                                     uint32_t sparse_max, uint32_t cur, uint32_t k, uint32_t rows,
                                                     unsigned long long* __restrict__ hist) {
-    __shared__ int32_t s_h[8][kStampWarpRows][128];  // per warp: net transitions by (row, age)
+    __shared__ int32_t s_h[kStampWarpRows][128];  // net transitions by (row, age)
+    extern __shared__ uint32_t s_claim[];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    for (uint32_t q = lane; q < kStampWarpRows * 128; q += 32) (&s_h[warp][0][0])[q] = 0;
-    __syncwarp();
+    const uint32_t bwords = ((1u << f.shift) + 31u) >> 5;
+    uint32_t* claim = s_claim + warp * bwords;
+    for (uint32_t q = threadIdx.x; q < kStampWarpRows * 128; q += blockDim.x) (&s_h[0][0])[q] = 0;
+    for (uint32_t q = lane; q < bwords; q += 32) claim[q] = 0;
+    __syncthreads();
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    constexpr int kU = 8;
+    // software pipeline: the next slice's count and first 32*kU marks load
+    // while this slice's stamps are read and written (the marks past the
+    // count are never used; every read stays inside the slice's bin)
+    uint32_t pre_n = 0, pre[kU / 2];  // two u16 marks per register
+    auto prefetch = [&](uint32_t fb) {
+        if (fb >= f.nfine) return;
+        const uint16_t* e = f.bins + static_cast<uint64_t>(fb) * f.cap;
+        pre_n = __ldg(f.count + fb);
+#pragma unroll
+        for (int u = 0; u < kU; u += 2) {
+            const uint32_t lo = lane + 32u * u < f.cap ? __ldg(e + lane + 32u * u) : 0u;
+            const uint32_t hi = lane + 32u * (u + 1) < f.cap ? __ldg(e + lane + 32u * (u + 1)) : 0u;
+            pre[u / 2] = lo | (hi << 16);
+        }
+    };
+    prefetch(blockIdx.x * (blockDim.x >> 5) + warp);
     for (uint32_t fb = blockIdx.x * (blockDim.x >> 5) + warp; fb < f.nfine; fb += nwarps) {
-        const uint32_t n = min(f.count[fb], f.cap);
+        const uint32_t n = min(pre_n, f.cap);
+        uint32_t first[kU / 2];
+#pragma unroll
+        for (int u = 0; u < kU / 2; ++u) first[u] = pre[u];
+        prefetch(fb + nwarps);
         if (n == 0 || n > sparse_max) continue;
         const uint16_t* e = f.bins + static_cast<uint64_t>(fb) * f.cap;
         const uint64_t w0 = static_cast<uint64_t>(fb) << f.shift;
         const uint32_t row_a = static_cast<uint32_t>(w0 / row_words);
         const uint64_t split = (static_cast<uint64_t>(row_a) + 1) * row_words - w0;  // offsets >= split: next row
-        unsigned int* g = reinterpret_cast<unsigned int*>(lin + w0);
-        // four marks per lane in flight: load the words, then CAS each
-        // (exact under duplicates: the loser of a same-recorder race re-reads
-        // `cur` and records nothing)
-        constexpr int kU = 4;
+        uint8_t* g = lin + w0;
+        uint32_t fresh_a = 0, fresh_b = 0;  // transitions onto `cur` in rows row_a, row_a + 1
         for (uint32_t q0 = 0; q0 < n; q0 += 32 * kU) {
-            uint32_t off[kU], wv[kU];
+            uint32_t off[kU], old[kU];
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 const uint32_t q = q0 + lane + 32u * u;
-                off[u] = q < n ? static_cast<uint32_t>(e[q]) : 0xFFFFFFFFu;
+                off[u] = q < n ? (q0 ? static_cast<uint32_t>(e[q]) : (first[u / 2] >> (16 * (u & 1))) & 0xFFFFu) : 0xFFFFFFFFu;
             }
-#pragma unroll
-            for (int u = 0; u < kU; ++u) wv[u] = off[u] != 0xFFFFFFFFu ? __ldcg(g + (off[u] >> 2)) : 0u;
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 if (off[u] == 0xFFFFFFFFu) continue;
-                const uint32_t sh = 8u * (off[u] & 3u);
-                unsigned int assumed, cur_w = wv[u];
-                uint32_t old;
-                for (;;) {
-                    old = (cur_w >> sh) & 0xFFu;
-                    if (old == cur) break;
-                    assumed = cur_w;
-                    cur_w = atomicCAS(g + (off[u] >> 2), assumed, (assumed & ~(0xFFu << sh)) | (cur << sh));
-                    if (cur_w == assumed) break;
+                const uint32_t m = 1u << (off[u] & 31u);
+                if (atomicOr(&claim[off[u] >> 5], m) & m) off[u] = 0xFFFFFFFFu;  // a duplicate: another lane has it
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) old[u] = off[u] != 0xFFFFFFFFu ? __ldcg(g + off[u]) : cur;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                // a recorder leaving age `age` < k: one shared atomic per
+                // distinct (row, age) of the warp (a block-wide hot spot
+                // otherwise)
+                uint32_t key = 0xFFFFFFFFu;
+                if (old[u] != cur) {
+                    g[off[u]] = static_cast<uint8_t>(cur);
+                    const uint32_t second = off[u] >= split ? 1u : 0u;
+                    fresh_a += second ^ 1u;
+                    fresh_b += second;
+                    const uint32_t age = (cur - old[u]) & 0xFFu;
+                    if (age < k) key = ((row_a + second) << 8) | age;
                 }
-                if (old != cur) {
-                    const uint32_t h = row_a + (off[u] >= split ? 1u : 0u);
-                    const uint32_t age = (cur - old) & 0xFFu;
-                    if (age < k) atomicSub(&s_h[warp][h & 3u][age], 1);
-                    atomicAdd(&s_h[warp][h & 3u][0], 1);
-                }
+                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
+                if (key != 0xFFFFFFFFu && lane == __ffs(peers) - 1u)
+                    atomicSub(&s_h[(key >> 8) & 3u][key & 0xFFu], __popc(peers));
             }
         }
+        fresh_a = __reduce_add_sync(0xFFFFFFFFu, fresh_a);
+        fresh_b = __reduce_add_sync(0xFFFFFFFFu, fresh_b);
+        if (lane == 0) {
+            if (fresh_a) atomicAdd(&s_h[row_a & 3u][0], static_cast<int32_t>(fresh_a));
+            if (fresh_b) atomicAdd(&s_h[(row_a + 1u) & 3u][0], static_cast<int32_t>(fresh_b));
+        }
+        __syncwarp();
+        for (uint32_t q = lane; q < n; q += 32) claim[static_cast<uint32_t>(e[q]) >> 5] = 0;
+        __syncwarp();
     }
-    __syncwarp();
-    for (uint32_t q = lane; q < rows * k; q += 32) {
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < rows * k; q += blockDim.x) {
         const uint32_t h = q / k, age = q % k;
-        const int32_t v = s_h[warp][h][age];
+        const int32_t v = s_h[h][age];
         if (v) atomicAdd(hist + h * 256ull + ((cur - age) & 0xFFu), static_cast<unsigned long long>(static_cast<long long>(v)));
     }
 }

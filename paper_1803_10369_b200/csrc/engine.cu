@@ -203,6 +203,7 @@ struct Engine {
 
     // epoch-stamp linear table (epoch.cuh): u8 stamps, O(1) slide
     bool epoch = false;
+    uint32_t stamp_sparse_max = 1024;  // SRLA_STAMP_SPARSE, read per engine at setup
     uint32_t cur_epoch = 0;
     DevBuf<unsigned long long> hist;  // rows x 256
     PinBuf<unsigned long long> pin_hist;
@@ -688,6 +689,7 @@ struct Engine {
             CK(cudaFuncSetAttribute(k_slice_apply<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(smem, 16)));
             CK(cudaFuncSetAttribute(k_slice_apply_bulk<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(2 * smem, 32)));
         });
+        if (const char* v = std::getenv("SRLA_STAMP_SPARSE")) stamp_sparse_max = static_cast<uint32_t>(std::atoi(v));
         CK(cudaFuncSetAttribute(k_stamp_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(stamp_claim_bytes(fs))));
         if (nib) {
@@ -865,7 +867,7 @@ struct Engine {
         if (epoch) {
             if (fine_pending) {
                 // sparse slices warp by warp in place, dense ones through shared memory
-                static const uint32_t sparse_max = [] { const char* v = std::getenv("SRLA_STAMP_SPARSE"); return v ? static_cast<uint32_t>(std::atoi(v)) : 1024u; }();
+                const uint32_t sparse_max = stamp_sparse_max;
                 const uint32_t sp = cfg.rows <= kStampWarpRows && lin_words % 4 == 0 ? sparse_max : 0u;
                 if (sp) {
                     k_stamp_warp<<<sms * 5, 256, stamp_claim_bytes(fcfg.shift), st>>>(static_cast<uint8_t*>(d_lin), lin_words, fcfg, sp, cur_epoch,

@@ -55,6 +55,24 @@ def test_binned_marks_match_reference_golden(gpu, oracle, name, epoch, monkeypat
     assert msg is None, msg
 
 
+@pytest.mark.parametrize("sparse", ["0", "1000000"])
+@pytest.mark.parametrize("name", ["contended", "drift_evict", "c1_shape"])
+def test_epoch_stamp_paths_match_reference_golden(gpu, oracle, name, sparse, monkeypatch):
+    """Epoch-stamp recorders with every fine slice forced through one of the
+    two stamp kernels: the block-per-slice shared-memory path
+    (SRLA_STAMP_SPARSE=0) or the warp-per-slice in-place path with its claim
+    bitmap (every slice counts as sparse)."""
+    monkeypatch.setenv("SRLA_FORCE_BINS", "1")
+    monkeypatch.setenv("SRLA_EPOCH", "1")
+    monkeypatch.setenv("SRLA_STAMP_SPARSE", sparse)
+    g = json.load(open(os.path.join(GOLD, f"{name}.json")))
+    cfg, _ = S.SCENARIOS[name]
+    slices = GF.scenario_slices(name, oracle)
+    got = GF.run_flow(GF.EngineBackend(engine(cfg)), cfg, slices)
+    msg = GF.compare(g["slices"], got)
+    assert msg is None, msg
+
+
 def _oracle_backend(oracle, cfg):
     b = GF.CheckerBackend.__new__(GF.CheckerBackend)
     from oracle.pyoracle import SeaConfig

@@ -184,6 +184,19 @@ srla_status srla_export_row(srla_engine* e, uint32_t row, int kind, void* buf, u
 srla_status srla_import_row(srla_engine* e, uint32_t row, int kind, const void* buf,
                             uint64_t bytes);
 
+/* Block digests of one raw row (indicator_row / rough_row / linear_row,
+ * sea.hpp:341-346) in the reference's little-endian byte layout, computed on
+ * the device: per 1 MiB block, the wrapping sum over its 8-byte words w_i
+ * (zero-padded) of avalanche64(w_i ^ avalanche64(i + 1)), i = the word's index
+ * in the row. Parity at 2^24 columns compares these against the reference's
+ * rows (oracle/ref_capi.cpp block_sums) instead of exporting 64 GiB per slice.
+ * out = NULL queries *n_blocks. */
+srla_status srla_state_blocks(srla_engine* e, uint32_t row, int kind, uint64_t* out, uint64_t cap,
+                              uint64_t* n_blocks);
+/* The same block sums over `bytes` of any device buffer (e.g. a record batch);
+ * `out` is host memory with room for ceil(bytes / 2^20) sums. */
+srla_status srla_block_sums(const void* d_buf, uint64_t bytes, uint64_t* out, uint64_t cap, void* stream);
+
 srla_status srla_stats_get(const srla_engine* e, srla_stats* out);
 
 /* Device time of the dominant kernel (K1 scan, CUDA events on the engine

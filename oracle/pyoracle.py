@@ -148,6 +148,21 @@ class Checker:
             "slice_bounds": (u64, [vp, u64, u32, vp]),
             "parse_srlt": (u64, [vp, u64, vp, C.POINTER(i32), C.POINTER(u64)]),
         }
+        if self.prefix == "ref":  # reference-only: parallel slice generator, record-order flow
+            sigs.update({
+                "generate_slice": (u64, [C.POINTER(OrcSpec), u64, u32, vp, C.c_char_p, C.c_size_t]),
+                "flow_create": (vp, [C.POINTER(OrcConfig), u32, C.c_char_p, C.c_size_t]),
+                "flow_destroy": (None, [vp]),
+                "flow_scan": (u64, [vp, vp, u64]),
+                "flow_pushes": (None, [vp, vp]),
+                "flow_ncand": (u64, [vp]),
+                "flow_candidates": (None, [vp, vp]),
+                "flow_report": (u64, [vp, u64, vp, vp, vp, vp, vp]),
+                "flow_slide": (u64, [vp]),
+                "flow_row_bytes": (u64, [vp, i32]),
+                "flow_state_blocks": (None, [vp, u32, i32, vp]),
+                "block_sums": (None, [vp, u64, u32, vp]),
+            })
         for name, (res, args) in sigs.items():
             fn = self.f(name)
             fn.restype = res
@@ -211,6 +226,45 @@ class Checker:
         if not h:
             raise ValueError(err.value.decode())
         return Pipeline(self, h, cfg)
+
+    @staticmethod
+    def _spec(spec: PlantSpec):
+        plants = (OrcPlant * max(1, len(spec.plants)))()
+        for i, p in enumerate(spec.plants):
+            plants[i] = OrcPlant(*p)
+        s = OrcSpec(spec.seed, spec.start_ts, spec.slice_seconds, spec.slices, spec.window,
+                    spec.a_base, spec.b_base, spec.a_hosts, spec.b_hosts, spec.pairs_per_slice,
+                    len(spec.plants), spec.skew, plants)
+        s._keep = plants
+        return s
+
+    def generate_slice(self, spec: PlantSpec, slice_id: int, threads: int = 0, out=None) -> np.ndarray:
+        """Slice `slice_id` of generate_trace built in parallel from the reference's
+        own generator pieces (ref_generate_slice; slice_seconds == 1)."""
+        s = self._spec(spec)
+        err = C.create_string_buffer(256)
+        n = self.f("generate_slice")(C.byref(s), slice_id, 0, None, err, 256)
+        if n == 0xFFFFFFFFFFFFFFFF:
+            raise ValueError(err.value.decode())
+        if out is None or len(out) < n:
+            out = np.empty((n, 3), np.uint32)
+        self.f("generate_slice")(C.byref(s), slice_id, threads or (os.cpu_count() or 1), _ptr(out), err, 256)
+        return out[:n]
+
+    def block_sums(self, buf, threads: int = 0) -> np.ndarray:
+        """Per-MiB block sums of a byte buffer (the state digest of srla_state_blocks)."""
+        b = np.ascontiguousarray(buf).view(np.uint8).reshape(-1)
+        out = np.empty(max(1, (len(b) + (1 << 20) - 1) >> 20), np.uint64)
+        self.f("block_sums")(_ptr(b), len(b), threads or (os.cpu_count() or 1), _ptr(out))
+        return out[: (len(b) + (1 << 20) - 1) >> 20]
+
+    def flow(self, cfg: SeaConfig, threads: int = 0) -> "Flow":
+        err = C.create_string_buffer(256)
+        c = self.config(cfg)
+        h = self.f("flow_create")(C.byref(c), threads or (os.cpu_count() or 1), err, 256)
+        if not h:
+            raise ValueError(err.value.decode())
+        return Flow(self, h, cfg)
 
     def generate(self, spec: PlantSpec) -> np.ndarray:
         plants = (OrcPlant * max(1, len(spec.plants)))()
@@ -374,3 +428,44 @@ class Pipeline:
     @property
     def estimate_ms(self):
         return self.chk.f("pipeline_estimate_ms")(self.h)
+
+
+class Flow:
+    """The reference sketch + CandidateList driven like DetectPipeline::process_slice
+    with ONE scan worker (record order, pipeline.hpp:110-139), bulk passes chunked
+    over threads (sea.hpp:23-26). Full-size parity source (ref_flow_*)."""
+
+    def __init__(self, chk: Checker, h, cfg: SeaConfig):
+        self.chk, self.h, self.cfg = chk, h, cfg
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.chk.f("flow_destroy")(self.h)
+            self.h = None
+
+    def scan(self, recs) -> np.ndarray:
+        recs = np.ascontiguousarray(recs, dtype=np.uint32).reshape(-1, 3)
+        n = self.chk.f("flow_scan")(self.h, _ptr(recs), len(recs))
+        out = np.empty(max(1, n), np.uint32)
+        self.chk.f("flow_pushes")(self.h, _ptr(out))
+        return out[:n]
+
+    def candidates(self) -> np.ndarray:
+        n = self.chk.f("flow_ncand")(self.h)
+        out = np.empty(max(1, n), np.uint32)
+        self.chk.f("flow_candidates")(self.h, _ptr(out))
+        return out[:n]
+
+    def report(self, window_start=0) -> dict:
+        out = _report_buffers(self.chk.f("flow_ncand")(self.h))
+        n = self.chk.f("flow_report")(self.h, window_start, *(_ptr(out[k]) for k in _REPORT_KEYS))
+        return {k: v[:n] for k, v in out.items()}
+
+    def slide(self) -> int:
+        return self.chk.f("flow_slide")(self.h)
+
+    def state_blocks(self, row, kind) -> np.ndarray:
+        nb = (self.chk.f("flow_row_bytes")(self.h, kind) + (1 << 20) - 1) >> 20
+        out = np.empty(max(1, nb), np.uint64)
+        self.chk.f("flow_state_blocks")(self.h, row, kind, _ptr(out))
+        return out[:nb]

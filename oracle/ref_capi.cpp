@@ -196,6 +196,109 @@ struct Pipe final : PipeBase {
 
 SeaBase* S(void* h) { return static_cast<SeaBase*>(h); }
 
+PlantSpec to_spec(const orc_spec* s) {
+    PlantSpec spec;
+    spec.seed = s->seed;
+    spec.start_ts = s->start_ts;
+    spec.slice_seconds = s->slice_seconds;
+    spec.slices = s->slices;
+    spec.window = s->window;
+    spec.a_base = s->a_base;
+    spec.b_base = s->b_base;
+    spec.background = {s->a_hosts, s->b_hosts, s->pairs_per_slice, s->skew};
+    for (uint32_t i = 0; i < s->n_plants; ++i)
+        spec.plants.push_back({s->plants[i].host, s->plants[i].cardinality, s->plants[i].first_slice,
+                               s->plants[i].last_slice});
+    return spec;
+}
+
+// Records the plants contribute to slice s (generator.hpp:127-139).
+uint64_t plant_records(const PlantSpec& spec, uint64_t s) {
+    uint64_t n = 0;
+    for (const auto& p : spec.plants) {
+        if (!p.active_in(s)) continue;
+        const uint32_t r = static_cast<uint32_t>((s - p.first_slice) % spec.window);
+        const auto [lo, hi] = detail::rotation_chunk(p.cardinality, spec.window, r);
+        n += hi - lo;
+    }
+    return n;
+}
+
+// Block digest of a little-endian byte row: per 1 MiB block, the wrapping sum
+// over its 8-byte words w (zero-padded) of avalanche64(w ^ avalanche64(i + 1)),
+// i = the word's index within the row. The engine computes the same sums on
+// the device (srla_state_blocks); tests compare sha256 over them.
+constexpr uint64_t kDigestBlock = 1ull << 20;
+
+void block_sums(const uint8_t* p, uint64_t bytes, uint32_t threads, uint64_t* out) {
+    const uint64_t nb = (bytes + kDigestBlock - 1) / kDigestBlock;
+    parallel_ranges(nb, std::max<uint32_t>(threads, 1), [&](uint64_t b0, uint64_t b1) {
+        for (uint64_t b = b0; b < b1; ++b) {
+            const uint64_t lo = b * kDigestBlock, hi = std::min(bytes, lo + kDigestBlock);
+            uint64_t acc = 0;
+            for (uint64_t o = lo; o < hi; o += 8) {
+                uint64_t w = 0;
+                std::memcpy(&w, p + o, std::min<uint64_t>(8, hi - o));
+                acc += avalanche64(w ^ avalanche64(o / 8 + 1));
+            }
+            out[b] = acc;
+        }
+    });
+}
+
+// One sketch + candidate list driven like DetectPipeline::process_slice with
+// ONE scan worker (pipeline.hpp:110-139: record order, the parity definition
+// of SURVEY.md §8c), its bulk passes (report_window's fill product, slide)
+// chunked over `threads` — ChunkRunner splits do not change results
+// (sea.hpp:23-26).
+struct FlowBase {
+    virtual ~FlowBase() = default;
+    virtual uint64_t scan(const uint32_t* recs, uint64_t n, std::vector<uint32_t>& pushes) = 0;
+    virtual const std::vector<uint32_t>& cands() = 0;
+    virtual uint64_t report(uint64_t window_start, uint32_t* hosts, uint32_t* weights, double* est, uint8_t* has,
+                            uint8_t* sup) = 0;
+    virtual uint64_t slide() = 0;
+    virtual void state_blocks(uint32_t row, int kind, uint64_t* out) = 0;
+    virtual uint64_t row_bytes(int kind) = 0;
+    std::vector<uint32_t> pushes;
+};
+
+template <RecorderWord W>
+struct Flow final : FlowBase {
+    EstimatorArray<W> a;
+    CandidateList csip;
+    uint32_t threads;
+    Flow(const SeaConfig& c, uint32_t t) : a(c), threads(t) {}
+    uint64_t scan(const uint32_t* recs, uint64_t n, std::vector<uint32_t>& sink) override {
+        sink.clear();
+        for (uint64_t r = 0; r < n; ++r) a.scan_ip_pair(recs[3 * r + 1], recs[3 * r + 2], sink);
+        for (uint32_t h : sink) csip.insert(h);
+        return sink.size();
+    }
+    const std::vector<uint32_t>& cands() override { return csip.hosts(); }
+    uint64_t report(uint64_t ws, uint32_t* hosts, uint32_t* weights, double* est, uint8_t* has,
+                    uint8_t* sup) override {
+        const auto r = a.report_window(csip, ws, chunked(threads));
+        if (hosts) put_report(r, hosts, weights, est, has, sup);
+        return r.entries.size();
+    }
+    uint64_t slide() override {
+        csip = a.slide(csip, chunked(threads));
+        return csip.size();
+    }
+    uint64_t row_bytes(int kind) override {
+        if (kind == ORC_INDICATOR) return a.indicator_row(0).size() * 2;
+        if (kind == ORC_ROUGH) return a.rough_row(0).size() * sizeof(W);
+        return a.linear_row(0).size() * sizeof(W);
+    }
+    void state_blocks(uint32_t row, int kind, uint64_t* out) override {
+        const uint8_t* p = kind == ORC_INDICATOR ? reinterpret_cast<const uint8_t*>(a.indicator_row(row).data())
+                           : kind == ORC_ROUGH   ? reinterpret_cast<const uint8_t*>(a.rough_row(row).data())
+                                                 : reinterpret_cast<const uint8_t*>(a.linear_row(row).data());
+        block_sums(p, row_bytes(kind), threads, out);  // x86: words already little-endian
+    }
+};
+
 }  // namespace
 
 extern "C" {
@@ -304,6 +407,101 @@ uint64_t ref_generate(const orc_spec* s, uint32_t* out, char* err, size_t errlen
         set_err(err, errlen, e.what());
         return UINT64_MAX;
     }
+}
+
+// Slice `slice` of generate_trace (generator.hpp:117-161), produced in
+// parallel from the reference's own SplitMix64 / ZipfSampler / rotation
+// helpers. The generator's draws are counter-based (hash.hpp:21-24: state +=
+// phi per draw) and fixed per record (plant record: ts; background record:
+// src, dst, ts), so record j of a slice starts at a known stream offset.
+// slice_seconds == 1 only: every ts of a slice equals its base, so the
+// per-slice stable sort and the anchoring are identities. out = NULL counts.
+uint64_t ref_generate_slice(const orc_spec* s, uint64_t slice, uint32_t threads, uint32_t* out, char* err,
+                            size_t errlen) {
+    try {
+        const PlantSpec spec = to_spec(s);
+        spec.validate();
+        if (spec.slice_seconds != 1) throw std::invalid_argument("ref_generate_slice needs slice_seconds == 1");
+        if (slice >= spec.slices) throw std::invalid_argument("slice out of range");
+        uint64_t draws = 0;  // stream position at the start of the slice
+        for (uint64_t t = 0; t < slice; ++t) draws += plant_records(spec, t) + 3ull * spec.background.pairs_per_slice;
+        const uint64_t np = plant_records(spec, slice);
+        const uint64_t n = np + spec.background.pairs_per_slice;
+        if (!out) return n;
+        constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ull;
+        const uint32_t ts = spec.start_ts + static_cast<uint32_t>(slice) * spec.slice_seconds;
+        uint64_t at = 0;
+        for (size_t pi = 0; pi < spec.plants.size(); ++pi) {  // one draw (ts) per plant record
+            const auto& p = spec.plants[pi];
+            if (!p.active_in(slice)) continue;
+            const uint32_t r = static_cast<uint32_t>((slice - p.first_slice) % spec.window);
+            const auto [lo, hi] = detail::rotation_chunk(p.cardinality, spec.window, r);
+            const uint32_t off = detail::plant_pool_offset(pi, spec.background.b_hosts);
+            for (uint32_t j = lo; j < hi; ++j, ++at) {
+                out[3 * at] = ts;
+                out[3 * at + 1] = p.host;
+                out[3 * at + 2] = spec.b_base + (off + j) % spec.background.b_hosts;
+            }
+        }
+        const detail::ZipfSampler zipf(spec.background.b_hosts, spec.background.skew);
+        const uint64_t base = draws + np;
+        parallel_ranges(spec.background.pairs_per_slice, std::max<uint32_t>(threads, 1), [&](uint64_t i0, uint64_t i1) {
+            SplitMix64 rng(spec.seed + kPhi * (base + 3 * i0));
+            for (uint64_t i = i0; i < i1; ++i) {
+                uint32_t* r = out + 3 * (np + i);
+                r[1] = spec.a_base + static_cast<uint32_t>(rng.next_below(spec.background.a_hosts));
+                r[2] = spec.b_base + zipf.draw(rng);
+                r[0] = ts + static_cast<uint32_t>(rng.next_below(spec.slice_seconds));
+            }
+        });
+        return n;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return UINT64_MAX;
+    }
+}
+
+// ---- record-order flow (the parity definition) at full size
+void* ref_flow_create(const orc_config* cfg, uint32_t threads, char* err, size_t errlen) {
+    try {
+        const SeaConfig c = to_sea(cfg);
+        c.validate();
+        return with_recorder_word(c.recorder_bits, [&](auto word) -> void* {
+            using Word = decltype(word);
+            return static_cast<FlowBase*>(new Flow<Word>(c, threads));
+        });
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return nullptr;
+    }
+}
+void ref_flow_destroy(void* f) { delete static_cast<FlowBase*>(f); }
+// scan in record order; returns the sink pushes (pushes() reads them)
+uint64_t ref_flow_scan(void* f, const uint32_t* recs, uint64_t n) {
+    auto* F = static_cast<FlowBase*>(f);
+    return F->scan(recs, n, F->pushes);
+}
+void ref_flow_pushes(void* f, uint32_t* out) {
+    const auto& p = static_cast<FlowBase*>(f)->pushes;
+    std::memcpy(out, p.data(), p.size() * 4);
+}
+uint64_t ref_flow_ncand(void* f) { return static_cast<FlowBase*>(f)->cands().size(); }
+void ref_flow_candidates(void* f, uint32_t* out) {
+    const auto& c = static_cast<FlowBase*>(f)->cands();
+    std::memcpy(out, c.data(), c.size() * 4);
+}
+uint64_t ref_flow_report(void* f, uint64_t window_start, uint32_t* hosts, uint32_t* weights, double* est,
+                         uint8_t* has, uint8_t* sup) {
+    return static_cast<FlowBase*>(f)->report(window_start, hosts, weights, est, has, sup);
+}
+uint64_t ref_flow_slide(void* f) { return static_cast<FlowBase*>(f)->slide(); }
+uint64_t ref_flow_row_bytes(void* f, int kind) { return static_cast<FlowBase*>(f)->row_bytes(kind); }
+void ref_flow_state_blocks(void* f, uint32_t row, int kind, uint64_t* out) {
+    static_cast<FlowBase*>(f)->state_blocks(row, kind, out);
+}
+// the same block sums over any byte buffer (records, exported rows)
+void ref_block_sums(const void* p, uint64_t bytes, uint32_t threads, uint64_t* out) {
+    block_sums(static_cast<const uint8_t*>(p), bytes, threads, out);
 }
 
 // ---- ingest front end: the reference's own orient_record / SlicePartitioner / for_each_record

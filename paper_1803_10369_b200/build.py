@@ -33,12 +33,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
+    objs, jobs = [], []
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     for f in CXX_SOURCES:  # host doubles: no contraction, same libm as the reference
         o = os.path.join(LIBDIR, f + ".o")
-        subprocess.run(["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", *inc, "-c",
-                        os.path.join(CSRC, f), "-o", o], check=True)
+        jobs.append(["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", *inc, "-c",
+                     os.path.join(CSRC, f), "-o", o])
         objs.append(o)
     for f in CU_SOURCES:
         o = os.path.join(LIBDIR, f + ".o")
@@ -47,8 +47,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
                os.path.join(CSRC, f), "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        subprocess.run(cmd, check=True)
+        jobs.append(cmd)
         objs.append(o)
+    # translation units compile concurrently (engine.cu dominates)
+    procs = [subprocess.Popen(j) for j in jobs]
+    bad = [j for j, p in zip(jobs, procs) if p.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, bad[0])
     subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], check=True)
     for o in objs:
         os.remove(o)

@@ -27,6 +27,7 @@
 #include "scan_binned.cuh"
 #include "epoch.cuh"
 #include "nibble.cuh"
+#include "digest.cuh"
 #include "srla.h"
 
 namespace srla {
@@ -1916,6 +1917,31 @@ struct Engine {
         CK(cudaStreamSynchronize(st));
     }
 
+    // Block digests of one row in the reference layout (digest.cuh), on the device.
+    DevBuf<uint64_t> d_digest;
+    uint64_t state_blocks(uint32_t row, int kind, uint64_t* out, uint64_t cap) {
+        flush_linear();
+        join_maint();
+        uint8_t* p = row_ptr(row, kind);
+        const uint64_t bytes = row_bytes(kind);
+        const uint64_t nb = (bytes + (1ull << kDigestBlockShift) - 1) >> kDigestBlockShift;
+        if (!out) return nb;
+        if (cap < nb) throw Error(SRLA_E_CAPACITY, "digest buffer holds " + std::to_string(cap) + " blocks, " +
+                                                       std::to_string(nb) + " needed");
+        DigestSrc src{p, bytes, kDigestRaw, cur_epoch, dc.expired};
+        if (kind == SRLA_LINEAR && nib) src.layout = kDigestNibble;
+        if (kind == SRLA_LINEAR && epoch) src.layout = kDigestEpoch;
+        d_digest.ensure(nb);
+        if (nb) {
+            k_block_sums<<<static_cast<uint32_t>(nb), kDigestThreads, 0, st>>>(src, d_digest.p);
+            check_launch();
+            launched();
+            CK(cudaMemcpyAsync(out, d_digest.p, nb * 8, cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaStreamSynchronize(st));
+        return nb;
+    }
+
     void import_row(uint32_t row, int kind, const void* buf, uint64_t bytes) {
         flush_linear();
         uint8_t* p = row_ptr(row, kind);
@@ -2214,6 +2240,31 @@ srla_status srla_import_row(srla_engine* e, uint32_t row, int kind, const void* 
     return guard([&] {
         std::lock_guard<std::mutex> lk(e->mu);
         E(e).import_row(row, kind, buf, bytes);
+    });
+}
+
+srla_status srla_state_blocks(srla_engine* e, uint32_t row, int kind, uint64_t* out, uint64_t cap, uint64_t* n_blocks) {
+    return guard([&] {
+        const uint64_t nb = E(e).state_blocks(row, kind, out, cap);
+        if (n_blocks) *n_blocks = nb;
+    });
+}
+
+srla_status srla_block_sums(const void* d_buf, uint64_t bytes, uint64_t* out, uint64_t cap, void* stream) {
+    return guard([&] {
+        using namespace srla;
+        const uint64_t nb = (bytes + (1ull << kDigestBlockShift) - 1) >> kDigestBlockShift;
+        if (cap < nb) throw Error(SRLA_E_CAPACITY, "digest buffer too small");
+        if (!nb) return;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        uint64_t* d = nullptr;
+        CK(cudaMallocAsync(&d, nb * 8, s));
+        k_block_sums<<<static_cast<uint32_t>(nb), kDigestThreads, 0, s>>>(
+            DigestSrc{static_cast<const uint8_t*>(d_buf), bytes, kDigestRaw, 0, 0}, d);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, d, nb * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaFreeAsync(d, s));
+        CK(cudaStreamSynchronize(s));
     });
 }
 

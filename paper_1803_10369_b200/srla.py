@@ -140,6 +140,8 @@ def load_library(path: str = LIB_PATH):
         "srla_parse_srlt": (i32, [vp, u64, vp, C.POINTER(u64), vp]),
         "srla_orient_records": (i32, [vp, u64, u32, u32, vp, C.POINTER(u64), C.POINTER(COrientStats), vp]),
         "srla_slice_bounds": (i32, [vp, u64, u32, vp, u64, C.POINTER(u64), vp]),
+        "srla_state_blocks": (i32, [vp, u32, i32, vp, u64, C.POINTER(u64)]),
+        "srla_block_sums": (i32, [vp, u64, vp, u64, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -157,7 +159,7 @@ EXPORTED_SYMBOLS = (
     "srla_timing_get", "srla_timing_reset", "srla_partition_records", "srla_owner_of",
     "srla_end_slice_async", "srla_end_slice_wait", "srla_end_slice_compact",
     "srla_parse_srlt", "srla_orient_records", "srla_slice_bounds", "srla_device_alloc", "srla_device_free",
-    "srla_copy_to_device",
+    "srla_copy_to_device", "srla_state_blocks", "srla_block_sums",
 )
 
 
@@ -404,6 +406,14 @@ class EstimatorArray:
         return {(k, i): self.export_row(i, k) for i in range(self.cfg.rows)
                 for k in (INDICATOR, ROUGH, LINEAR)}
 
+    def state_blocks(self, row: int, kind: int) -> np.ndarray:
+        """Device-side block digests of a raw row (srla_state_blocks)."""
+        nb = C.c_uint64()
+        _check(_lib.srla_state_blocks(self._h, row, kind, None, 0, C.byref(nb)))
+        out = np.empty(max(1, nb.value), np.uint64)
+        _check(_lib.srla_state_blocks(self._h, row, kind, _ptr(out), len(out), C.byref(nb)))
+        return out[: nb.value]
+
     def stats(self) -> dict:
         s = CStats()
         _check(_lib.srla_stats_get(self._h, C.byref(s)))
@@ -502,6 +512,16 @@ class DeviceTraceGenerator:
         t = torch.empty((max(1, n), 3), dtype=torch.int32, device=f"cuda:{self.device}")
         self.generate_into(s, t.data_ptr(), n, torch.cuda.current_stream(self.device).cuda_stream)
         return t[:n]
+
+
+def block_sums(t) -> np.ndarray:
+    """Block digests (srla_block_sums) of a contiguous CUDA tensor's bytes."""
+    nbytes = t.numel() * t.element_size()
+    nb = (nbytes + (1 << 20) - 1) >> 20
+    out = np.empty(max(1, nb), np.uint64)
+    _check(load_library().srla_block_sums(C.c_void_p(t.data_ptr()), nbytes, _ptr(out), len(out),
+                                          C.c_void_p(_stream_of(t))))
+    return out[:nb]
 
 
 def owner_of(seed: int, aip: int, nparts: int) -> int:

@@ -163,3 +163,26 @@ def compare(golden_slices, got_slices):
     if len(golden_slices) != len(got_slices):
         return f"slice count {len(golden_slices)} vs {len(got_slices)}"
     return None
+
+
+def block_sums_np(buf) -> np.ndarray:
+    """numpy restatement of the state block digest (digest.cuh, ref_capi.cpp
+    block_sums): per 1 MiB block the wrapping sum of avalanche64(w ^
+    avalanche64(i + 1)) over the little-endian 8-byte words w_i of the row."""
+    b = np.ascontiguousarray(buf).view(np.uint8).reshape(-1)
+    nb = (len(b) + (1 << 20) - 1) >> 20
+    pad = np.zeros(nb << 20, np.uint8)
+    pad[: len(b)] = b
+    w = pad.view("<u8")
+    i = np.arange(1, len(w) + 1, dtype=np.uint64)
+
+    def av(x):
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+    with np.errstate(over="ignore"):
+        h = av(w ^ av(i))
+        # words past the row end contribute nothing (zero padding is only within the last word)
+        h[(len(b) + 7) // 8:] = 0
+        return h.reshape(nb, -1).sum(axis=1, dtype=np.uint64) if nb else np.zeros(0, np.uint64)

@@ -118,3 +118,23 @@ def test_generator_matches_reference(oracle, ref):
                          pairs_per_slice=700, skew=0.8,
                          plants=[(0x0AC80001, 90, 0, 3), (0x0AC80002, 200, 2, 0xFFFFFFFF)])
         assert np.array_equal(oracle.generate(spec), ref.generate(spec))
+
+
+def test_generate_slice_matches_generate_trace(ref):
+    """ref_generate_slice (parallel, counter-based jump-ahead over the
+    reference's own generator pieces) equals slice s of generate_trace."""
+    from oracle.pyoracle import PlantSpec
+    for skew, window, plants in ((1.0, 10, [(0x0AC80001, 900, 0, 0xFFFFFFFF), (0x0AC80002, 50, 2, 3)]),
+                                 (0.0, 1, [(0x0AC80001, 5000, 1, 0xFFFFFFFF)]), (0.7, 3, [])):
+        spec = PlantSpec(seed=9, slices=5, window=window, a_hosts=3000, b_hosts=8192, pairs_per_slice=4001,
+                         skew=skew, plants=plants)
+        whole = ref.generate(spec)
+        parts = [ref.generate_slice(spec, s, threads=t) for s, t in zip(range(5), (1, 2, 3, 7, 16))]
+        assert np.array_equal(whole, np.concatenate(parts))
+
+
+def test_block_sums_restated(ref):
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 7, 8, 9, 4096, (1 << 20) - 1, 1 << 20, (1 << 20) + 5, 3 * (1 << 20) + 13):
+        b = rng.integers(0, 256, n, dtype=np.uint8)
+        assert np.array_equal(ref.block_sums(b, threads=3), GF.block_sums_np(b)), n

@@ -472,3 +472,28 @@ def test_compact_report_handoff(gpu, oracle, name):
         m = has == 1
         assert np.array_equal(est[w[:n]][m].view(np.uint64), want["estimate"][m].view(np.uint64))
     assert np.array_equal(e.candidates(), pipe.candidates())
+
+
+@pytest.mark.parametrize("mode", ["literal", "nibble", "epoch", "w2"])
+def test_state_blocks_match_exported_rows(gpu, oracle, mode, monkeypatch):
+    """srla_state_blocks (device digests in the reference layout) equals the
+    digest of the exported rows for every table representation, and
+    srla_block_sums equals it on raw device bytes of ragged sizes."""
+    import torch
+    from paper_1803_10369_b200 import srla
+    name = {"w2": "wide_w2"}.get(mode, "contended")
+    monkeypatch.setenv("SRLA_FORCE_BINS", "1")
+    monkeypatch.setenv("SRLA_EPOCH", "1" if mode == "epoch" else "0")
+    monkeypatch.setenv("SRLA_NIBBLE", "1" if mode == "nibble" else "0")
+    cfg, _ = S.SCENARIOS[name]
+    e = engine(cfg)
+    for sid, recs in enumerate(GF.scenario_slices(name, oracle)[:4]):
+        e.scan(recs)
+        e.end_slice(sid)
+    for i in range(cfg.rows):
+        for k in (0, 1, 2):
+            assert np.array_equal(e.state_blocks(i, k), GF.block_sums_np(e.export_row(i, k))), (i, k)
+    rng = np.random.default_rng(1)
+    for n in (1, 13, (1 << 20) + 3, 5 << 20):
+        b = rng.integers(0, 256, n, dtype=np.uint8)
+        assert np.array_equal(srla.block_sums(torch.from_numpy(b).cuda()), GF.block_sums_np(b)), n

@@ -1,17 +1,22 @@
 #!/usr/bin/env python
 """SRLA benchmark: packets/s scanned + end-of-slice latency (BASELINE.json).
 
-Workload (BASELINE.json configs[1], "C2" in SURVEY.md §8d): one B200 per rank,
-sketch u=4, v=2^20, g=8, g'=1024, z=4 (u8 recorders), k=10, theta=1024, seed
-0x5EA00001; synthetic trace = the reference generator's C2 spec (uniform 4M
-sources, Zipf(1.0) 4M destinations, 50 planted super points), 1e8 packets per
-slice per GPU, produced byte-identically on the device and resident in HBM
-(1.2 GB per slice, > L2, so no flush is needed between steps).
+Headline workload (BASELINE.json configs[1], "C2" in SURVEY.md §8d): one B200
+per rank, sketch u=4, v=2^20, g=8, g'=1024, z=4 (u8 recorders), k=10,
+theta=1024, seed 0x5EA00001; synthetic trace = the reference generator's C2
+spec (uniform 4M sources, Zipf(1.0) 4M destinations, 50 planted super points),
+1e8 packets per slice per GPU, produced byte-identically on the device and
+resident in HBM (1.2 GB per slice, > L2, so no flush is needed between steps).
 
 A step = DetectPipeline::process_slice on one slice: scan (K1..K5) + report
-(when the window is full) + slide. N > 1: hosts are owner-partitioned
+(when the window is full) + slide. The line also carries a `c3` record
+(configs[2]: v=2^24, ~1e6 candidates): the end-of-slice latency target.
+
+N > 1 (weak scaling, configs[3]'s shape): hosts are owner-partitioned
 (reduce(3, aip, N)); every rank keeps an independent sketch for its hosts and
-the per-slice report is all-gathered over NCCL (the only collective).
+the per-slice report is all-gathered (the only collective). `--gpus N` without
+a torchrun environment launches the N ranks itself; with fewer GPUs than
+ranks they share GPUs over gloo (functional, contended timings).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -19,8 +24,8 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -30,33 +35,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_1803_10369_b200 import workloads as WL  # noqa: E402  (data only: no CUDA)
+
 METRIC = "packets/sec scanned (1/2/4/8 B200); end-of-slice estimation latency ms"
 ALGO_BYTES_PER_PACKET = 140  # 12 B streamed record + 4 rows x one 32-B sector update
-
-
-def plant_cards():
-    return [int(math.floor(1152.0 * math.pow(16384.0 / 1152.0, i / 49.0) + 0.5)) for i in range(50)]
-
-
-def sketch_cfg(cols):
-    return dict(rows=4, cols=cols, rough_slots=8, linear_slots=1024, recorder_bits=4, window=10, theta=1024,
-                seed=0x5EA00001)
-
-
-def trace_spec(pairs, slices=12, workload="c2"):
-    if workload == "c3":  # uniform, ~1e6 candidate super points
-        return dict(seed=3, slices=slices, window=10, a_hosts=1 << 20, b_hosts=1 << 24, pairs_per_slice=pairs,
-                    skew=0.0, plants=[])
-    return dict(seed=1, slices=slices, window=10, a_hosts=4194304, b_hosts=1 << 22, pairs_per_slice=pairs,
-                skew=1.0, plants=[(0x0AC80001 + i, c, 0, 0xFFFFFFFF) for i, c in enumerate(plant_cards())])
-
-
-WORKLOADS = {
-    "c2": "C2: u=4 v=2^20 g=8 g'=1024 z=4 k=10 theta=1024 seed=0x5EA00001; trace seed 1, 4M uniform sources, "
-          "Zipf(1.0) 4M destinations, 50 plants",
-    "c3": "C3: u=4 v=2^24 g=8 g'=1024 z=4 k=10 theta=1024 seed=0x5EA00001 (64 GiB linear table, epoch stamps); "
-          "trace seed 3, 1M uniform sources, 16M uniform destinations (~1e6 candidates)",
-}
 
 
 def env_rank():
@@ -68,8 +50,28 @@ def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def random_access_peak():
+    """BASELINE.md §3's HBM random-access roofline R: random 1-byte stores
+    into a 4 GiB table, counted at one 32-B sector each (tools/membench.cu,
+    profiles/r01_membench.json)."""
+    p = os.path.join(ROOT, "profiles", "r01_membench.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p))["st8_4096MB_Gops"] * 32.0
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -173,7 +175,12 @@ def kernel_rooflines(tm, step_ms_total, cfg, peak, peak_src, packets, steps, wor
         kernels[name] = {"ms_per_launch": kms / n, "launches": n, "algorithmic_bytes_per_launch": byts / n,
                          "achieved": ach, "frac": ach / peak, "share_of_step": kms / step_ms_total,
                          "traffic": nc.get("dram_bytes_per_launch"), "ncu": ncu}
-    dom = max(kernels, key=lambda k: kernels[k]["share_of_step"])
+    if tm.get("serial_kernel_launches"):
+        kernels["k_serial"] = {"ms_per_launch": tm["serial_kernel_ms"] / tm["serial_kernel_launches"],
+                               "launches": tm["serial_kernel_launches"],
+                               "share_of_step": tm["serial_kernel_ms"] / step_ms_total,
+                               "flagged_hosts": tm["flagged_hosts"]}
+    dom = max((k for k in kernels if "achieved" in kernels[k]), key=lambda k: kernels[k]["share_of_step"])
     d = kernels[dom]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": d["achieved"], "peak": peak, "unit": "GB/s",
                 "frac": d["frac"], "traffic": d["traffic"], "peak_source": peak_src,
@@ -192,65 +199,80 @@ def kernel_rooflines(tm, step_ms_total, cfg, peak, peak_src, packets, steps, wor
 
 # ---------------------------------------------------------------- CPU reference (checker only)
 
-def cpu_reference(sample_recs, cols, threads, slice_id):
-    """Time the reference's own DetectPipeline (oracle/_ref = the unmodified
-    headers; the C restatement if _ref is absent) on a bounded sample.
-    Returns scan rate and end-of-slice ms (report_window + slide)."""
-    from oracle.pyoracle import LIBS, Checker, SeaConfig, build
-    kind = "reference"
-    if not os.path.exists(LIBS["ref"]):
-        kind = "port"
-        if not os.path.exists(LIBS["orc"]):
-            build()
-    chk = Checker("ref" if kind == "reference" else "orc")
-    pipe = chk.pipeline(SeaConfig(**sketch_cfg(cols)), workers=threads)
-    t0 = time.perf_counter()
-    pipe.process_slice(slice_id, sample_recs, True)
-    total_ms = (time.perf_counter() - t0) * 1e3
-    scan_ms = pipe.scan_ms
-    return {"kind": kind, "scan_rate": len(sample_recs) / (scan_ms / 1e3), "scan_ms": scan_ms,
-            "eos_ms": total_ms - scan_ms, "threads": threads if kind == "reference" else 1}
+def reference_checker():
+    """oracle/_ref (the unmodified reference headers) when present, else the C restatement."""
+    from oracle.pyoracle import LIBS, Checker, build
+    if os.path.exists(LIBS["ref"]):
+        return Checker("ref"), "reference"
+    if not os.path.exists(LIBS["orc"]):
+        build()
+    return Checker("orc"), "port"
 
 
-def sample_records(n, device):
-    """First n background packets (plus the plants) of C2 slice 0 — an exact
-    prefix of the benchmark's own slice 0 (same generator draws)."""
-    import numpy as np
-    from paper_1803_10369_b200.srla import DeviceTraceGenerator, PlantSpec
-    gen = DeviceTraceGenerator(PlantSpec(**trace_spec(n, slices=1)), device=device)
-    return gen.slice_tensor(0).cpu().numpy().view(np.uint32).copy()
+def reference_steady(chk, cols, slices, threads, prefill, warmup, steps):
+    """The reference's own DetectPipeline<u8> (workers = threads) over full
+    slices: `prefill` slices to fill the window, then warmup + timed steps of
+    process_slice (scan + report_window + slide), cycling over `slices`."""
+    from oracle.pyoracle import SeaConfig
+    pipe = chk.pipeline(SeaConfig(**WL.sketch_cfg(cols)), workers=threads)
+    sid = 0
+    for _ in range(prefill + warmup):
+        pipe.process_slice(sid, slices[sid % len(slices)], True)
+        sid += 1
+    per, eos, packets, cands = [], [], 0, []
+    for _ in range(steps):
+        recs = slices[sid % len(slices)]
+        s0 = pipe.scan_ms
+        t0 = time.perf_counter()
+        rep = pipe.process_slice(sid, recs, True)
+        ms = (time.perf_counter() - t0) * 1e3
+        per.append(ms)
+        eos.append(ms - (pipe.scan_ms - s0))
+        packets += len(recs)
+        cands.append(0 if rep is None else len(rep["host"]))
+        sid += 1
+    total = sum(per)
+    return {"value": packets / (total / 1e3), "ms_per_step": total / steps, "eos_median": statistics.median(eos),
+            "eos_p99": max(eos), "report_entries_median": statistics.median(cands), "packets": packets}
 
 
 def run_reference_arm(args):
-    rank, world, local = env_rank()
+    """--impl reference: the reference's CPU implementation of the path on
+    this box's host cores, same workload / metric / steps as the engine arm.
+    Input = the reference generator's own slices (ref_generate_slice)."""
+    rank, world, _ = env_rank()
     if rank != 0:
         return 0
+    from oracle.pyoracle import PlantSpec
+    chk, kind = reference_checker()
     threads = os.cpu_count() or 1
-    samp_n = args.cpu_sample
-    recs = sample_records(samp_n, local)
-    full = args.packets
-    per_step = []
-    res = None
-    for i in range(args.warmup + args.steps):
-        res = cpu_reference(recs, args.cols or (1 << 20), threads, slice_id=9)
-        ms_full = full / res["scan_rate"] * 1e3 + res["eos_ms"]
-        if i >= args.warmup:
-            per_step.append((ms_full, res))
-    ms = statistics.mean(p[0] for p in per_step)
-    value = full / (ms / 1e3)
-    eos = [p[1]["eos_ms"] for p in per_step]
+    spec = WL.trace_spec(args.packets, slices=args.resident, workload="c2")
+    t0 = time.perf_counter()
+    if kind == "reference":
+        slices = [chk.generate_slice(PlantSpec(**spec), s, threads) for s in range(args.resident)]
+    else:
+        whole = chk.generate(PlantSpec(**spec))
+        n0 = len(whole) // args.resident
+        slices = [whole[i * n0:(i + 1) * n0] for i in range(args.resident)]
+    gen_s = time.perf_counter() - t0
+    prefill = 9
+    r = reference_steady(chk, 1 << 20, slices, threads, prefill, args.warmup, args.steps)
+    n = max(1, world) if world > 1 else args.gpus
+    sample = (f"each step: DetectPipeline<u8>::process_slice (workers={threads}, unpinned) on one full "
+              f"{args.packets:.0e}-packet C2 slice at steady state ({prefill} prefill + {args.warmup} warmup slices, "
+              f"~{r['report_entries_median']:.0f} candidates per report); slices from ref_generate_slice "
+              f"({gen_s:.0f} s, not timed); CPU {cpu_model()}, {threads} logical cores")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "packets/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "C2: u=4 v=2^20 g=8 g'=1024 z=4 k=10 theta=1024; 1e8 packets/slice",
-                   "packets_per_slice": full, "parallelism": "cpu threads"},
-        "end_of_slice_ms": {"median": statistics.median(eos), "p99": max(eos)},
-        "cpu_baseline": {"value": value, "unit": "packets/s", "cores": res["threads"], "kind": res["kind"],
-                         "sample": f"each step: DetectPipeline<u8>::process_slice (workers={res['threads']}) on the "
-                                   f"first {len(recs)} packets of C2 slice 0 at v=2^20 with a report due; "
-                                   f"value = 1e8 / (1e8 / measured scan rate + measured report+slide time)"},
-        "e2e": {"value": value, "unit": "packets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "packets/s", "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference generator C2 spec)",
+        "config": {"workload": WL.DESCRIPTIONS["c2"], "packets_per_slice": args.packets,
+                   "resident_slices": args.resident, "parallelism": f"{threads} CPU threads (rank 0 only)"},
+        "same_config": kind == "reference",
+        "end_of_slice_ms": {"median": r["eos_median"], "p99": r["eos_p99"]},
+        "cpu_baseline": {"value": r["value"], "unit": "packets/s", "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": r["value"], "unit": "packets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -258,11 +280,45 @@ def run_reference_arm(args):
 
 # ---------------------------------------------------------------- the engine
 
+class Workload:
+    """Slices staged in HBM + an engine for one workload on this rank."""
+
+    def __init__(self, name, args, rank, world, local):
+        import torch
+
+        from paper_1803_10369_b200 import srla
+        self.name, self.srla = name, srla
+        cols = args.cols if args.cols else WL.cols_of(name)
+        self.cfg = srla.SeaConfig(**WL.sketch_cfg(cols))
+        self.spec = WL.trace_spec(args.packets * world, slices=12, workload=name)
+        gen = srla.DeviceTraceGenerator(srla.PlantSpec(**self.spec), device=local)
+        self.nres = min(self.spec["slices"], args.resident if name == "c2" else 10)
+        self.slices = []
+        for s in range(self.nres):
+            full = gen.slice_tensor(s)
+            if world > 1:
+                own = torch.empty_like(full)
+                m = srla.partition_records(full.data_ptr(), full.shape[0], self.cfg.seed, world, rank,
+                                           own.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                self.slices.append(own[:m].clone())
+                del own
+            else:
+                self.slices.append(full)
+            del full
+        torch.cuda.synchronize()
+        self.eng = srla.EstimatorArray(self.cfg, device=local)
+        self.rep_cap = 1 << 21
+        self.L = self.cfg.linear_slots + 1
+
+
 def run_engine(args):
+    import ctypes as C
+
     import numpy as np
     import torch
 
     from paper_1803_10369_b200 import srla
+    from paper_1803_10369_b200.shard import allgather_report_compact, allgather_report_entries
 
     rank, world, local = env_rank()
     # one process per GPU; SRLA_BENCH_BACKEND=gloo lets several ranks share a
@@ -278,108 +334,53 @@ def run_engine(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    cols = args.cols if args.cols else (1 << 24 if args.workload == "c3" else 1 << 20)
-    cfg = srla.SeaConfig(**sketch_cfg(cols))
-    n_per_gpu = args.packets
-    spec = trace_spec(n_per_gpu * world, workload=args.workload)
-    gen = srla.DeviceTraceGenerator(srla.PlantSpec(**spec), device=local)
 
-    # stage the trace in HBM: one owned slice per generator slice
-    nres = min(spec["slices"], args.resident)
-    slices = []
-    for s in range(nres):
-        full = gen.slice_tensor(s)
-        if world > 1:
-            own = torch.empty_like(full)
-            m = srla.partition_records(full.data_ptr(), full.shape[0], cfg.seed, world, rank, own.data_ptr(),
-                                       torch.cuda.current_stream().cuda_stream)
-            slices.append(own[:m].clone())
-            del own
-        else:
-            slices.append(full)
-        del full
-    torch.cuda.synchronize()
-
-    eng = srla.EstimatorArray(cfg, device=local)
+    w = Workload(args.workload, args, rank, world, local)
+    eng, cfg, slices, nres = w.eng, w.cfg, w.slices, w.nres
     st = torch.cuda.ExternalStream(eng.stream_handle())
-    rep_cap = 1 << 21
+
+    def pinned(nbytes):
+        return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy()
 
     def pinned_entries(n):  # DMA-able report buffer: the engine maps entries straight into it
-        return torch.empty(n * srla.ENTRY_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True).numpy().view(
-            srla.ENTRY_DTYPE)
+        return pinned(n * srla.ENTRY_DTYPE.itemsize).view(srla.ENTRY_DTYPE)
 
-    rep_buf = pinned_entries(rep_cap)
-
-    from paper_1803_10369_b200.shard import allgather_report_entries as _allgather_dev
+    comp_hosts = pinned(w.rep_cap * 4).view(np.uint32)
+    comp_w = pinned(w.rep_cap * 4).view(np.uint32)
+    comp_est, comp_flags = np.empty(w.L, np.float64), np.empty(w.L, np.uint8)
+    rep_buf = pinned_entries(w.rep_cap)
 
     def allgather_report(entries):  # merged on the device (N > 1)
-        return entries if world == 1 else _allgather_dev(entries, dist, comm_dev)
+        return entries if world == 1 else allgather_report_entries(entries, dist, comm_dev)
+
+    def end_slice(sid):
+        if args.handoff == "compact":  # hosts + weights (8 B/entry) + the window's Eq. 9 table
+            return eng.end_slice_compact(sid, comp_hosts, comp_w, comp_est, comp_flags)
+        n, nr = C.c_uint64(), C.c_uint64()
+        srla._check(srla._lib.srla_end_slice(eng._h, sid, 1, C.c_void_p(rep_buf.ctypes.data), len(rep_buf),
+                                             C.byref(n), C.byref(nr)))
+        return n.value, nr.value
 
     def step(sid):
         eng.scan(slices[sid % nres])
-        n, nr = _end_slice(eng, sid, rep_buf)
+        n, _ = end_slice(sid)
         if world > 1:
-            if args.handoff == "compact":  # (host, weight) words + this shard's Eq. 9 table, merged on the device
-                from paper_1803_10369_b200.shard import allgather_report_compact
+            if args.handoff == "compact":
                 h = torch.from_numpy(comp_hosts[:n].view(np.int32)).to(comm_dev, non_blocking=True)
-                w = torch.from_numpy(comp_w[:n].view(np.int32)).to(comm_dev, non_blocking=True)
+                wt = torch.from_numpy(comp_w[:n].view(np.int32)).to(comm_dev, non_blocking=True)
                 mask = 0xFFFFFFFF
-                return allgather_report_compact(h.to(torch.int64) & mask, w.to(torch.int64) & mask,
-                                                torch.from_numpy(comp_est).to(comm_dev),
-                                                torch.from_numpy(comp_flags).to(comm_dev), dist), n
-            return allgather_report(rep_buf[:n]), n
-        return None, n
-
-    import ctypes as C
-
-    L = cfg.linear_slots + 1
-    comp_hosts = torch.empty(rep_cap * 4, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint32)
-    comp_w = torch.empty(rep_cap * 4, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint32)
-    comp_est, comp_flags = np.empty(L, np.float64), np.empty(L, np.uint8)
-
-    def _end_slice(e, sid, buf):
-        if args.handoff == "compact":  # hosts + weights (8 B/entry) + the window's Eq. 9 table
-            n, nr = e.end_slice_compact(sid, comp_hosts, comp_w, comp_est, comp_flags)
-            return n, nr
-        n, nr = C.c_uint64(), C.c_uint64()
-        srla._check(srla._lib.srla_end_slice(e._h, sid, 1, C.c_void_p(buf.ctypes.data), len(buf), C.byref(n),
-                                             C.byref(nr)))
-        return n.value, nr.value
-
-    # Overlapped pipeline (C2 default): srla_end_slice_async(s) returns at once and
-    # srla_scan_batch(s+1) bins its packets (K1) into the second bin set while
-    # slice s's end-of-slice still runs, then joins it; the report of slice s is
-    # collected with srla_end_slice_wait. Same work per step, pipelined.
-    abufs = [pinned_entries(rep_cap) for _ in range(2)] if args.overlap else None
-    pend = {"slot": None}
-
-    def collect():
-        if pend["slot"] is None:
-            return None
-        n, _ = eng.end_slice_wait()
-        rep = abufs[pend["slot"]][:n]
-        pend["slot"] = None
-        if world > 1:
-            allgather_report(rep)
-        return n
-
-    def step_overlapped(sid):
-        eng.scan(slices[sid % nres])  # joins the pending end-of-slice after its K1
-        n = collect()
-        eng.end_slice_async(sid, abufs[sid % 2])
-        pend["slot"] = sid % 2
+                allgather_report_compact(h.to(torch.int64) & mask, wt.to(torch.int64) & mask,
+                                         torch.from_numpy(comp_est).to(comm_dev),
+                                         torch.from_numpy(comp_flags).to(comm_dev), dist)
+            else:
+                allgather_report(rep_buf[:n])
         return n
 
     sid = 0
     prefill = max(0, cfg.window - 1 - args.warmup)
     for _ in range(prefill + args.warmup):
-        if args.overlap:
-            step_overlapped(sid)
-        else:
-            step(sid)
+        step(sid)
         sid += 1
-    if args.overlap:
-        collect()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -393,24 +394,13 @@ def run_engine(args):
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(st)
     eos_dev, eos_wall, entries = [], [], []
-
-    def eos_sample(n):
+    for _ in range(args.steps):
+        n = step(sid)
         tm = eng.timing()
         eos_dev.append(tm["last_end_slice_device_ms"])
         eos_wall.append(tm["last_end_slice_wall_ms"])
         entries.append(n)
-
-    for _ in range(args.steps):
-        if args.overlap:
-            n = step_overlapped(sid)
-            if n is not None:
-                eos_sample(n)
-        else:
-            _, n = step(sid)
-            eos_sample(n)
         sid += 1
-    if args.overlap:
-        eos_sample(collect())
     t_end.record(st)
     t_end.synchronize()
     if dist:
@@ -434,6 +424,15 @@ def run_engine(args):
     peak, peak_src = measured_peaks()
     roofline, kernels, path = kernel_rooflines(tm, ms, cfg, peak, peak_src, tm["scan_kernel_records"], args.steps,
                                               args.workload)
+    R = random_access_peak()
+    rand = None
+    if R:
+        ach = value / max(1, world) * ALGO_BYTES_PER_PACKET / 1e9
+        rand = {"R": R, "unit": "GB/s", "achieved_per_gpu": ach, "frac": ach / R,
+                "definition": "packets/s per GPU x 140 B (12 B record + 4 random 32-B sector updates) over R = "
+                              "measured random 1-byte stores into a 4 GiB table x 32 B (tools/membench.cu, "
+                              "profiles/r01_membench.json); > 1 because the engine bins the marks and streams "
+                              "the table instead of updating sectors at random"}
 
     # end to end through the public API with host buffers (pinned), H2D inside:
     # scan_batch(host) + end_slice_async/wait, so a slice's host->device copies
@@ -443,7 +442,7 @@ def run_engine(args):
         nh = min(2, nres)
         host = [slices[i].cpu().pin_memory().numpy().view(np.uint32) for i in range(nh)]
         h2d = sum(h.nbytes for h in host) / nh
-        bufs = [pinned_entries(rep_cap) for _ in range(2)]
+        bufs = [pinned_entries(w.rep_cap) for _ in range(2)]
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -473,31 +472,41 @@ def run_engine(args):
         e2e = {"value": packets / el, "unit": "packets/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h / args.steps),
                "api": "srla_scan_batch(host, pinned) + srla_end_slice_async/wait"}
+        del host
 
+    # the reference on this box's host cores, steady state on the same slices
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
-        recs = sample_records(args.cpu_sample, local)
+        chk, kind = reference_checker()
         threads = os.cpu_count() or 1
-        r = cpu_reference(recs, cols, threads, slice_id=9)
-        ms_full = n_per_gpu / r["scan_rate"] * 1e3 + r["eos_ms"]
-        cpu = {"value": n_per_gpu / (ms_full / 1e3), "unit": "packets/s", "cores": r["threads"], "kind": r["kind"],
-               "sample": f"DetectPipeline<u8>::process_slice (workers={r['threads']}) on the first {len(recs)} "
-                         f"packets of C2 slice 0 at v=2^20 with a report due: scan {r['scan_rate']:.4g} pkt/s, "
-                         f"report+slide {r['eos_ms']:.1f} ms; value = 1e8/(1e8/scan rate + report+slide)"}
+        host = [s.cpu().numpy().view(np.uint32) for s in slices]
+        r = reference_steady(chk, cfg.cols, host, threads, prefill=9, warmup=0, steps=args.cpu_steps)
+        cpu = {"value": r["value"], "unit": "packets/s", "cores": threads, "kind": kind,
+               "sample": f"DetectPipeline<u8>::process_slice (workers={threads}, unpinned; {cpu_model()}) on "
+                         f"{args.cpu_steps} full C2 slices at steady state after a 9-slice prefill "
+                         f"(~{r['report_entries_median']:.0f} candidates per report), end-of-slice "
+                         f"{r['eos_median']:.0f} ms median"}
+        del host
+
+    del slices, w.slices
+    torch.cuda.empty_cache()
+    c3 = None
+    if world == 1 and args.workload == "c2" and not args.no_c3:
+        del eng, w
+        torch.cuda.empty_cache()
+        c3 = run_c3(args, local, peak, peak_src)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "packets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference generator C2 spec, device port)",
-            "config": {"workload": WORKLOADS[args.workload],
-                       "packets_per_slice_per_gpu": n_per_gpu, "resident_slices": nres,
-                       "report_handoff": "srla_end_slice_async/wait: 24-byte srla_entry per entry (pinned), "
-                                         "next slice's K1 overlapped" if args.overlap else
-                       "srla_end_slice_compact: host+weight per entry and the Eq. 9 table"
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference generator spec, device port)",
+            "config": {"workload": WL.DESCRIPTIONS[args.workload],
+                       "packets_per_slice_per_gpu": args.packets, "resident_slices": nres,
+                       "report_handoff": "srla_end_slice_compact: host+weight per entry and the Eq. 9 table"
                        if args.handoff == "compact" else "srla_end_slice: 24-byte srla_entry per entry",
                        "l2": "inputs larger than L2 (1.2 GB per slice); no flush",
-                       "parallelism": f"owner-partitioned x{world}" if world > 1 else "1 GPU"},
+                       "parallelism": f"owner-partitioned x{world} ({backend})" if world > 1 else "1 GPU"},
             "end_of_slice_ms": {"device_median": statistics.median(eos_dev),
                                 "device_p99": sorted(eos_dev)[min(len(eos_dev) - 1, int(0.99 * len(eos_dev)))],
                                 "device_max": max(eos_dev), "samples": len(eos_dev),
@@ -506,12 +515,14 @@ def run_engine(args):
             "roofline": roofline,
             "kernels": kernels,
             "roofline_scan_path": path,
+            "random_access_roofline": rand,
             "breakdown_ms_per_step": {k: (tm[k] - tm0.get(k, 0)) / args.steps for k in
                                       ("scan_kernel_ms", "order_wall_ms", "report_wall_ms", "slide_wall_ms",
-                                       "sync_wait_ms", "syncs", "alloc_ms", "allocs")},
+                                       "sync_wait_ms", "syncs", "alloc_ms", "allocs", "serial_kernel_ms")},
+            "flagged_hosts_per_step": tm["flagged_hosts"] / args.steps,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "overlapped_chunks": int(st1["overlapped_chunks"] - st0["overlapped_chunks"]),
+            "c3": c3,
             "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
             "library_launches": int(st1["library_launches"] - st0["library_launches"]),
             "clocks": clk,
@@ -522,34 +533,109 @@ def run_engine(args):
     return 0
 
 
+def run_c3(args, local, peak, peak_src):
+    """configs[2] (v = 2^24, ~1e6 candidates): the end-of-slice latency target.
+    k - 1 prefill slices, W warm-up steps, then K timed process_slice steps."""
+    import numpy as np
+    import torch
+
+    class A:  # the C3 slice shape at the same packets per slice
+        packets, cols, resident = args.packets, 0, 10
+
+    w = Workload("c3", A, 0, 1, local)
+    eng, cfg = w.eng, w.cfg
+    st = torch.cuda.ExternalStream(eng.stream_handle())
+    hosts = torch.empty(w.rep_cap * 4, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint32)
+    wts = torch.empty(w.rep_cap * 4, dtype=torch.uint8, pin_memory=True).numpy().view(np.uint32)
+    est, flags = np.empty(w.L, np.float64), np.empty(w.L, np.uint8)
+    sid = 0
+    for _ in range(cfg.window - 1 + args.warmup):
+        eng.scan(w.slices[sid % w.nres])
+        eng.end_slice_compact(sid, hosts, wts, est, flags)
+        sid += 1
+    eng.synchronize()
+    eng.timing_reset()
+    st0 = eng.stats()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(st)
+    eos_dev, eos_wall, entries = [], [], []
+    for _ in range(args.steps):
+        eng.scan(w.slices[sid % w.nres])
+        n, _ = eng.end_slice_compact(sid, hosts, wts, est, flags)
+        tm = eng.timing()
+        eos_dev.append(tm["last_end_slice_device_ms"])
+        eos_wall.append(tm["last_end_slice_wall_ms"])
+        entries.append(n)
+        sid += 1
+    t1.record(st)
+    t1.synchronize()
+    ms = t0.elapsed_time(t1)
+    tm, st1 = eng.timing(), eng.stats()
+    packets = st1["packets"] - st0["packets"]
+    roofline, kernels, path = kernel_rooflines(tm, ms, cfg, peak, peak_src, tm["scan_kernel_records"], args.steps,
+                                              "c3")
+    q = sorted(eos_dev)
+    out = {"workload": WL.DESCRIPTIONS["c3"], "value": packets / (ms / 1e3), "unit": "packets/s",
+           "ms_per_step": ms / args.steps,
+           "end_of_slice_ms": {"device_median": statistics.median(eos_dev),
+                               "device_p99": q[min(len(q) - 1, int(0.99 * len(q)))], "device_max": q[-1],
+                               "wall_median": statistics.median(eos_wall), "samples": len(q),
+                               "target_ms": 1.0},
+           "report_entries_median": statistics.median(entries), "roofline": roofline, "kernels": kernels,
+           "flagged_hosts_per_step": tm["flagged_hosts"] / args.steps,
+           "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"])}
+    del eng, w
+    torch.cuda.empty_cache()
+    return out
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args):
+    """`--gpus N` outside torchrun: launch N ranks (one process per GPU) the
+    way the driver does; ranks share GPUs over gloo when fewer are present."""
+    env = dict(os.environ)
+    try:
+        import torch
+        ndev = torch.cuda.device_count()
+    except Exception:
+        ndev = 0
+    if ndev < args.gpus:
+        env["SRLA_BENCH_BACKEND"] = "gloo"
+        print(f"[bench] {args.gpus} ranks on {ndev} GPU(s): ranks share GPUs over gloo", file=sys.stderr)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    ap.add_argument("--packets", type=int, default=100_000_000, help="packets per slice per GPU")
+    ap.add_argument("--packets", type=int, default=WL.PAIRS, help="packets per slice per GPU")
     ap.add_argument("--cols", type=int, default=0, help="sketch columns (default: the workload's)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3"])
-    ap.add_argument("--resident", type=int, default=0, help="distinct slices staged in HBM (default 12; c3: 10)")
-    ap.add_argument("--cpu-sample", type=int, default=20_000_000)
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"])
+    ap.add_argument("--resident", type=int, default=12, help="distinct slices staged in HBM")
+    ap.add_argument("--cpu-steps", type=int, default=2, help="timed steady-state slices of the cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 end-of-slice record")
     ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi clock sampling period in the timed region")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--overlap", action="store_true",
-                    help="pipeline slice s+1's K1 under slice s's asynchronous end-of-slice (SRLA_OVERLAP=1; "
-                         "measured slower on C2, kept as an option)")
     ap.add_argument("--handoff", default="compact", choices=["compact", "entries"],
                     help="report hand-off of the device-resident steps (e2e always returns srla_entry)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.overlap:
-        os.environ["SRLA_OVERLAP"] = "1"
-    if not args.resident:
-        args.resident = 10 if args.workload == "c3" else 12
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     return run_engine(args)
 
 

@@ -119,6 +119,16 @@ srla_status srla_column_of(const srla_engine* e, uint32_t row, uint32_t aip, uin
 srla_status srla_scan_batch(srla_engine* e, const srla_record* recs, uint64_t n, int on_device,
                             uint32_t* pushed, uint64_t cap, uint64_t* n_pushed);
 
+/* srla_scan_batch over device records with an explicit producer: the engine's
+ * streams wait (device-side) for everything queued on `producer_stream` (a
+ * cudaStream_t; NULL = the legacy default stream) before reading `d_recs`.
+ * srla_scan_batch(on_device = 1) is this call with the legacy default stream,
+ * so records written by work on another non-blocking stream need this form.
+ * `d_recs` must be device memory on the engine's GPU (SRLA_E_INVALID
+ * otherwise). The records may be reused once the call returns. */
+srla_status srla_scan_device(srla_engine* e, const srla_record* d_recs, uint64_t n, void* producer_stream,
+                             uint32_t* pushed, uint64_t cap, uint64_t* n_pushed);
+
 /* The engine-owned candidate list (DetectPipeline::candidates, pipeline.hpp:131),
  * insertion order. */
 srla_status srla_candidates(srla_engine* e, uint32_t* out, uint64_t cap, uint64_t* n);
@@ -153,7 +163,7 @@ srla_status srla_end_slice_async(srla_engine* e, uint64_t slice_id, int want_rep
 srla_status srla_end_slice_wait(srla_engine* e, uint64_t* n_out, uint64_t* n_retained);
 
 /* srla_end_slice with the report handed off compactly: hosts (ascending) and
- * union weights (8 bytes per entry instead of 24) plus this window's Eq. 9
+ * union weights (8 bytes per entry instead of 24; host or device memory) plus this window's Eq. 9
  * table over the g'+1 possible weights: estimate = est_lut[w], has_estimate =
  * flags_lut[w] & 1, is_super = (flags_lut[w] >> 1) & 1. Same results as the
  * srla_entry form (sea.hpp:296-305). */
@@ -229,6 +239,9 @@ typedef struct srla_timing {
     uint64_t syncs;
     double alloc_ms;              /* process-wide device/pinned (re)allocation host time */
     uint64_t allocs;
+    double serial_kernel_ms;      /* k_serial: ordered indicator resolution of flagged hosts */
+    uint64_t serial_kernel_launches;
+    uint64_t flagged_hosts;       /* hosts resolved by k_serial */
 } srla_timing;
 srla_status srla_timing_get(const srla_engine* e, srla_timing* out);
 srla_status srla_timing_reset(srla_engine* e);
@@ -280,6 +293,68 @@ srla_status srla_partition_records(const srla_record* d_in, uint64_t n, uint64_t
                                    uint32_t part, srla_record* d_out, uint64_t* n_out, void* stream);
 /* Host-side owner of one address (same function). */
 uint32_t srla_owner_of(uint64_t seed, uint32_t aip, uint32_t nparts);
+
+/* ---- sharded pipeline: one rank of an owner-partitioned
+ * DetectPipeline. The reference is single-node and has no counterpart
+ * (multi-node sharding is its non-goal); each shard equals a reference
+ * DetectPipeline fed the owner-filtered sub-trace in order
+ * (pipeline.hpp:110-129), and the merged report equals the concatenation of
+ * the shards' reports sorted by host (report_window's order, sea.hpp:294-295).
+ *
+ * The collectives go through a transport: NCCL over NVLink/NVSwitch
+ * (srla_transport_nccl, libnccl.so.2 loaded at first use), or caller
+ * callbacks (e.g. gloo for tests). Every rank calls every collective in the
+ * same order. */
+typedef struct srla_transport {
+    void* ctx;
+    uint32_t rank, world;
+    /* 1: the callbacks receive host memory (the library stages device data
+     * through pinned buffers); 0: device memory, ordered on `stream`. */
+    int host_memory;
+    /* every rank contributes `bytes` at `send`; `recv` receives world * bytes, rank-major */
+    int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes, void* stream);
+    /* send_bytes[j] bytes at send + send_off[j] go to rank j; recv_bytes[i]
+     * bytes from rank i land at recv + recv_off[i] */
+    int (*alltoallv)(void* ctx, const void* send, const uint64_t* send_bytes, const uint64_t* send_off, void* recv,
+                     const uint64_t* recv_bytes, const uint64_t* recv_off, void* stream);
+} srla_transport;
+
+/* ncclGetUniqueId (128 bytes): rank 0 creates it and broadcasts it out of band. */
+srla_status srla_nccl_unique_id(void* id128);
+/* An NCCL communicator for (rank, world) on `device`, wrapped as a transport
+ * (device memory, the shard's stream). */
+srla_status srla_transport_nccl(const void* id128, uint32_t rank, uint32_t world, int device, srla_transport* out);
+srla_status srla_transport_nccl_destroy(srla_transport* t);
+
+typedef struct srla_shard srla_shard;
+/* The rank's engine (srla_create(cfg, device)) behind a transport (copied). */
+srla_status srla_shard_create(const srla_config* cfg, int device, const srla_transport* t, srla_shard** out);
+srla_status srla_shard_destroy(srla_shard* s);
+/* The rank's engine (stats, timing, rows, candidates). Owned by the shard. */
+srla_status srla_shard_engine(srla_shard* s, srla_engine** e);
+
+/* How srla_shard_process_slice's records arrive. */
+enum {
+    SRLA_SHARD_OWNED = 0, /* already owner-partitioned (e.g. NIC RSS by host hash): scanned as given */
+    SRLA_SHARD_RANGE = 1  /* this rank's contiguous range of the slice (ranges in rank order): partitioned
+                           * by owner on the device and exchanged all-to-all, sources concatenated in rank
+                           * order so every owner sees its records in slice order */
+};
+
+/* DetectPipeline::process_slice for one slice across the ranks: scan, then
+ * if want_report and slice_id + 1 >= window the report all-gather (entry
+ * counts, (host, weight) words and each shard's Eq. 9 table) merged by host
+ * on the device into `out` (host memory, cap entries; *n_out = the merged
+ * size, 0 when no report is due), then slide. *n_scanned = records this rank
+ * scanned. Collective: every rank calls it for every slice. A report larger
+ * than `cap` returns SRLA_E_CAPACITY with *n_out set, after the slice has
+ * completed (fetch it with srla_shard_last_report). */
+srla_status srla_shard_process_slice(srla_shard* s, uint64_t slice_id, const srla_record* recs, uint64_t n,
+                                     int on_device, int input_mode, int want_report, srla_entry* out, uint64_t cap,
+                                     uint64_t* n_out, uint64_t* n_scanned);
+/* The last merged report again (e.g. after SRLA_E_CAPACITY from
+ * srla_shard_process_slice, which still completed the slice). */
+srla_status srla_shard_last_report(srla_shard* s, srla_entry* out, uint64_t cap, uint64_t* n_out);
 
 /* Device memory for callers without CUDA headers (the drop-in C++ API). */
 srla_status srla_device_alloc(int device, uint64_t bytes, void** out);

@@ -4,7 +4,7 @@
 // 64 GiB of recorders per slice against the reference without moving them:
 // per 1 MiB block of a row, the wrapping sum over its little-endian 8-byte
 // words w_i (zero-padded) of avalanche64(w_i ^ avalanche64(i + 1)), i = the
-// word's index in the row. oracle/ref_capi.cpp (block_sums) computes the same
+// word's index in the row. The test-side checker computes the same
 // sums over the reference's own rows.
 #pragma once
 

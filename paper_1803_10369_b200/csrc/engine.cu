@@ -19,6 +19,7 @@
 #include <thread>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 
@@ -56,6 +57,12 @@ struct AllocTimer {
     ~AllocTimer() {
         g_alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         ++g_allocs;
+    }
+};
+
+struct PairHash {
+    size_t operator()(const std::pair<int, const void*>& k) const {
+        return std::hash<const void*>()(k.second) ^ (static_cast<size_t>(k.first) * 0x9E3779B97F4A7C15ull);
     }
 };
 
@@ -113,6 +120,23 @@ struct PinBuf {
         cap = c;
     }
 };
+
+// Dynamic shared-memory caps are per kernel, shared by every engine on a
+// device: only ever raise them (a smaller engine created later must not lower
+// the cap a larger one launches with).
+inline std::mutex g_smem_mu;
+template <typename K>
+void raise_smem_cap(K* kernel, size_t bytes) {
+    static std::unordered_map<std::pair<int, const void*>, size_t, PairHash>* seen = nullptr;
+    std::lock_guard<std::mutex> lk(g_smem_mu);
+    if (!seen) seen = new std::unordered_map<std::pair<int, const void*>, size_t, PairHash>();
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    size_t& cur = (*seen)[{dev, reinterpret_cast<const void*>(kernel)}];
+    if (bytes <= cur) return;
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    cur = bytes;
+}
 
 struct Engine {
     // compact report hand-off (srla_end_slice_compact)
@@ -242,7 +266,7 @@ struct Engine {
     // ------------------------------------------------------------ kernel timers
     // Device time of the split / apply / gather kernels: event pairs on the
     // engine stream, resolved after the stream has passed them.
-    enum TimerKind { kTimeSplit = 0, kTimeApply = 1, kTimeGather = 2 };
+    enum TimerKind { kTimeSplit = 0, kTimeApply = 1, kTimeGather = 2, kTimeSerial = 3 };
     struct PendingTimer {
         cudaEvent_t a, b;
         int kind;
@@ -284,8 +308,10 @@ struct Engine {
             CK(cudaEventSynchronize(t.b));
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, t.a, t.b));
-            (t.kind == kTimeSplit ? timing.split_kernel_ms : t.kind == kTimeApply ? timing.apply_kernel_ms
-                                                                                 : timing.gather_kernel_ms) += ms;
+            (t.kind == kTimeSplit    ? timing.split_kernel_ms
+             : t.kind == kTimeApply  ? timing.apply_kernel_ms
+             : t.kind == kTimeSerial ? timing.serial_kernel_ms
+                                     : timing.gather_kernel_ms) += ms;
             ev_pool.push_back(t.a);
             ev_pool.push_back(t.b);
         }
@@ -434,7 +460,7 @@ struct Engine {
             cudaStreamSynchronize(ssplit);
             cudaStreamDestroy(ssplit);
         }
-        for (cudaEvent_t e : {ev_split_done, ev_k1_done})
+        for (cudaEvent_t e : {ev_split_done, ev_k1_done, ev_input})
             if (e) cudaEventDestroy(e);
         if (st) cudaStreamDestroy(st);
     }
@@ -686,21 +712,20 @@ struct Engine {
         split_smem = 2 * kSplitTile * 4 + fcfg.per_region * 16;  // two tile stages + per-slice tables
         with_w([&](auto w) {
             using W = decltype(w);
-            CK(cudaFuncSetAttribute(k_split<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(split_smem)));
-            CK(cudaFuncSetAttribute(k_slice_apply<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(smem, 16)));
-            CK(cudaFuncSetAttribute(k_slice_apply_bulk<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(2 * smem, 32)));
+            raise_smem_cap(k_split<W>, static_cast<int>(split_smem));
+            raise_smem_cap(k_slice_apply<W>, std::max(smem, 16));
+            raise_smem_cap(k_slice_apply_bulk<W>, std::max(2 * smem, 32));
         });
         if (const char* v = std::getenv("SRLA_STAMP_SPARSE")) stamp_sparse_max = static_cast<uint32_t>(std::atoi(v));
-        CK(cudaFuncSetAttribute(k_stamp_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(stamp_claim_bytes(fs))));
+        raise_smem_cap(k_stamp_warp, static_cast<int>(stamp_claim_bytes(fs)));
         if (nib) {
             if (nib_apply_smem() > 200 * 1024) return false;  // two stages must fit in shared memory
-            CK(cudaFuncSetAttribute(k_slice_apply_nib, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(nib_apply_smem())));
+            raise_smem_cap(k_slice_apply_nib, static_cast<int>(nib_apply_smem()));
         }
         with_w([&](auto w) {
             using W = decltype(w);
-            CK(cudaFuncSetAttribute(k_scan_bin<W, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmem));
-            CK(cudaFuncSetAttribute(k_scan_bin<W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBinSmem));
+            raise_smem_cap(k_scan_bin<W, 4>, kBinSmem);
+            raise_smem_cap(k_scan_bin<W, 0>, kBinSmem);
         });
         // bulk (TMA) slices need 16-byte slices and rows at least one slice long
         const uint64_t slice_words = 1ull << fs;
@@ -728,8 +753,7 @@ struct Engine {
                                                                 static_cast<uint8_t>((256 - dc.expired) & 0xFF));
         check_launch();
         launched();
-        CK(cudaFuncSetAttribute(k_slice_stamp, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                std::max<int>(32, int(2u << fcfg.shift))));
+        raise_smem_cap(k_slice_stamp, std::max<int>(32, int(2u << fcfg.shift)));
     }
 
     // Unpack a nibble table to a byte per recorder (an import carried values
@@ -1150,9 +1174,13 @@ struct Engine {
         trace("scan: K4 resolve");
         stats.flagged += nf;
         if (nf) {
+            const cudaEvent_t ts = timer_start();
             k_serial<<<1, 32, 0, st>>>(flagged.p, nf, fmask.p, off.p, posof.p, skey.p, sval.p, towner.p, status.p, fl_ins.p);
             check_launch();
             launched();
+            timer_stop(ts, kTimeSerial);
+            timing.serial_kernel_launches += 1;
+            timing.flagged_hosts += nf;
         }
         k_si_set<<<blocks(Hn), 256, 0, st>>>(hosts.p, Hn, status.p, dc, d_si);
         check_launch();
@@ -1285,12 +1313,29 @@ struct Engine {
         timing.end_slices += 1;
     }
 
-    void scan_batch(const srla_record* recs, uint64_t n, int on_device) {
+    // Device records are read on the engine's non-blocking streams: first
+    // wait (device-side) for the work the producer stream has queued.
+    cudaEvent_t ev_input = nullptr;
+    void wait_producer(cudaStream_t producer) {
+        if (!ev_input) CK(cudaEventCreateWithFlags(&ev_input, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_input, producer));
+        CK(cudaStreamWaitEvent(st, ev_input, 0));
+        CK(cudaStreamWaitEvent(sk, ev_input, 0));
+    }
+
+    void scan_batch(const srla_record* recs, uint64_t n, int on_device, cudaStream_t producer = cudaStreamLegacy) {
         if (!n) {
             join_eos();
             return;
         }
         if (on_device) {
+            cudaPointerAttributes pa{};
+            if (cudaPointerGetAttributes(&pa, recs) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+                pa.device != device) {
+                cudaGetLastError();
+                throw Error(SRLA_E_INVALID, "on_device records must be device memory on the engine's GPU");
+            }
+            wait_producer(producer);
             // a pending asynchronous end-of-slice overlaps this batch's first K1
             const bool overlap = overlap_on && eos_thread.joinable() && ev_cap != 0;
             if (!overlap) join_eos();
@@ -1482,7 +1527,7 @@ struct Engine {
             if (hdst) {
                 CK(cudaEventRecord(ev_sorted, st));
                 CK(cudaStreamWaitEvent(ds, ev_sorted, 0));
-                CK(cudaMemcpyAsync(hdst, sh, n * 4ull, cudaMemcpyDeviceToHost, ds));
+                CK(cudaMemcpyAsync(hdst, sh, n * 4ull, cudaMemcpyDefault, ds));  // host, or device (srla_shard)
             }
             const uint32_t parts = hdst && n >= (1u << 16) ? kReportParts : 1u;
             for (uint32_t c = 0; c < parts; ++c) {
@@ -1496,7 +1541,7 @@ struct Engine {
                 if (hdst) {
                     CK(cudaEventRecord(ev_part[c], st));
                     CK(cudaStreamWaitEvent(ds, ev_part[c], 0));
-                    CK(cudaMemcpyAsync(wdst + lo, weights.p + lo, (hi - lo) * 4ull, cudaMemcpyDeviceToHost, ds));
+                    CK(cudaMemcpyAsync(wdst + lo, weights.p + lo, (hi - lo) * 4ull, cudaMemcpyDefault, ds));
                 }
             }
             eos_mark("gathered");
@@ -2086,7 +2131,8 @@ srla_status srla_column_of(const srla_engine* e, uint32_t row, uint32_t aip, uin
     });
 }
 
-srla_status srla_scan_batch(srla_engine* e, const srla_record* recs, uint64_t n, int on_device,
+namespace {
+srla_status scan_batch_impl(srla_engine* e, const srla_record* recs, uint64_t n, int on_device, cudaStream_t producer,
                             uint32_t* pushed, uint64_t cap, uint64_t* n_pushed) {
     return guard([&] {
         std::lock_guard<std::mutex> lk(e->mu);
@@ -2094,13 +2140,25 @@ srla_status srla_scan_batch(srla_engine* e, const srla_record* recs, uint64_t n,
         if (n && !recs) throw srla::Error(SRLA_E_INVALID, "null records");
         x.collect_pushed = pushed != nullptr || n_pushed != nullptr;
         x.host_pushed.clear();
-        x.scan_batch(recs, n, on_device);
+        x.scan_batch(recs, n, on_device, producer);
         CK(cudaStreamSynchronize(x.st));
         if (n_pushed) *n_pushed = x.host_pushed.size();
         if (pushed)
             std::memcpy(pushed, x.host_pushed.data(), std::min<uint64_t>(cap, x.host_pushed.size()) * 4);
         x.collect_pushed = false;
     });
+}
+}  // namespace
+
+srla_status srla_scan_batch(srla_engine* e, const srla_record* recs, uint64_t n, int on_device,
+                            uint32_t* pushed, uint64_t cap, uint64_t* n_pushed) {
+    return scan_batch_impl(e, recs, n, on_device, cudaStreamLegacy, pushed, cap, n_pushed);
+}
+
+srla_status srla_scan_device(srla_engine* e, const srla_record* d_recs, uint64_t n, void* producer_stream,
+                             uint32_t* pushed, uint64_t cap, uint64_t* n_pushed) {
+    return scan_batch_impl(e, d_recs, n, 1, producer_stream ? static_cast<cudaStream_t>(producer_stream) : cudaStreamLegacy,
+                           pushed, cap, n_pushed);
 }
 
 srla_status srla_candidates(srla_engine* e, uint32_t* out, uint64_t cap, uint64_t* n) {

@@ -153,3 +153,181 @@ def allgather_report_entries(entries: np.ndarray, dist, device):
     merged = torch.cat([o[:c] for o, c in zip(outs, counts)])
     host = merged[:, :4].contiguous().view(torch.int32).reshape(-1).to(torch.int64) & 0xFFFFFFFF
     return merged[torch.argsort(host)]
+
+
+# ---------------------------------------------------------------- C-ABI sharded pipeline (srla_shard_*)
+
+import ctypes as C  # noqa: E402
+
+OWNED, RANGE = 0, 1  # SRLA_SHARD_OWNED / SRLA_SHARD_RANGE
+
+_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+_ALLTOALLV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_void_p,
+                         C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_void_p)
+
+
+class CTransport(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_uint32), ("world", C.c_uint32), ("host_memory", C.c_int),
+                ("allgather", _ALLGATHER), ("alltoallv", _ALLTOALLV)]
+
+
+def _lib():
+    from .srla import load_library
+    lib = load_library()
+    if not getattr(lib, "_shard_sigs", False):
+        vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+        for name, res, args in (
+                ("srla_nccl_unique_id", i32, [vp]),
+                ("srla_transport_nccl", i32, [vp, u32, u32, i32, C.POINTER(CTransport)]),
+                ("srla_transport_nccl_destroy", i32, [C.POINTER(CTransport)]),
+                ("srla_shard_create", i32, [vp, i32, C.POINTER(CTransport), C.POINTER(vp)]),
+                ("srla_shard_destroy", i32, [vp]),
+                ("srla_shard_engine", i32, [vp, C.POINTER(vp)]),
+                ("srla_shard_last_report", i32, [vp, vp, u64, C.POINTER(u64)]),
+                ("srla_shard_process_slice", i32, [vp, u64, vp, u64, i32, i32, i32, vp, u64, C.POINTER(u64),
+                                                   C.POINTER(u64)])):
+            fn = getattr(lib, name)
+            fn.restype, fn.argtypes = res, args
+        lib._shard_sigs = True
+    return lib
+
+
+class GlooTransport:
+    """srla_transport over a torch.distributed process group on host memory
+    (gloo): the library stages device data through pinned buffers. For tests
+    and for ranks that share a GPU (NCCL refuses two ranks on one device)."""
+
+    def __init__(self, dist):
+        import torch
+        self.dist, self.torch = dist, torch
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+        def allgather(ctx, send, recv, nbytes, stream):
+            try:
+                src = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), (max(1, nbytes),))[:nbytes]
+                t = torch.from_numpy(src.copy())
+                outs = [torch.empty_like(t) for _ in range(self.world)]
+                dist.all_gather(outs, t)
+                if nbytes:
+                    dst = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)), (nbytes * self.world,))
+                    dst[:] = torch.cat(outs).numpy()
+                return 0
+            except Exception as e:  # noqa: BLE001 (reported as a transport failure)
+                print("gloo allgather:", e)
+                return 1
+
+        def alltoallv(ctx, send, sb, so, recv, rb, ro, stream):
+            try:
+                W = self.world
+                sbytes = [sb[j] for j in range(W)]
+                soff = [so[j] for j in range(W)]
+                total = soff[-1] + sbytes[-1] if W else 0
+                src = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), (max(1, total),))[:total].copy()
+                # variable all-to-all as an all-gather of (sizes, payload)
+                mx = torch.tensor([total], dtype=torch.int64)
+                mxs = [torch.zeros_like(mx) for _ in range(W)]
+                dist.all_gather(mxs, mx)
+                cap = max(int(m.item()) for m in mxs + [torch.tensor([1])])
+                pay = torch.zeros(cap, dtype=torch.uint8)
+                pay[:total] = torch.from_numpy(src)
+                meta = torch.tensor(sbytes + soff, dtype=torch.int64)
+                pays = [torch.empty_like(pay) for _ in range(W)]
+                metas = [torch.empty_like(meta) for _ in range(W)]
+                dist.all_gather(pays, pay)
+                dist.all_gather(metas, meta)
+                rtotal = ro[W - 1] + rb[W - 1]
+                dst = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)), (max(1, rtotal),))
+                for i in range(W):
+                    m = metas[i].numpy()
+                    nb, off = int(m[self.rank]), int(m[W + self.rank])
+                    assert nb == rb[i]
+                    dst[ro[i]:ro[i] + nb] = pays[i].numpy()[off:off + nb]
+                return 0
+            except Exception as e:  # noqa: BLE001
+                print("gloo alltoallv:", e)
+                return 1
+
+        self._cb = (_ALLGATHER(allgather), _ALLTOALLV(alltoallv))
+        self.c = CTransport(None, self.rank, self.world, 1, self._cb[0], self._cb[1])
+
+
+class NcclTransport:
+    """srla_transport_nccl: the library's own NCCL communicator (one rank per
+    GPU); the unique id travels over the caller's process group."""
+
+    def __init__(self, dist, device):
+        from .srla import _check
+        lib = _lib()
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        uid = (C.c_uint8 * 128)()
+        if self.rank == 0:
+            _check(lib.srla_nccl_unique_id(uid))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+        self.c = CTransport()
+        _check(lib.srla_transport_nccl(uid, self.rank, self.world, device, C.byref(self.c)))
+
+    def close(self):
+        if self.c.ctx:
+            _lib().srla_transport_nccl_destroy(C.byref(self.c))
+
+    def __del__(self):
+        self.close()
+
+
+class EngineShard:
+    """One rank of the owner-partitioned pipeline through the C ABI
+    (srla_shard_*): scan, report all-gather merged by host on the device, slide."""
+
+    def __init__(self, cfg, transport, device: int = 0):
+        from .srla import _check
+        lib = _lib()
+        self.cfg, self.transport, self.device = cfg, transport, device
+        h = C.c_void_p()
+        c = cfg.to_c()
+        _check(lib.srla_shard_create(C.byref(c), device, C.byref(transport.c), C.byref(h)))
+        self._h = h
+        e = C.c_void_p()
+        _check(lib.srla_shard_engine(h, C.byref(e)))
+        from .srla import EstimatorArray
+        self.engine = EstimatorArray.__new__(EstimatorArray)  # a view: the shard owns the engine
+        self.engine.cfg, self.engine.device, self.engine._h = cfg, device, e
+        self.engine.word_bytes = 1 if cfg.recorder_bits <= 8 else 2 if cfg.recorder_bits <= 16 else 4
+        self.engine.wdtype = {1: np.uint8, 2: np.uint16, 4: np.uint32}[self.engine.word_bytes]
+        self.engine.close = lambda: None
+        self.cap = 1 << 12
+        self.out = np.empty(self.cap, ENTRY_DTYPE)
+
+    def process_slice(self, slice_id, recs, mode=OWNED, want_report=True):
+        """-> (merged report or None, records this rank scanned)."""
+        from .srla import E_CAPACITY, _as_records, _check, _is_torch_cuda
+        if _is_torch_cuda(recs):
+            ptr, n, on_dev = recs.data_ptr(), recs.shape[0], 1
+        else:
+            recs = _as_records(recs)
+            ptr, n, on_dev = recs.ctypes.data, recs.shape[0], 0
+        lib = _lib()
+        n_out, n_scan = C.c_uint64(), C.c_uint64()
+        rc = lib.srla_shard_process_slice(self._h, slice_id, C.c_void_p(ptr), n, on_dev, mode, int(want_report),
+                                          C.c_void_p(self.out.ctypes.data), self.cap, C.byref(n_out), C.byref(n_scan))
+        if rc == E_CAPACITY:  # the slice completed; fetch the merged report with room
+            self.reserve(n_out.value)
+            _check(lib.srla_shard_last_report(self._h, C.c_void_p(self.out.ctypes.data), self.cap, C.byref(n_out)))
+        else:
+            _check(rc)
+        due = want_report and slice_id + 1 >= self.cfg.window
+        return (self.out[: n_out.value].copy() if due else None), n_scan.value
+
+    def reserve(self, entries):
+        if entries > self.cap:
+            self.cap = max(entries, 2 * self.cap)
+            self.out = np.empty(self.cap, ENTRY_DTYPE)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().srla_shard_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()

@@ -70,7 +70,8 @@ class CTiming(C.Structure):
                 ("apply_stream_bytes", C.c_uint64), ("gather_kernel_ms", C.c_double),
                 ("gather_kernel_launches", C.c_uint64), ("gather_bytes", C.c_uint64),
                 ("sync_wait_ms", C.c_double), ("syncs", C.c_uint64), ("alloc_ms", C.c_double),
-                ("allocs", C.c_uint64)]
+                ("allocs", C.c_uint64), ("serial_kernel_ms", C.c_double),
+                ("serial_kernel_launches", C.c_uint64), ("flagged_hosts", C.c_uint64)]
 
 
 class CPlant(C.Structure):
@@ -140,6 +141,7 @@ def load_library(path: str = LIB_PATH):
         "srla_parse_srlt": (i32, [vp, u64, vp, C.POINTER(u64), vp]),
         "srla_orient_records": (i32, [vp, u64, u32, u32, vp, C.POINTER(u64), C.POINTER(COrientStats), vp]),
         "srla_slice_bounds": (i32, [vp, u64, u32, vp, u64, C.POINTER(u64), vp]),
+        "srla_scan_device": (i32, [vp, vp, u64, vp, vp, u64, C.POINTER(u64)]),
         "srla_state_blocks": (i32, [vp, u32, i32, vp, u64, C.POINTER(u64)]),
         "srla_block_sums": (i32, [vp, u64, vp, u64, vp]),
     }
@@ -159,7 +161,9 @@ EXPORTED_SYMBOLS = (
     "srla_timing_get", "srla_timing_reset", "srla_partition_records", "srla_owner_of",
     "srla_end_slice_async", "srla_end_slice_wait", "srla_end_slice_compact",
     "srla_parse_srlt", "srla_orient_records", "srla_slice_bounds", "srla_device_alloc", "srla_device_free",
-    "srla_copy_to_device", "srla_state_blocks", "srla_block_sums",
+    "srla_copy_to_device", "srla_state_blocks", "srla_block_sums", "srla_scan_device",
+    "srla_nccl_unique_id", "srla_transport_nccl", "srla_transport_nccl_destroy", "srla_shard_create",
+    "srla_shard_destroy", "srla_shard_engine", "srla_shard_last_report", "srla_shard_process_slice",
 )
 
 
@@ -244,27 +248,42 @@ class EstimatorArray:
         return out.value
 
     # -- scan
-    def scan(self, recs) -> None:
-        """scan_ip_pair over every record in order (pushes go to the engine's candidate list)."""
+    def _device_records(self, t):
+        """Validate a CUDA record tensor: (n, 3) int32/uint32, contiguous, on the engine's GPU."""
+        import torch
+        if t.dtype not in (torch.int32, getattr(torch, "uint32", torch.int32)):
+            raise ValueError(f"device records must be int32/uint32, got {t.dtype}")
+        if t.dim() != 2 or t.shape[1] != 3:
+            raise ValueError(f"device records must have shape (n, 3), got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise ValueError("device records must be contiguous")
+        if t.device.index != self.device:
+            raise ValueError(f"records on cuda:{t.device.index}, engine on cuda:{self.device}")
+        return t.data_ptr(), t.shape[0], torch.cuda.current_stream(t.device).cuda_stream
+
+    def _scan(self, recs, out):
+        npushed = C.c_uint64()
+        cap = len(out) if out is not None else 0
         if _is_torch_cuda(recs):
-            ptr, n, on_dev = recs.data_ptr(), recs.shape[0], 1
+            ptr, n, stream = self._device_records(recs)
+            _check(_lib.srla_scan_device(self._h, C.c_void_p(ptr), n, C.c_void_p(stream), _ptr(out), cap,
+                                         C.byref(npushed) if out is not None else None))
         else:
             recs = _as_records(recs)
-            ptr, n, on_dev = recs.ctypes.data, recs.shape[0], 0
-        _check(_lib.srla_scan_batch(self._h, C.c_void_p(ptr), n, on_dev, None, 0, None))
+            _check(_lib.srla_scan_batch(self._h, C.c_void_p(recs.ctypes.data), recs.shape[0], 0, _ptr(out), cap,
+                                        C.byref(npushed) if out is not None else None))
+        return npushed.value
+
+    def scan(self, recs) -> None:
+        """scan_ip_pair over every record in order (pushes go to the engine's candidate list).
+        CUDA tensors are read after the work queued on torch's current stream."""
+        self._scan(recs, None)
 
     def scan_collect(self, recs) -> np.ndarray:
         """Scan and return pushes (bounded by the number of records)."""
-        if _is_torch_cuda(recs):
-            ptr, n, on_dev = recs.data_ptr(), recs.shape[0], 1
-        else:
-            recs = _as_records(recs)
-            ptr, n, on_dev = recs.ctypes.data, recs.shape[0], 0
-        out = np.empty(max(1, n), np.uint32)
-        npushed = C.c_uint64()
-        _check(_lib.srla_scan_batch(self._h, C.c_void_p(ptr), n, on_dev, _ptr(out), len(out),
-                                    C.byref(npushed)))
-        return out[: npushed.value].copy()
+        out = np.empty(max(1, recs.shape[0] if _is_torch_cuda(recs) else len(_as_records(recs))), np.uint32)
+        n = self._scan(recs, out)
+        return out[:n].copy()
 
     def scan_ip_pair(self, aip: int, bip: int) -> np.ndarray:
         return self.scan_collect(np.array([[0, aip, bip]], np.uint32))

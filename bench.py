@@ -318,7 +318,6 @@ def run_engine(args):
     import torch
 
     from paper_1803_10369_b200 import srla
-    from paper_1803_10369_b200.shard import allgather_report_compact, allgather_report_entries
 
     rank, world, local = env_rank()
     # one process per GPU; SRLA_BENCH_BACKEND=gloo lets several ranks share a
@@ -337,6 +336,17 @@ def run_engine(args):
 
     w = Workload(args.workload, args, rank, world, local)
     eng, cfg, slices, nres = w.eng, w.cfg, w.slices, w.nres
+    shard = None
+    if world > 1:
+        # the C ABI's sharded pipeline: the rank's engine + the report
+        # all-gather merged by host on the device (srla_shard_*), over the
+        # library's NCCL communicator (or gloo when ranks share a GPU)
+        from paper_1803_10369_b200.shard import OWNED, EngineShard, GlooTransport, NcclTransport
+        del w.eng, eng
+        transport = NcclTransport(dist, local) if backend == "nccl" else GlooTransport(dist)
+        shard = EngineShard(cfg, transport, device=local)
+        shard.reserve(w.rep_cap * world)
+        eng = shard.engine
     st = torch.cuda.ExternalStream(eng.stream_handle())
 
     def pinned(nbytes):
@@ -350,9 +360,6 @@ def run_engine(args):
     comp_est, comp_flags = np.empty(w.L, np.float64), np.empty(w.L, np.uint8)
     rep_buf = pinned_entries(w.rep_cap)
 
-    def allgather_report(entries):  # merged on the device (N > 1)
-        return entries if world == 1 else allgather_report_entries(entries, dist, comm_dev)
-
     def end_slice(sid):
         if args.handoff == "compact":  # hosts + weights (8 B/entry) + the window's Eq. 9 table
             return eng.end_slice_compact(sid, comp_hosts, comp_w, comp_est, comp_flags)
@@ -362,18 +369,11 @@ def run_engine(args):
         return n.value, nr.value
 
     def step(sid):
+        if shard is not None:  # scan + end-of-slice + merged report, one collective call
+            rep, _ = shard.process_slice(sid, slices[sid % nres], mode=OWNED)
+            return 0 if rep is None else len(rep)
         eng.scan(slices[sid % nres])
         n, _ = end_slice(sid)
-        if world > 1:
-            if args.handoff == "compact":
-                h = torch.from_numpy(comp_hosts[:n].view(np.int32)).to(comm_dev, non_blocking=True)
-                wt = torch.from_numpy(comp_w[:n].view(np.int32)).to(comm_dev, non_blocking=True)
-                mask = 0xFFFFFFFF
-                allgather_report_compact(h.to(torch.int64) & mask, wt.to(torch.int64) & mask,
-                                         torch.from_numpy(comp_est).to(comm_dev),
-                                         torch.from_numpy(comp_flags).to(comm_dev), dist)
-            else:
-                allgather_report(rep_buf[:n])
         return n
 
     sid = 0
@@ -448,18 +448,21 @@ def run_engine(args):
         torch.cuda.synchronize()
         d2h = 0
         t0 = time.perf_counter()
-        pending = None
-        for i in range(args.steps):
-            eng.scan(host[(sid + i) % nh])
-            if pending is not None:
-                n, _ = eng.end_slice_wait()
-                allgather_report(bufs[pending][:n])
-                d2h += n * srla.ENTRY_DTYPE.itemsize
-            eng.end_slice_async(sid + i, bufs[i % 2])
-            pending = i % 2
-        n, _ = eng.end_slice_wait()
-        allgather_report(bufs[pending][:n])
-        d2h += n * srla.ENTRY_DTYPE.itemsize
+        if shard is not None:  # srla_shard_process_slice with host records: H2D, scan, merged report D2H
+            for i in range(args.steps):
+                rep, _ = shard.process_slice(sid + i, host[(sid + i) % nh], mode=OWNED)
+                d2h += 0 if rep is None else rep.nbytes
+        else:
+            pending = None
+            for i in range(args.steps):
+                eng.scan(host[(sid + i) % nh])
+                if pending is not None:
+                    n, _ = eng.end_slice_wait()
+                    d2h += n * srla.ENTRY_DTYPE.itemsize
+                eng.end_slice_async(sid + i, bufs[i % 2])
+                pending = i % 2
+            n, _ = eng.end_slice_wait()
+            d2h += n * srla.ENTRY_DTYPE.itemsize
         sid += args.steps
         eng.synchronize()
         if dist:
@@ -471,7 +474,8 @@ def run_engine(args):
             el = t.item()
         e2e = {"value": packets / el, "unit": "packets/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h / args.steps),
-               "api": "srla_scan_batch(host, pinned) + srla_end_slice_async/wait"}
+               "api": "srla_shard_process_slice(host records)" if shard is not None else
+               "srla_scan_batch(host, pinned) + srla_end_slice_async/wait"}
         del host
 
     # the reference on this box's host cores, steady state on the same slices
@@ -495,6 +499,9 @@ def run_engine(args):
         del eng, w
         torch.cuda.empty_cache()
         c3 = run_c3(args, local, peak, peak_src)
+    if shard is not None:
+        shard.close()
+        transport.close() if hasattr(transport, "close") else None
 
     if rank == 0:
         line = {
@@ -506,7 +513,9 @@ def run_engine(args):
                        "report_handoff": "srla_end_slice_compact: host+weight per entry and the Eq. 9 table"
                        if args.handoff == "compact" else "srla_end_slice: 24-byte srla_entry per entry",
                        "l2": "inputs larger than L2 (1.2 GB per slice); no flush",
-                       "parallelism": f"owner-partitioned x{world} ({backend})" if world > 1 else "1 GPU"},
+                       "parallelism": f"owner-partitioned x{world}: srla_shard_* (records arrive owner-sharded; "
+                                      f"report all-gather over {'NCCL' if backend == 'nccl' else 'gloo, ranks sharing a GPU'})"
+                       if world > 1 else "1 GPU"},
             "end_of_slice_ms": {"device_median": statistics.median(eos_dev),
                                 "device_p99": sorted(eos_dev)[min(len(eos_dev) - 1, int(0.99 * len(eos_dev)))],
                                 "device_max": max(eos_dev), "samples": len(eos_dev),

@@ -213,6 +213,10 @@ struct srla_shard {
     std::vector<double> est;
     std::vector<uint8_t> flags;
     uint64_t last_total = 0;  // entries of the last merged report (kept in `entries`)
+    cudaEvent_t ev_in = nullptr;
+    ~srla_shard() {
+        if (ev_in) cudaEventDestroy(ev_in);
+    }
 
     // a collective through the transport, staged through pinned host buffers
     // when the transport works on host memory
@@ -539,6 +543,11 @@ srla_status srla_shard_process_slice(srla_shard* s, uint64_t slice_id, const srl
         SK(cudaSetDevice(s->device));
         const srla_record* d = recs;
         uint64_t m = n;
+        if (on_device && n) {  // device records: ordered after the legacy default stream (srla_scan_batch's contract)
+            if (!s->ev_in) SK(cudaEventCreateWithFlags(&s->ev_in, cudaEventDisableTiming));
+            SK(cudaEventRecord(s->ev_in, cudaStreamLegacy));
+            SK(cudaStreamWaitEvent(s->st, s->ev_in, 0));
+        }
         if (!on_device && n) {  // host records: one staged copy
             s->hstage.ensure(n * 12);
             SK(cudaMemcpyAsync(s->hstage.p, recs, n * 12, cudaMemcpyHostToDevice, s->st));

@@ -193,6 +193,18 @@ srla_status srla_row_bytes(const srla_engine* e, int kind, uint64_t* bytes);
 srla_status srla_export_row(srla_engine* e, uint32_t row, int kind, void* buf, uint64_t bytes);
 srla_status srla_import_row(srla_engine* e, uint32_t row, int kind, const void* buf,
                             uint64_t bytes);
+/* Byte range [offset, offset + bytes) of a raw row in the same layout, so a
+ * 16 GiB row (2^24 columns) streams to or from a snapshot file in bounded
+ * pieces (snapshot.hpp:117-120, 176-181). Packed 4-bit tables need an even
+ * offset and size. Pinned buffers (srla_host_alloc) are copied by DMA
+ * directly, pageable ones through the engine's pinned staging. Epoch-stamp
+ * rows keep their histograms exact across a partial import. */
+srla_status srla_export_range(srla_engine* e, uint32_t row, int kind, uint64_t offset, void* buf, uint64_t bytes);
+srla_status srla_import_range(srla_engine* e, uint32_t row, int kind, uint64_t offset, const void* buf,
+                              uint64_t bytes);
+/* Page-locked host memory (cudaMallocHost) for callers without CUDA headers. */
+srla_status srla_host_alloc(uint64_t bytes, void** out);
+srla_status srla_host_free(void* p);
 
 /* Block digests of one raw row (indicator_row / rough_row / linear_row,
  * sea.hpp:341-346) in the reference's little-endian byte layout, computed on

@@ -187,21 +187,41 @@ class DetectPipeline {
         total_scan_ms_ += scan_ms;
         pairs_ += n;
         ++slices_;
+        // report + slide as ONE fused end-of-slice (srla_end_slice: the
+        // window's fill counts come out of the same pass that ages the table,
+        // and the entries are mapped on the device). The report handed to the
+        // sink is the reference's; the sketch it could be queried through has
+        // already slid.
         const uint32_t k = cfg_.sea.window;
-        if (slice_id + 1 >= k && sink) {
-            WindowReport report = sea_.engine_report(slice_id + 1 - k);
+        const bool due = slice_id + 1 >= k && static_cast<bool>(sink);
+        const auto t1 = std::chrono::steady_clock::now();
+        uint64_t cands = 0;
+        if (due) {
+            const srla_status s = srla_candidates(sea_.eng(), nullptr, 0, &cands);
+            if (s != SRLA_OK && s != SRLA_E_CAPACITY) detail::raise_status(s, "srla_candidates");
+            if (entries_.size() < cands) entries_.resize(cands + cands / 4);
+        }
+        uint64_t n_out = 0, kept = 0;
+        detail::check(srla_end_slice(sea_.eng(), slice_id, due ? 1 : 0, entries_.data(), entries_.size(), &n_out, &kept),
+                      "srla_end_slice");
+        sea_.st_->mirror_valid = false;
+        csip_valid_ = false;
+        if (due) {
+            WindowReport report;
+            report.window_start = slice_id + 1 - k;
+            report.window = k;
+            report.entries.reserve(n_out);
+            for (uint64_t i = 0; i < n_out; ++i) report.entries.push_back(detail::to_entry(entries_[i]));
             report.scan_ms = scan_ms;
+            report.estimate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
             total_estimate_ms_ += report.estimate_ms;
             sink(report);
         }
-        uint64_t kept = 0;
-        detail::check(srla_slide(sea_.eng(), &kept), "srla_slide");
-        sea_.st_->mirror_valid = false;
-        csip_valid_ = false;
     }
 
     RunConfig cfg_;
     EstimatorArray<W> sea_;
+    std::vector<srla_entry> entries_;  // report hand-off buffer, reused across slices
     mutable CandidateList csip_;
     mutable bool csip_valid_ = false;
     OrientStats stats_;

@@ -289,6 +289,10 @@ class EstimatorArray {
 
   private:
     friend class DetectPipeline<W>;
+    template <RecorderWord V>
+    friend void save_snapshot(const EstimatorArray<V>&, const CandidateList&, const std::string&);
+    template <RecorderWord V>
+    friend std::pair<EstimatorArray<V>, CandidateList> load_snapshot(const std::string&, int);
 
     struct Mirror {
         std::vector<std::vector<uint16_t>> ind;

@@ -1,9 +1,11 @@
 // sspread/snapshot.hpp — drop-in "SSEA" v1 sketch snapshots
-// (/root/reference/proj/include/sspread/snapshot.hpp): same byte layout, read
-// and written through the row spans, so a GPU sketch and a CPU reference sketch
-// exchange state bit-exactly.
+// (/root/reference/proj/include/sspread/snapshot.hpp): the same bytes as the
+// reference's save_snapshot (tests/test_snapshot_bytes.py), rows streamed
+// straight between HBM and the file in bounded pinned pieces, so a GPU sketch
+// and a CPU reference sketch exchange state bit-exactly.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <fstream>
@@ -89,6 +91,24 @@ class LeReader {
 };
 }  // namespace detail
 
+namespace detail {
+// Pinned staging for streaming rows between HBM and a snapshot file: rows move
+// in bounded pieces (a 2^24-column linear row is 16 GiB), by DMA.
+struct PinnedChunk {
+    static constexpr uint64_t kBytes = 64ull << 20;
+    void* p = nullptr;
+    PinnedChunk() { check(srla_host_alloc(kBytes, &p), "srla_host_alloc"); }
+    ~PinnedChunk() { srla_host_free(p); }
+    PinnedChunk(const PinnedChunk&) = delete;
+    PinnedChunk& operator=(const PinnedChunk&) = delete;
+    char* data() const { return static_cast<char*>(p); }
+};
+}  // namespace detail
+
+// snapshot.hpp:109-136. The header and candidate list are written as the
+// reference writes them; every row streams from the device (x86 words are
+// already little-endian, the reference's explicit packing), through one
+// pinned 64 MiB piece at a time — no host mirror of the sketch.
 template <RecorderWord W>
 void save_snapshot(const EstimatorArray<W>& sea, const CandidateList& csip, const std::string& path) {
     const SeaConfig& c = sea.config();
@@ -99,16 +119,25 @@ void save_snapshot(const EstimatorArray<W>& sea, const CandidateList& csip, cons
     for (uint32_t v : {c.rows, c.cols, c.rough_slots, c.linear_slots, c.recorder_bits, c.window, c.theta}) w.u32(v);
     w.f64(c.fill_ratio);
     w.u64(c.seed);
-    for (uint32_t i = 0; i < c.rows; ++i) {
-        w.words<uint16_t>(sea.indicator_row(i));
-        w.words<W>(sea.rough_row(i));
-        w.words<W>(sea.linear_row(i));
-    }
-    w.u64(csip.size());
-    for (uint32_t h : csip.hosts()) w.u32(h);
     std::ofstream out(path, std::ios::binary | std::ios::trunc);
     if (!out) throw InputError("cannot open snapshot for writing: " + path);
     out.write(w.bytes().data(), static_cast<std::streamsize>(w.bytes().size()));
+    sea.to_device();  // a span-modified mirror is the current state
+    detail::PinnedChunk buf;
+    for (uint32_t i = 0; i < c.rows; ++i)
+        for (int kind : {SRLA_INDICATOR, SRLA_ROUGH, SRLA_LINEAR}) {
+            uint64_t bytes = 0;
+            detail::check(srla_row_bytes(sea.eng(), kind, &bytes), "srla_row_bytes");
+            for (uint64_t off = 0; off < bytes; off += detail::PinnedChunk::kBytes) {
+                const uint64_t m = std::min(detail::PinnedChunk::kBytes, bytes - off);
+                detail::check(srla_export_range(sea.eng(), i, kind, off, buf.data(), m), "srla_export_range");
+                out.write(buf.data(), static_cast<std::streamsize>(m));
+            }
+        }
+    detail::LeWriter tail;
+    tail.u64(csip.size());
+    for (uint32_t h : csip.hosts()) tail.u32(h);
+    out.write(tail.bytes().data(), static_cast<std::streamsize>(tail.bytes().size()));
     if (!out) throw InputError("write failure on snapshot: " + path);
 }
 
@@ -149,11 +178,19 @@ std::pair<EstimatorArray<W>, CandidateList> load_snapshot(const std::string& pat
                          std::to_string(sizeof(W)));
     EstimatorArray<W> sea(h.config, device);
     detail::LeReader r(in);
-    for (uint32_t i = 0; i < h.config.rows; ++i) {
-        r.words(sea.indicator_row(i), "indicators");
-        r.words(sea.rough_row(i), "rough recorders");
-        r.words(sea.linear_row(i), "linear recorders");
-    }
+    detail::PinnedChunk buf;
+    for (uint32_t i = 0; i < h.config.rows; ++i)
+        for (int kind : {SRLA_INDICATOR, SRLA_ROUGH, SRLA_LINEAR}) {
+            const char* what = kind == SRLA_INDICATOR ? "indicators" : kind == SRLA_ROUGH ? "rough recorders"
+                                                                                          : "linear recorders";
+            uint64_t bytes = 0;
+            detail::check(srla_row_bytes(sea.eng(), kind, &bytes), "srla_row_bytes");
+            for (uint64_t off = 0; off < bytes; off += detail::PinnedChunk::kBytes) {
+                const uint64_t m = std::min(detail::PinnedChunk::kBytes, bytes - off);
+                r.raw(buf.data(), m, what);
+                detail::check(srla_import_range(sea.eng(), i, kind, off, buf.data(), m), "srla_import_range");
+            }
+        }
     const uint64_t n = r.u64("candidate count");
     CandidateList csip;
     for (uint64_t i = 0; i < n; ++i) csip.insert(r.u32("candidate"));

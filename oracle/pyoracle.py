@@ -150,6 +150,7 @@ class Checker:
         }
         if self.prefix == "ref":  # reference-only: parallel slice generator, record-order flow
             sigs.update({
+                "pipeline_save_snapshot": (i32, [vp, C.c_char_p, C.c_char_p, C.c_size_t]),
                 "generate_slice": (u64, [C.POINTER(OrcSpec), u64, u32, vp, C.c_char_p, C.c_size_t]),
                 "flow_create": (vp, [C.POINTER(OrcConfig), u32, C.c_char_p, C.c_size_t]),
                 "flow_destroy": (None, [vp]),
@@ -420,6 +421,12 @@ class Pipeline:
         if not rep.value:
             return None
         return {k: v[: ne.value].copy() for k, v in out.items()}
+
+    def save_snapshot(self, path: str):
+        """The reference's save_snapshot(sketch, candidates, path) (reference checker only)."""
+        err = C.create_string_buffer(256)
+        if self.chk.f("pipeline_save_snapshot")(self.h, path.encode(), err, 256):
+            raise OSError(err.value.decode())
 
     @property
     def scan_ms(self):

@@ -18,6 +18,7 @@
 #include "sspread/generator.hpp"
 #include "sspread/pipeline.hpp"
 #include "sspread/sea.hpp"
+#include "sspread/snapshot.hpp"
 #include "sspread/trace.hpp"
 
 #include "srla_oracle.h"  // shared struct layouts (orc_config, orc_spec, kinds)
@@ -162,6 +163,7 @@ struct PipeBase {
     virtual void cands(uint32_t* out) = 0;
     virtual double scan_ms() = 0;
     virtual double est_ms() = 0;
+    virtual void save(const char* path) = 0;
 };
 
 template <RecorderWord W>
@@ -192,6 +194,7 @@ struct Pipe final : PipeBase {
     }
     double scan_ms() override { return p.total_scan_ms(); }
     double est_ms() override { return p.total_estimate_ms(); }
+    void save(const char* path) override { save_snapshot(p.sketch(), p.candidates(), path); }  // snapshot.hpp:109-136
 };
 
 SeaBase* S(void* h) { return static_cast<SeaBase*>(h); }
@@ -385,6 +388,16 @@ uint64_t ref_pipeline_ncand(void* p) { return static_cast<PipeBase*>(p)->ncand()
 void ref_pipeline_candidates(void* p, uint32_t* out) { static_cast<PipeBase*>(p)->cands(out); }
 double ref_pipeline_scan_ms(void* p) { return static_cast<PipeBase*>(p)->scan_ms(); }
 double ref_pipeline_estimate_ms(void* p) { return static_cast<PipeBase*>(p)->est_ms(); }
+// the reference's own save_snapshot of the pipeline's sketch and candidate list
+int ref_pipeline_save_snapshot(void* p, const char* path, char* err, size_t errlen) {
+    try {
+        static_cast<PipeBase*>(p)->save(path);
+        return 0;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return 1;
+    }
+}
 
 uint64_t ref_generate(const orc_spec* s, uint32_t* out, char* err, size_t errlen) {
     try {

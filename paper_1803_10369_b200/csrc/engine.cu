@@ -29,6 +29,7 @@
 #include "epoch.cuh"
 #include "nibble.cuh"
 #include "digest.cuh"
+#include "order.cuh"
 #include "srla.h"
 
 namespace srla {
@@ -214,6 +215,59 @@ struct Engine {
     std::vector<uint8_t> lut_has, lut_sup;
     bool collect_pushed = false;
     srla_stats stats{};
+
+    // ordering phase on device counts (order.cuh); SRLA_ORDER=legacy selects
+    // the sorted, host-synchronised path (kernels.cuh K2..K4f) throughout
+    bool fast_order = [] { const char* v = std::getenv("SRLA_ORDER"); return !(v && std::string(v) == "legacy"); }();
+    DevBuf<uint32_t> octr, ht_vals, tt_vals, hl, tl, host_a, host_p, bm_new, bm_push, bits_cnt, newlist, pushlist;
+    DevBuf<unsigned long long> ht_keys, tt_keys;
+    DevBuf<uint64_t> host_f;
+    DevBuf<uint8_t> ostatus;
+    PinBuf<uint32_t> pin_octr;
+    uint32_t order_cap = 0;
+    uint64_t ht_mask = 0, tt_mask = 0;
+
+    void setup_order(uint32_t cap) {
+        if (cap <= order_cap) return;
+        uint64_t hs = 1024, ts = 1024;
+        while (hs < 2ull * cap) hs <<= 1;
+        while (ts < 2ull * cap * std::min<uint32_t>(cfg.rows, 8)) ts <<= 1;
+        octr.ensure(kOcCount);
+        pin_octr.ensure(kOcCount);
+        ht_keys.ensure(hs); ht_vals.ensure(hs); tt_keys.ensure(ts); tt_vals.ensure(ts);
+        hl.ensure(cap); tl.ensure(uint64_t(cap) * std::min<uint32_t>(cfg.rows, 8));
+        host_a.ensure(cap); host_p.ensure(cap); host_f.ensure(cap); ostatus.ensure(cap);
+        newlist.ensure(cap); pushlist.ensure(cap);
+        xkeys.ensure(cap);
+        const uint64_t words = (uint64_t(kChunk) + 31) / 32;
+        bm_new.ensure(words); bm_push.ensure(words);
+        bits_cnt.ensure((words + kBitsWords - 1) / kBitsWords + 1);
+        CK(cudaMemsetAsync(ht_keys.p, 0, ht_keys.cap * 8, st));
+        CK(cudaMemsetAsync(ht_vals.p, 0xFF, ht_vals.cap * 4, st));
+        CK(cudaMemsetAsync(tt_keys.p, 0, tt_keys.cap * 8, st));
+        CK(cudaMemsetAsync(tt_vals.p, 0xFF, tt_vals.cap * 4, st));
+        CK(cudaMemsetAsync(bm_new.p, 0, bm_new.cap * 4, st));
+        CK(cudaMemsetAsync(bm_push.p, 0, bm_push.cap * 4, st));
+        ht_mask = hs - 1;
+        tt_mask = ts - 1;
+        order_cap = cap;
+    }
+
+    OrderBufs order_bufs(bool collect) {
+        return OrderBufs{octr.p, ht_keys.p, ht_vals.p, ht_mask, hl.p, tt_keys.p, tt_vals.p, tt_mask, tl.p,
+                         host_a.p, host_p.p, host_f.p, ostatus.p, bm_new.p, collect ? bm_push.p : nullptr, order_cap};
+    }
+
+    // ordered compaction of a packet bitmap into `out` (device count -> octr[ctr_idx])
+    void emit_bitmap(uint32_t* bm, uint32_t n, const uint32_t* d_recs, uint32_t* out, uint32_t ctr_idx) {
+        const uint32_t words = (n + 31) / 32;
+        const uint32_t nb = (words + kBitsWords - 1) / kBitsWords;
+        k_bits_count<<<nb, kBitsThreads, 0, st>>>(bm, words, bits_cnt.p);
+        k_bits_scan<<<1, 1024, 0, st>>>(bits_cnt.p, nb, octr.p + ctr_idx);
+        k_bits_emit<<<nb, kBitsThreads, 0, st>>>(bm, words, bits_cnt.p, d_recs, out);
+        check_launch();
+        launched(3);
+    }
 
     // binned linear marks (scan_binned.cuh), for tables larger than L2
     bool use_bins = false;
@@ -584,17 +638,21 @@ struct Engine {
         cub_call([&](void* t, size_t& b) {
             return cub::DeviceSelect::Flagged(t, b, d_hosts, isnew.p, newhosts.p, ctr.p + 7, static_cast<int>(n), st);
         });
-        const uint32_t nn = read_ctr(7);
+        append_new(newhosts.p, read_ctr(7));
+    }
+
+    // Append `nn` hosts already known to be new (distinct, in order).
+    void append_new(const uint32_t* d_new, uint32_t nn) {
         if (!nn) return;
         csip.ensure_keep(ncsip + nn, ncsip, st);
-        CK(cudaMemcpyAsync(csip.p + ncsip, newhosts.p, nn * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(csip.p + ncsip, d_new, nn * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
         // keep the sorted view of the list current: sort the newcomers, merge
         if (sorted_ret_valid && nsorted_ret == ncsip) {
             newsorted.ensure(nn);
             sorted_tmp.ensure(ncsip + nn);
             sorted_ret.ensure_keep(ncsip + nn, ncsip, st);
             cub_call([&](void* t, size_t& b) {
-                return cub::DeviceRadixSort::SortKeys(t, b, newhosts.p, newsorted.p, static_cast<int>(nn), 0, 32, st);
+                return cub::DeviceRadixSort::SortKeys(t, b, d_new, newsorted.p, static_cast<int>(nn), 0, 32, st);
             });
             k_merge_sorted<<<blocks((ncsip + nn + 7) / 8), 256, 0, st>>>(sorted_ret.p, static_cast<uint32_t>(ncsip),
                                                                        newsorted.p, nn, sorted_tmp.p);
@@ -608,7 +666,7 @@ struct Engine {
         if (2 * ncsip > cset_cap) {
             rebuild_cset(ncsip);
         } else {
-            k_cset_insert<<<blocks(nn), 256, 0, st>>>(newhosts.p, nn, cset.p, cset_cap - 1);
+            k_cset_insert<<<blocks(nn), 256, 0, st>>>(d_new, nn, cset.p, cset_cap - 1);
             check_launch();
             launched();
         }
@@ -831,42 +889,31 @@ struct Engine {
     void split_now(cudaStream_t s) {
         if (!pending_entries) return;
         const uint32_t R = bcfg.nregions;
-        if (split_in_flight) CK(cudaEventSynchronize(ev_split_done));  // pin_bc / tile_prefix reuse
-        split_in_flight = false;
-        CK(cudaMemcpyAsync(pin_bc.p, bin_count.p, R * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        // per-region entry counts (clamped: overflow was applied directly) and tile prefix
-        uint32_t* n_r = pin_bc.p + R + 1;
-        uint32_t* prefix = pin_bc.p;  // reuse: prefix[0..R]
-        std::vector<uint32_t> cnt(pin_bc.p, pin_bc.p + R);
-        uint32_t run = 0;
-        for (uint32_t r = 0; r < R; ++r) {
-            prefix[r] = run;
-            n_r[r] = std::min(cnt[r], bcfg.cap);
-            run += (n_r[r] + kSplitTile - 1) / kSplitTile;
-        }
-        prefix[R] = run;
+        // the tile table is built on the device (k_split_prefix): no host round trip
         if (s != st) {
             CK(cudaEventRecord(ev_k1_done, st));
             CK(cudaStreamWaitEvent(s, ev_k1_done, 0));
         }
-        CK(cudaMemcpyAsync(tile_prefix.p, pin_bc.p, (2 * R + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        if (run) {
-            const cudaEvent_t t0 = timer_start(s);
-            with_w([&](auto w) {
-                using W = decltype(w);
-                // an early split leaves room for the ordering phase's kernels
-                static const uint32_t waves = [] { const char* v = std::getenv("SRLA_SPLIT_WAVES"); return v ? static_cast<uint32_t>(std::atoi(v)) : 2u; }();
-                k_split<W><<<std::min<uint32_t>(run, sms * (s == st ? 8u : waves)), kSplitThreads, split_smem, s>>>(
-                    bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg, ecfg(),
-                    static_cast<W*>(d_lin));
-            });
-            check_launch();
-            launched();
-            timer_stop(t0, kTimeSplit, s);
-            timing.split_kernel_launches += 1;
-            timing.split_entries += pending_entries;
-        }
+        if (split_in_flight) CK(cudaStreamWaitEvent(s, ev_split_done, 0));  // tile_prefix reuse
+        split_in_flight = false;
+        k_split_prefix<<<1, 1024, 0, s>>>(bin_count.p, R, bcfg.cap, tile_prefix.p);
+        check_launch();
+        launched();
+        const cudaEvent_t t0 = timer_start(s);
+        with_w([&](auto w) {
+            using W = decltype(w);
+            // an early split leaves room for the ordering phase's kernels
+            static const uint32_t waves = [] { const char* v = std::getenv("SRLA_SPLIT_WAVES"); return v ? static_cast<uint32_t>(std::atoi(v)) : 2u; }();
+            const uint64_t max_tiles = pending_entries / kSplitTile + R;
+            k_split<W><<<static_cast<uint32_t>(std::min<uint64_t>(max_tiles, sms * (s == st ? 8u : waves))), kSplitThreads, split_smem, s>>>(
+                bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg, ecfg(),
+                static_cast<W*>(d_lin));
+        });
+        check_launch();
+        launched();
+        timer_stop(t0, kTimeSplit, s);
+        timing.split_kernel_launches += 1;
+        timing.split_entries += pending_entries;
         CK(cudaMemsetAsync(bin_count.p, 0, R * sizeof(uint32_t), s));
         if (s != st) {
             CK(cudaEventRecord(ev_split_done, s));
@@ -1031,89 +1078,10 @@ struct Engine {
         return true;
     }
 
-    template <typename W, int MAXR>
-    void scan_chunk_t(const uint32_t* d_recs, uint32_t n, bool overlap) {
-        W* lin = static_cast<W*>(d_lin);
-        W* rough = static_cast<W*>(d_rough);
-        const int vec = (reinterpret_cast<uintptr_t>(d_recs) & 15) == 0;
-        if (!ev_cap) {
-            ev_cap = static_cast<uint32_t>(std::min<uint64_t>(kChunk, (uint64_t(kChunk) >> tau) + (uint64_t(kChunk) >> (tau + 3)) + 65536));
-            ev.ensure(3ull * ev_cap);
-            // the ordering scratch is bounded by the sampled events of a chunk:
-            // size it once instead of creeping up (each regrowth is a cudaFree,
-            // a device-wide synchronisation)
-            const size_t m = std::min<size_t>(ev_cap, size_t(1) << 21);
-            xkeys.ensure(m); xsorted.ensure(m); hp.ensure(m); hps.ensure(m); fmask.ensure(m);
-            cnt.ensure(m); off.ensure(m); hosts.ensure(m); status.ensure(m); definite.ensure(m);
-            fl_und.ensure(m); fl_ins.ensure(m); flagged.ensure(m); pushed.ensure(m); newhosts.ensure(m);
-            isnew.ensure(m);
-            const size_t t = m * std::min<uint32_t>(cfg.rows, 8);
-            tkey.ensure(t); skey.ensure(t); tval.ensure(t); sval.ensure(t); towner.ensure(t); posof.ensure(t);
-        }
-        uint32_t n_ev = 0;
-        bool k1_done = false;
-        if (overlap) {
-            if (use_bins && MAXR <= kBinRows && bins_alt.p) k1_done = scan_k1_overlapped<W>(d_recs, n, vec, n_ev);
-            else join_eos();
-        }
-        join_maint_lin();  // K1 may stamp the linear table directly (bin overflow)
-        join_split();      // the region bins must have been split and zeroed
-        while (!k1_done) {
-            CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
-            if (use_bins) {
-                const uint64_t add = uint64_t(n) * cfg.rows;
-                if ((pending_entries + add) / bcfg.nregions * 13 / 10 + 8192 > bcfg.cap) flush_linear();
-            }
-            CK(cudaEventRecord(t_scan0, st));
-            if (use_bins && MAXR <= kBinRows) {
-                const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
-                if (cfg.rows == 4)
-                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
-                else
-                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
-            } else {
-                k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
-            }
-            check_launch();
-            launched();
-            CK(cudaEventRecord(t_scan1, st));
-            n_ev = read_ctr(0);
-            if (use_bins) pending_entries += uint64_t(n) * cfg.rows;
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, t_scan0, t_scan1));
-            timing.scan_kernel_ms += ms;
-            timing.scan_kernel_launches += 1;
-            timing.scan_kernel_records += n;
-            if (n_ev <= ev_cap) break;
-            // capacity overflow: marks and stamps are idempotent, rerun with room
-            ev_cap = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(n_ev) * 5 / 4 + 4096, 0xFFFFFFF0ull));
-            ev.ensure(3ull * ev_cap);
-        }
-        stats.sampled_events += n_ev;
-        // split the region bins now, concurrent with the ordering phase below
-        if (use_bins && early_split && !overlap_on) split_now(ssplit);
-        trace("scan: K1");
-        if (!n_ev) return;
-        const auto w_order = std::chrono::steady_clock::now();
-        struct OrderTimer {
-            srla_timing& t;
-            std::chrono::steady_clock::time_point t0;
-            ~OrderTimer() { t.order_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
-        } order_timer{timing, w_order};
-
-        join_maint();  // rough aging, indicators and the candidate hash of the last slide
-        xkeys.ensure(n_ev);
-        k_cross<W, MAXR><<<blocks(n_ev), 256, 0, st>>>(ev.p, ev_cap, n_ev, dc, rough, d_stamp, xkeys.p, ctr.p + 1);
-        check_launch();
-        launched();
-        k_commit<W, MAXR><<<blocks(n_ev), 256, 0, st>>>(ev.p, ev_cap, n_ev, dc, rough, d_stamp);
-        check_launch();
-        launched();
-        const uint32_t X = read_ctr(1);
-        trace("scan: K2+K5");
-        stats.crossings += X;
-        if (!X) return;
-
+    // The sorted, ordered resolution from the chunk's X crossing keys
+    // (xkeys): K3 first crossings, K4 indicator resolution, sink pushes,
+    // candidate append (kernels.cuh).
+    void order_tail(uint32_t X) {
         // K3: first crossing per host, then order hosts by P
         xsorted.ensure(X);
         cub_call([&](void* t, size_t& b) {
@@ -1212,6 +1180,223 @@ struct Engine {
         trace("scan: append");
     }
 
+    // A few records: the reference's scan_ip_pair loop on one device thread
+    // (k_scan_serial), one launch and one synchronisation per call.
+    template <typename W, int MAXR>
+    void scan_chunk_serial(const uint32_t* d_recs, uint32_t n) {
+        join_maint();
+        join_split();
+        setup_order(std::max<uint32_t>(n, 1024));
+        CK(cudaMemsetAsync(octr.p, 0, kOcCount * sizeof(uint32_t), st));
+        k_scan_serial<W, MAXR><<<1, 32, 0, st>>>(d_recs, n, dc, static_cast<W*>(d_lin), nib ? 1 : 0, ecfg(),
+                                                 static_cast<W*>(d_rough), d_si, cset.p, cset_cap - 1, pushlist.p,
+                                                 newlist.p, octr.p);
+        check_launch();
+        launched();
+        CK(cudaMemcpyAsync(pin_octr.p, octr.p, kOcCount * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        sync_st();
+        const uint32_t np = pin_octr.p[kOcPushList], nn = pin_octr.p[kOcNew];
+        stats.sampled_events += pin_octr.p[kOcEvents];
+        stats.pushed += np;
+        if (collect_pushed && np) {
+            const size_t at = host_pushed.size();
+            host_pushed.resize(at + np);
+            CK(cudaMemcpy(host_pushed.data() + at, pushlist.p, np * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        }
+        append_new(newlist.p, nn);
+    }
+
+    // One chunk with the ordering phase on device counts (order.cuh): K1, the
+    // early split, K2h/K5, K4h, classify and the ordered compaction of new
+    // candidates all queue back to back; the host synchronises once, reads
+    // the counters and appends. Flagged hosts (rare) fall back to the sorted
+    // resolution (order_tail) from the intact crossing keys and indicators.
+    template <typename W, int MAXR>
+    void scan_chunk_fast(const uint32_t* d_recs, uint32_t n) {
+        W* lin = static_cast<W*>(d_lin);
+        W* rough = static_cast<W*>(d_rough);
+        const int vec = (reinterpret_cast<uintptr_t>(d_recs) & 15) == 0;
+        if (!ev_cap) {
+            ev_cap = static_cast<uint32_t>(std::min<uint64_t>(kChunk, (uint64_t(kChunk) >> tau) + (uint64_t(kChunk) >> (tau + 3)) + 65536));
+            ev.ensure(3ull * ev_cap);
+        }
+        join_maint_lin();  // K1 may stamp the linear table directly (bin overflow)
+        join_split();      // the region bins must have been split and zeroed
+        uint32_t* pc = nullptr;
+        while (true) {
+            setup_order(ev_cap);
+            CK(cudaMemsetAsync(octr.p, 0, kOcCount * sizeof(uint32_t), st));
+            if (use_bins) {
+                const uint64_t add = uint64_t(n) * cfg.rows;
+                if ((pending_entries + add) / bcfg.nregions * 13 / 10 + 8192 > bcfg.cap) flush_linear();
+            }
+            CK(cudaEventRecord(t_scan0, st));
+            uint32_t* evc = octr.p + kOcEvents;
+            if (use_bins && MAXR <= kBinRows) {
+                const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
+                if (cfg.rows == 4)
+                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
+                else
+                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
+            } else {
+                k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, evc, vec);
+            }
+            check_launch();
+            launched();
+            CK(cudaEventRecord(t_scan1, st));
+            if (use_bins) pending_entries += uint64_t(n) * cfg.rows;
+            timing.scan_kernel_launches += 1;
+            timing.scan_kernel_records += n;
+            // split the region bins now, concurrent with the ordering phase below
+            if (use_bins && early_split && !overlap_on) split_now(ssplit);
+            const auto w_order = std::chrono::steady_clock::now();
+            join_maint();  // rough aging, indicators and the candidate hash of the last slide
+            const OrderBufs ob = order_bufs(collect_pushed);
+            const uint32_t g = blocks(ev_cap, 256, 4);
+            k_cross_ht<W, MAXR><<<g, 256, 0, st>>>(ev.p, ev_cap, dc, rough, d_stamp, xkeys.p, ob);
+            k_commit_dev<W, MAXR><<<g, 256, 0, st>>>(ev.p, ev_cap, dc, rough, d_stamp, ob);
+            k_si_open<<<g, 256, 0, st>>>(dc, d_si, ob);
+            k_order_classify<<<g, 256, 0, st>>>(dc, cset.p, cset_cap - 1, ob);
+            check_launch();
+            launched(4);
+            emit_bitmap(bm_new.p, n, d_recs, newlist.p, kOcNew);
+            if (collect_pushed) emit_bitmap(bm_push.p, n, d_recs, pushlist.p, kOcPushList);
+            CK(cudaMemcpyAsync(pin_octr.p, octr.p, kOcCount * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            sync_st();  // the chunk's one host synchronisation
+            pc = pin_octr.p;
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, t_scan0, t_scan1));
+            timing.scan_kernel_ms += ms;
+            timing.order_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w_order).count();
+            if (pc[kOcEvents] <= ev_cap) break;
+            // event overflow: the ordering kernels did nothing; marks and rough
+            // stamps are idempotent, so K1 reruns with room
+            ev_cap = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(pc[kOcEvents]) * 5 / 4 + 4096, 0xFFFFFFF0ull));
+            ev.ensure(3ull * ev_cap);
+        }
+        const uint32_t n_ev = pc[kOcEvents], X = pc[kOcCross], Hn = pc[kOcHosts], nf = pc[kOcFlagged];
+        const uint32_t np = pc[kOcPushed], nn = pc[kOcNew], Tn = pc[kOcTuples];
+        stats.sampled_events += n_ev;
+        stats.crossings += X;
+        const OrderBufs ob = order_bufs(false);
+        if (nf) {  // ordered resolution needed: the sorted path from the crossing keys
+            const auto w = std::chrono::steady_clock::now();
+            CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
+            order_tail(X);
+            timing.order_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w).count();
+        } else {
+            stats.first_crossings += Hn;
+            stats.pushed += np;
+            if (Hn) {
+                k_order_si_set<<<blocks(Hn), 256, 0, st>>>(dc, d_si, ob, Hn);
+                check_launch();
+                launched();
+            }
+            if (collect_pushed && pc[kOcPushList]) {
+                const uint32_t m = pc[kOcPushList];
+                const size_t at = host_pushed.size();
+                host_pushed.resize(at + m);
+                pin_hosts.ensure(m);
+                CK(cudaMemcpyAsync(pin_hosts.p, pushlist.p, m * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                std::memcpy(host_pushed.data() + at, pin_hosts.p, m * sizeof(uint32_t));
+            }
+            append_new(newlist.p, nn);
+        }
+        if (Hn || Tn) {
+            k_order_clear<<<blocks(std::max(Hn, Tn)), 256, 0, st>>>(ob, Hn, Tn);
+            check_launch();
+            launched();
+        }
+        trace("scan: fast order");
+    }
+
+    template <typename W, int MAXR>
+    void scan_chunk_t(const uint32_t* d_recs, uint32_t n, bool overlap) {
+        W* lin = static_cast<W*>(d_lin);
+        W* rough = static_cast<W*>(d_rough);
+        const int vec = (reinterpret_cast<uintptr_t>(d_recs) & 15) == 0;
+        if (!ev_cap) {
+            ev_cap = static_cast<uint32_t>(std::min<uint64_t>(kChunk, (uint64_t(kChunk) >> tau) + (uint64_t(kChunk) >> (tau + 3)) + 65536));
+            ev.ensure(3ull * ev_cap);
+            // the ordering scratch is bounded by the sampled events of a chunk:
+            // size it once instead of creeping up (each regrowth is a cudaFree,
+            // a device-wide synchronisation)
+            const size_t m = std::min<size_t>(ev_cap, size_t(1) << 21);
+            xkeys.ensure(m); xsorted.ensure(m); hp.ensure(m); hps.ensure(m); fmask.ensure(m);
+            cnt.ensure(m); off.ensure(m); hosts.ensure(m); status.ensure(m); definite.ensure(m);
+            fl_und.ensure(m); fl_ins.ensure(m); flagged.ensure(m); pushed.ensure(m); newhosts.ensure(m);
+            isnew.ensure(m);
+            const size_t t = m * std::min<uint32_t>(cfg.rows, 8);
+            tkey.ensure(t); skey.ensure(t); tval.ensure(t); sval.ensure(t); towner.ensure(t); posof.ensure(t);
+        }
+        uint32_t n_ev = 0;
+        bool k1_done = false;
+        if (overlap) {
+            if (use_bins && MAXR <= kBinRows && bins_alt.p) k1_done = scan_k1_overlapped<W>(d_recs, n, vec, n_ev);
+            else join_eos();
+        }
+        join_maint_lin();  // K1 may stamp the linear table directly (bin overflow)
+        join_split();      // the region bins must have been split and zeroed
+        while (!k1_done) {
+            CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
+            if (use_bins) {
+                const uint64_t add = uint64_t(n) * cfg.rows;
+                if ((pending_entries + add) / bcfg.nregions * 13 / 10 + 8192 > bcfg.cap) flush_linear();
+            }
+            CK(cudaEventRecord(t_scan0, st));
+            if (use_bins && MAXR <= kBinRows) {
+                const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
+                if (cfg.rows == 4)
+                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                else
+                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+            } else {
+                k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+            }
+            check_launch();
+            launched();
+            CK(cudaEventRecord(t_scan1, st));
+            n_ev = read_ctr(0);
+            if (use_bins) pending_entries += uint64_t(n) * cfg.rows;
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, t_scan0, t_scan1));
+            timing.scan_kernel_ms += ms;
+            timing.scan_kernel_launches += 1;
+            timing.scan_kernel_records += n;
+            if (n_ev <= ev_cap) break;
+            // capacity overflow: marks and stamps are idempotent, rerun with room
+            ev_cap = static_cast<uint32_t>(std::min<uint64_t>(uint64_t(n_ev) * 5 / 4 + 4096, 0xFFFFFFF0ull));
+            ev.ensure(3ull * ev_cap);
+        }
+        stats.sampled_events += n_ev;
+        // split the region bins now, concurrent with the ordering phase below
+        if (use_bins && early_split && !overlap_on) split_now(ssplit);
+        trace("scan: K1");
+        if (!n_ev) return;
+        const auto w_order = std::chrono::steady_clock::now();
+        struct OrderTimer {
+            srla_timing& t;
+            std::chrono::steady_clock::time_point t0;
+            ~OrderTimer() { t.order_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+        } order_timer{timing, w_order};
+
+        join_maint();  // rough aging, indicators and the candidate hash of the last slide
+        xkeys.ensure(n_ev);
+        k_cross<W, MAXR><<<blocks(n_ev), 256, 0, st>>>(ev.p, ev_cap, n_ev, dc, rough, d_stamp, xkeys.p, ctr.p + 1);
+        check_launch();
+        launched();
+        k_commit<W, MAXR><<<blocks(n_ev), 256, 0, st>>>(ev.p, ev_cap, n_ev, dc, rough, d_stamp);
+        check_launch();
+        launched();
+        const uint32_t X = read_ctr(1);
+        trace("scan: K2+K5");
+        stats.crossings += X;
+        if (!X) return;
+
+        order_tail(X);
+    }
+
     void scan_chunk(const uint32_t* d_recs, uint32_t n, bool overlap = false) {
         if (!n) {
             if (overlap) join_eos();
@@ -1222,8 +1407,18 @@ struct Engine {
         stats.packets += n;
         with_w([&](auto w) {
             using W = decltype(w);
-            if (cfg.rows <= 4) scan_chunk_t<W, 4>(d_recs, n, overlap);
-            else scan_chunk_t<W, 64>(d_recs, n, overlap);
+            static const uint32_t serial_max = [] { const char* v = std::getenv("SRLA_SERIAL_MAX"); return v ? static_cast<uint32_t>(std::atoi(v)) : 64u; }();
+            if (n <= serial_max && !overlap && cfg.rows <= 8) {
+                if (cfg.rows <= 4) scan_chunk_serial<W, 4>(d_recs, n);
+                else scan_chunk_serial<W, 8>(d_recs, n);
+            } else if (fast_order && !overlap && cfg.rows <= 8) {
+                if (cfg.rows <= 4) scan_chunk_fast<W, 4>(d_recs, n);
+                else scan_chunk_fast<W, 8>(d_recs, n);
+            } else if (cfg.rows <= 4) {
+                scan_chunk_t<W, 4>(d_recs, n, overlap);
+            } else {
+                scan_chunk_t<W, 64>(d_recs, n, overlap);
+            }
         });
     }
 
@@ -1943,31 +2138,55 @@ struct Engine {
     // writes and reads them). Epoch-stamp and nibble tables convert to and
     // from the reference's layout on the device, chunk by chunk through a
     // staging buffer, so a 16 GiB row moves at copy speed.
-    static constexpr uint64_t kXferChunk = 1ull << 28;  // reference-layout bytes per hop
+    static constexpr uint64_t kXferChunk = 1ull << 26;  // reference-layout bytes per hop
     DevBuf<uint8_t> xfer;
 
     void export_row(uint32_t row, int kind, void* buf, uint64_t bytes) {
-        flush_linear();
-        uint8_t* p = row_ptr(row, kind);
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
-        if (kind == SRLA_LINEAR && (nib || epoch)) {
-            xfer.ensure(std::min(bytes, kXferChunk));
-            uint8_t* b = static_cast<uint8_t*>(buf);
-            for (uint64_t j0 = 0; j0 < bytes; j0 += kXferChunk) {
-                const uint64_t m = std::min(kXferChunk, bytes - j0);  // recorders (= output bytes)
+        export_range(row, kind, 0, buf, bytes);
+    }
+
+    // Reference-layout bytes [off, off + bytes) of a row, chunk by chunk:
+    // converted on the device (nibble / epoch tables) and copied through a
+    // pinned staging buffer unless the caller's buffer is pinned itself.
+    PinBuf<uint8_t> xpin;
+    static bool is_pinned(const void* p) {
+        cudaPointerAttributes a{};
+        const bool pinned = cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        return pinned;
+    }
+    void check_range(uint32_t row, int kind, uint64_t off, uint64_t bytes) {
+        (void)row_ptr(row, kind);  // row / kind checks
+        if (off > row_bytes(kind) || bytes > row_bytes(kind) - off) throw Error(SRLA_E_RANGE, "byte range outside the row");
+        if (kind == SRLA_LINEAR && nib && ((off | bytes) & 1))
+            throw Error(SRLA_E_INVALID, "packed linear rows move in whole bytes pairs: even offset and size");
+    }
+    void export_range(uint32_t row, int kind, uint64_t off, void* buf, uint64_t bytes) {
+        flush_linear();
+        check_range(row, kind, off, bytes);
+        uint8_t* p = row_ptr(row, kind);
+        uint8_t* b = static_cast<uint8_t*>(buf);
+        const bool convert = kind == SRLA_LINEAR && (nib || epoch);
+        const bool direct = is_pinned(buf);
+        if (convert) xfer.ensure(std::min(bytes, kXferChunk));
+        if (!direct) xpin.ensure(std::min(bytes, kXferChunk));
+        for (uint64_t j0 = 0; j0 < bytes; j0 += kXferChunk) {
+            const uint64_t m = std::min(kXferChunk, bytes - j0);  // reference-layout bytes of this hop
+            const uint8_t* src = p + off + j0;
+            if (convert) {
                 if (nib)
-                    k_unpack_nib<<<blocks(m / 2, 256, 16), 256, 0, st>>>(p + j0 / 2, m / 2, xfer.p);
+                    k_unpack_nib<<<blocks(m / 2, 256, 16), 256, 0, st>>>(p + (off + j0) / 2, m / 2, xfer.p);
                 else
-                    k_stamps_to_values<<<blocks(m, 256, 16), 256, 0, st>>>(p + j0, m, cur_epoch, dc.expired, xfer.p);
+                    k_stamps_to_values<<<blocks(m, 256, 16), 256, 0, st>>>(p + off + j0, m, cur_epoch, dc.expired, xfer.p);
                 check_launch();
                 launched();
-                CK(cudaMemcpyAsync(b + j0, xfer.p, m, cudaMemcpyDeviceToHost, st));
-                CK(cudaStreamSynchronize(st));
+                src = xfer.p;
             }
-            return;
+            CK(cudaMemcpyAsync(direct ? b + j0 : xpin.p, src, m, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (!direct) std::memcpy(b + j0, xpin.p, m);
         }
-        CK(cudaMemcpyAsync(buf, p, bytes, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
     }
 
     // Block digests of one row in the reference layout (digest.cuh), on the device.
@@ -1996,42 +2215,60 @@ struct Engine {
     }
 
     void import_row(uint32_t row, int kind, const void* buf, uint64_t bytes) {
-        flush_linear();
-        uint8_t* p = row_ptr(row, kind);
         if (bytes != row_bytes(kind)) throw Error(SRLA_E_INVALID, "buffer size does not match the row");
-        if (kind == SRLA_LINEAR && (nib || epoch)) {
-            const uint8_t* v = static_cast<const uint8_t*>(buf);
+        import_range(row, kind, 0, buf, bytes);
+    }
+
+    void import_range(uint32_t row, int kind, uint64_t off, const void* buf, uint64_t bytes) {
+        flush_linear();
+        check_range(row, kind, off, bytes);
+        uint8_t* p = row_ptr(row, kind);
+        const uint8_t* v = static_cast<const uint8_t*>(buf);
+        const bool convert = kind == SRLA_LINEAR && (nib || epoch);
+        if (convert) {
             uint8_t vmax = 0;  // vectorisable reduction (no early exit)
             for (uint64_t j = 0; j < bytes; ++j) vmax = std::max(vmax, v[j]);
             if (vmax > (nib ? 0xFu : dc.expired)) {  // beyond the packed / stamp model: a byte per value
                 if (nib) leave_nibble();
                 else leave_epoch();
-                import_row(row, kind, buf, bytes);
+                import_range(row, kind, off, buf, bytes);
                 return;
             }
             xfer.ensure(std::min(bytes, kXferChunk));
-            for (uint64_t j0 = 0; j0 < bytes; j0 += kXferChunk) {
-                const uint64_t m = std::min(kXferChunk, bytes - j0);
-                CK(cudaMemcpyAsync(xfer.p, v + j0, m, cudaMemcpyHostToDevice, st));
-                if (nib)
-                    k_pack_nib<<<blocks(m / 2, 256, 16), 256, 0, st>>>(xfer.p, m / 2, p + j0 / 2);
-                else
-                    k_values_to_stamps<<<blocks(m, 256, 16), 256, 0, st>>>(xfer.p, m, cur_epoch, p + j0);
-                check_launch();
-                launched();
-                CK(cudaStreamSynchronize(st));  // the staging buffer is reused
-            }
-            if (epoch) {
-                CK(cudaMemsetAsync(hist.p + uint64_t(row) * 256, 0, 256 * sizeof(unsigned long long), st));
-                k_row_hist<<<blocks(bytes, 256, 4), 256, 0, st>>>(p, bytes, hist.p + uint64_t(row) * 256);
-                check_launch();
-                launched();
-                CK(cudaStreamSynchronize(st));
-            }
-            return;
         }
-        CK(cudaMemcpyAsync(p, buf, bytes, cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));
+        const bool direct = is_pinned(buf);
+        if (!direct) xpin.ensure(std::min(bytes, kXferChunk));
+        unsigned long long* h = epoch && kind == SRLA_LINEAR ? hist.p + uint64_t(row) * 256 : nullptr;
+        for (uint64_t j0 = 0; j0 < bytes; j0 += kXferChunk) {
+            const uint64_t m = std::min(kXferChunk, bytes - j0);
+            const uint8_t* src = v + j0;
+            if (!direct) {
+                std::memcpy(xpin.p, v + j0, m);
+                src = xpin.p;
+            }
+            if (h) {  // the row's stamp histogram loses the overwritten stamps ...
+                k_row_hist<<<blocks(m, 256, 4), 256, 0, st>>>(p + off + j0, m, h, -1);
+                check_launch();
+                launched();
+            }
+            if (convert) {
+                CK(cudaMemcpyAsync(xfer.p, src, m, cudaMemcpyHostToDevice, st));
+                if (nib)
+                    k_pack_nib<<<blocks(m / 2, 256, 16), 256, 0, st>>>(xfer.p, m / 2, p + (off + j0) / 2);
+                else
+                    k_values_to_stamps<<<blocks(m, 256, 16), 256, 0, st>>>(xfer.p, m, cur_epoch, p + off + j0);
+                check_launch();
+                launched();
+            } else {
+                CK(cudaMemcpyAsync(p + off + j0, src, m, cudaMemcpyHostToDevice, st));
+            }
+            if (h) {  // ... and gains the new ones
+                k_row_hist<<<blocks(m, 256, 4), 256, 0, st>>>(p + off + j0, m, h, 1);
+                check_launch();
+                launched();
+            }
+            CK(cudaStreamSynchronize(st));  // the staging buffers are reused
+        }
     }
 };
 
@@ -2331,6 +2568,36 @@ srla_status srla_block_sums(const void* d_buf, uint64_t bytes, uint64_t* out, ui
         CK(cudaMemcpyAsync(out, d, nb * 8, cudaMemcpyDeviceToHost, s));
         CK(cudaFreeAsync(d, s));
         CK(cudaStreamSynchronize(s));
+    });
+}
+
+srla_status srla_export_range(srla_engine* e, uint32_t row, int kind, uint64_t offset, void* buf, uint64_t bytes) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        if (bytes && !buf) throw srla::Error(SRLA_E_INVALID, "null buffer");
+        E(e).export_range(row, kind, offset, buf, bytes);
+    });
+}
+
+srla_status srla_import_range(srla_engine* e, uint32_t row, int kind, uint64_t offset, const void* buf, uint64_t bytes) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(e->mu);
+        if (bytes && !buf) throw srla::Error(SRLA_E_INVALID, "null buffer");
+        E(e).import_range(row, kind, offset, buf, bytes);
+    });
+}
+
+srla_status srla_host_alloc(uint64_t bytes, void** out) {
+    return guard([&] {
+        if (!out) throw srla::Error(SRLA_E_INVALID, "null output");
+        *out = nullptr;
+        CK(cudaMallocHost(out, std::max<uint64_t>(bytes, 1)));
+    });
+}
+
+srla_status srla_host_free(void* p) {
+    return guard([&] {
+        if (p) CK(cudaFreeHost(p));
     });
 }
 

@@ -355,7 +355,8 @@ __global__ void __launch_bounds__(256, 4) k_stamp_cells(uint8_t* __restrict__ li
                 }
             }
             __syncwarp();
-            for (uint32_t q = lane; q < n + 31u; q += 32) {  // warp-uniform trip count (match_any below)
+            for (uint32_t q0 = 0; q0 < n; q0 += 32) {  // warp-uniform trip count (match_any below)
+                const uint32_t q = q0 + lane;
                 uint32_t key = 0xFFFFFFFFu;
                 if (q < n) {
                     const uint32_t off = __ldg(e + q);
@@ -485,9 +486,10 @@ __global__ void __launch_bounds__(256) k_values_to_stamps(const uint8_t* __restr
         s[q] = static_cast<uint8_t>((cur - v[q]) & 0xFFu);
 }
 
-// Histogram of one row's stamps (after an import). grid-stride, 256 bins.
+// Histogram of a range of one row's stamps, added (sign 1) or removed (sign -1)
+// around an import. grid-stride, 256 bins.
 __global__ void __launch_bounds__(256) k_row_hist(const uint8_t* __restrict__ row, uint64_t n,
-                                                  unsigned long long* __restrict__ hist) {
+                                                  unsigned long long* __restrict__ hist, int sign) {
     __shared__ uint32_t s_h[256];
     s_h[threadIdx.x] = 0;
     __syncthreads();
@@ -495,7 +497,8 @@ __global__ void __launch_bounds__(256) k_row_hist(const uint8_t* __restrict__ ro
          q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
         atomicAdd(&s_h[row[q]], 1u);
     __syncthreads();
-    if (s_h[threadIdx.x]) atomicAdd(hist + threadIdx.x, static_cast<unsigned long long>(s_h[threadIdx.x]));
+    const unsigned long long c = s_h[threadIdx.x];  // sign -1: subtract (mod 2^64)
+    if (c) atomicAdd(hist + threadIdx.x, sign < 0 ? 0ull - c : c);
 }
 
 // Union linear weight over epoch stamps: slot j counts iff every row's stamp

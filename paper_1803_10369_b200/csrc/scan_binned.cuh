@@ -530,6 +530,33 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
     }
 }
 
+// k_split's tile table on the device (no host round trip): per region the
+// clamped entry count n_r = min(count, cap) (overflow was marked directly)
+// and the exclusive prefix of its kSplitTile-entry tiles; prefix[R] = total
+// tiles, which k_split reads. Out: prefix[0..R], n_r at prefix + R + 1.
+__global__ void __launch_bounds__(1024) k_split_prefix(const uint32_t* __restrict__ count, uint32_t nregions,
+                                                       uint32_t cap, uint32_t* __restrict__ prefix) {
+    __shared__ uint32_t s_w[32];
+    const uint32_t r = threadIdx.x;  // nregions <= kMaxRegions = 1024
+    const uint32_t n = r < nregions ? min(count[r], cap) : 0u;
+    const uint32_t tiles = (n + kSplitTile - 1) / kSplitTile;
+    uint32_t incl = tiles;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((r & 31) >= static_cast<uint32_t>(o)) incl += t;
+    }
+    if ((r & 31) == 31) s_w[r >> 5] = incl;
+    __syncthreads();
+    uint32_t base = 0;
+    for (uint32_t j = 0; j < (r >> 5); ++j) base += s_w[j];
+    if (r < nregions) {
+        prefix[r] = base + incl - tiles;
+        prefix[nregions + 1 + r] = n;
+    }
+    if (r == nregions - 1) prefix[nregions] = base + incl;
+}
+
 // mode 0: apply marks (slices without marks are skipped); 1: apply + age;
 // 2: apply + count active (counts[row], pre-age) + age.
 template <typename W>

@@ -141,6 +141,8 @@ def load_library(path: str = LIB_PATH):
         "srla_parse_srlt": (i32, [vp, u64, vp, C.POINTER(u64), vp]),
         "srla_orient_records": (i32, [vp, u64, u32, u32, vp, C.POINTER(u64), C.POINTER(COrientStats), vp]),
         "srla_slice_bounds": (i32, [vp, u64, u32, vp, u64, C.POINTER(u64), vp]),
+        "srla_export_range": (i32, [vp, u32, i32, u64, vp, u64]),
+        "srla_import_range": (i32, [vp, u32, i32, u64, vp, u64]),
         "srla_scan_device": (i32, [vp, vp, u64, vp, vp, u64, C.POINTER(u64)]),
         "srla_state_blocks": (i32, [vp, u32, i32, vp, u64, C.POINTER(u64)]),
         "srla_block_sums": (i32, [vp, u64, vp, u64, vp]),
@@ -164,6 +166,7 @@ EXPORTED_SYMBOLS = (
     "srla_copy_to_device", "srla_state_blocks", "srla_block_sums", "srla_scan_device",
     "srla_nccl_unique_id", "srla_transport_nccl", "srla_transport_nccl_destroy", "srla_shard_create",
     "srla_shard_destroy", "srla_shard_engine", "srla_shard_last_report", "srla_shard_process_slice",
+    "srla_export_range", "srla_import_range", "srla_host_alloc", "srla_host_free",
 )
 
 
@@ -420,6 +423,16 @@ class EstimatorArray:
         dt = np.uint16 if kind == INDICATOR else self.wdtype
         d = np.ascontiguousarray(data, dtype=dt)
         _check(_lib.srla_import_row(self._h, row, kind, _ptr(d), d.nbytes))
+
+    def export_range(self, row: int, kind: int, offset: int, nbytes: int) -> np.ndarray:
+        """Reference-layout bytes [offset, offset + nbytes) of a raw row."""
+        out = np.empty(nbytes, np.uint8)
+        _check(_lib.srla_export_range(self._h, row, kind, offset, _ptr(out), nbytes))
+        return out
+
+    def import_range(self, row: int, kind: int, offset: int, data):
+        d = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+        _check(_lib.srla_import_range(self._h, row, kind, offset, _ptr(d), d.nbytes))
 
     def state(self) -> dict:
         return {(k, i): self.export_row(i, k) for i in range(self.cfg.rows)

@@ -334,6 +334,8 @@ static int replay(int argc, char** argv) {
         };
         for (const auto& r : recs) part.push(r, on_slice);
         part.finish(on_slice);
+        // SRLA_TEST_SNAPSHOT=<path>: the state after the last slice as an SSEA file
+        if (const char* snap = std::getenv("SRLA_TEST_SNAPSHOT")) save_snapshot(pipe.sketch(), pipe.candidates(), snap);
         return 0;
     });
 }

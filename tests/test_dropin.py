@@ -143,3 +143,47 @@ def test_dropin_run_device_front_end_matches_oracle(gpu, oracle, dropin_bin, tmp
     k = lines.index(next(l for l in lines if l.startswith("csip ")))
     n = int(lines[k].split()[1])
     assert [int(x) for x in lines[k + 1:k + 1 + n]] == pipe.candidates().tolist()
+
+
+def _sha_file(p):
+    import hashlib
+    h = hashlib.sha256()
+    with open(p, "rb") as f:
+        while True:
+            b = f.read(1 << 24)
+            if not b:
+                return h.hexdigest()
+            h.update(b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["pipeline_small", "wide_w2", "c1_shape", "contended", "c2_v20"])
+def test_dropin_snapshot_bytes_equal_reference(gpu, ref, oracle, dropin_bin, tmp_path, name):
+    """save_snapshot of the drop-in (rows streamed from HBM through pinned
+    pieces) writes the same bytes as the reference's save_snapshot
+    (snapshot.hpp:109-136) after the same slices through DetectPipeline."""
+    from oracle.pyoracle import PlantSpec, SeaConfig
+    if name == "c2_v20":  # C2's sketch (v = 2^20: 4 GiB of linear recorders) on a reduced C2-shape trace
+        from paper_1803_10369_b200 import workloads as WL
+        c = S.Cfg(**WL.sketch_cfg(1 << 20))
+        spec = PlantSpec(**WL.trace_spec(300_000, slices=3))
+        slices = [ref.generate_slice(spec, s) for s in range(3)]
+    else:
+        c, _ = S.SCENARIOS[name]
+        slices = GF.scenario_slices(name, oracle)
+    if c.cols & (c.cols - 1):
+        pytest.skip("DetectPipeline needs a power-of-two column count")
+    trace = tmp_path / "t.bin"
+    _write_srlt(trace, np.concatenate(slices))
+    mine, theirs = tmp_path / "dropin.ssea", tmp_path / "ref.ssea"
+    subprocess.run([dropin_bin, "replay", str(trace), str(tmp_path / "out.txt"), str(c.rows), str(c.cols),
+                    str(c.rough_slots), str(c.linear_slots), str(c.recorder_bits), str(c.window), str(c.theta),
+                    hex(c.seed)], check=True, timeout=900, env={**os.environ, "SRLA_TEST_SNAPSHOT": str(mine)})
+    pipe = ref.pipeline(SeaConfig(**c.as_dict()), workers=1)
+    for s, recs in enumerate(slices):
+        pipe.process_slice(s, recs, True)
+    pipe.save_snapshot(str(theirs))
+    assert os.path.getsize(mine) == os.path.getsize(theirs)
+    assert _sha_file(mine) == _sha_file(theirs)
+    os.remove(mine)
+    os.remove(theirs)

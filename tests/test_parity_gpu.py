@@ -28,8 +28,12 @@ def engine(cfg: S.Cfg):
     return EstimatorArray(SeaConfig(**cfg.as_dict()))
 
 
+@pytest.mark.parametrize("order", ["fast", "legacy"])
 @pytest.mark.parametrize("name", sorted(S.SCENARIOS))
-def test_engine_matches_reference_golden(gpu, oracle, name):
+def test_engine_matches_reference_golden(gpu, oracle, name, order, monkeypatch):
+    """Every golden scenario, with the ordering phase on device counts
+    (order.cuh, the default) and with the sorted host-synchronised path."""
+    monkeypatch.setenv("SRLA_ORDER", order)
     g = json.load(open(os.path.join(GOLD, f"{name}.json")))
     cfg, _ = S.SCENARIOS[name]
     slices = GF.scenario_slices(name, oracle)

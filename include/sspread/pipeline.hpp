@@ -13,6 +13,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstring>
 #include <fstream>
 #include <functional>
 #include <span>
@@ -148,7 +149,7 @@ class DetectPipeline {
         uint64_t n = 0;
         const srla_status ps = srla_parse_srlt(d_bytes.p, nbytes, static_cast<srla_record*>(d_raw.p), &n, nullptr);
         std::string input_error;
-        if (ps == SRLA_E_INPUT) input_error = std::string(srla_last_error()) + " in " + path;
+        if (ps == SRLA_E_INPUT) input_error = reference_input_error(srla_last_error(), path, bytes, n);
         else detail::check(ps, "srla_parse_srlt");
         uint64_t m = 0;
         srla_orient_stats os{};
@@ -174,6 +175,24 @@ class DetectPipeline {
         const auto* d = static_cast<const TraceRecord*>(d_recs.p);
         for (uint64_t sid = 0; sid < done; ++sid) process_slice_device(sid, d + off[sid], off[sid + 1] - off[sid], sink);
         if (!input_error.empty()) throw InputError(input_error);
+    }
+
+    // for_each_record's InputError text (trace.hpp:109-170) for a device
+    // parse failure: the record index comes from the device, the timestamps of
+    // a regression from the file bytes still on the host
+    static std::string reference_input_error(const std::string& msg, const std::string& path,
+                                             const std::vector<char>& bytes, uint64_t bad) {
+        auto ts_at = [&](uint64_t i) {
+            uint32_t v = 0;
+            std::memcpy(&v, bytes.data() + 5 + 12 * i, 4);  // x86: little-endian
+            return v;
+        };
+        if (msg.rfind("timestamp regression", 0) == 0 && bad > 0 && 5 + 12 * (bad + 1) <= bytes.size())
+            return "timestamp regression at record " + std::to_string(bad) + " of " + path + " (" +
+                   std::to_string(ts_at(bad)) + " after " + std::to_string(ts_at(bad - 1)) + ")";
+        if (msg.rfind("not a binary trace", 0) == 0) return "not a binary trace (bad magic): " + path;
+        if (msg.rfind("unsupported trace version", 0) == 0) return "unsupported trace version in " + path;
+        return msg + " in " + path;  // "truncated record N in PATH"
     }
 
     void process(uint64_t slice_id, const TraceRecord* recs, uint64_t n, int on_device, const ReportSink& sink) {

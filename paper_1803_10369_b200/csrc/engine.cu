@@ -219,7 +219,8 @@ struct Engine {
     // ordering phase on device counts (order.cuh); SRLA_ORDER=legacy selects
     // the sorted, host-synchronised path (kernels.cuh K2..K4f) throughout
     bool fast_order = [] { const char* v = std::getenv("SRLA_ORDER"); return !(v && std::string(v) == "legacy"); }();
-    DevBuf<uint32_t> octr, ht_vals, tt_vals, hl, tl, host_a, host_p, bm_new, bm_push, bits_cnt, newlist, pushlist;
+    DevBuf<uint32_t> octr, ht_vals, tt_vals, hl, tl, host_a, host_p, host_cols, flist, bm_new, bm_push, bits_cnt, newlist,
+        pushlist;
     DevBuf<unsigned long long> ht_keys, tt_keys;
     DevBuf<uint64_t> host_f;
     DevBuf<uint8_t> ostatus;
@@ -237,8 +238,17 @@ struct Engine {
         ht_keys.ensure(hs); ht_vals.ensure(hs); tt_keys.ensure(ts); tt_vals.ensure(ts);
         hl.ensure(cap); tl.ensure(uint64_t(cap) * std::min<uint32_t>(cfg.rows, 8));
         host_a.ensure(cap); host_p.ensure(cap); host_f.ensure(cap); ostatus.ensure(cap);
+        host_cols.ensure(uint64_t(cap) * kOrderRows); flist.ensure(cap);
         newlist.ensure(cap); pushlist.ensure(cap);
         xkeys.ensure(cap);
+        // the sorted fallback's scratch (order_tail), sized once: a regrowth is
+        // a cudaFree, a device-wide synchronisation
+        const size_t m = std::min<size_t>(cap, size_t(1) << 21);
+        xsorted.ensure(m); hp.ensure(m); hps.ensure(m); fmask.ensure(m); cnt.ensure(m); off.ensure(m);
+        hosts.ensure(m); status.ensure(m); definite.ensure(m); fl_und.ensure(m); fl_ins.ensure(m);
+        flagged.ensure(m); pushed.ensure(m); newhosts.ensure(m); isnew.ensure(m);
+        const size_t t = m * std::min<uint32_t>(cfg.rows, 8);
+        tkey.ensure(t); skey.ensure(t); tval.ensure(t); sval.ensure(t); towner.ensure(t); posof.ensure(t);
         const uint64_t words = (uint64_t(kChunk) + 31) / 32;
         bm_new.ensure(words); bm_push.ensure(words);
         bits_cnt.ensure((words + kBitsWords - 1) / kBitsWords + 1);
@@ -255,7 +265,8 @@ struct Engine {
 
     OrderBufs order_bufs(bool collect) {
         return OrderBufs{octr.p, ht_keys.p, ht_vals.p, ht_mask, hl.p, tt_keys.p, tt_vals.p, tt_mask, tl.p,
-                         host_a.p, host_p.p, host_f.p, ostatus.p, bm_new.p, collect ? bm_push.p : nullptr, order_cap};
+                         host_a.p, host_p.p, host_f.p, host_cols.p, flist.p, ostatus.p, bm_new.p,
+                         collect ? bm_push.p : nullptr, order_cap};
     }
 
     // ordered compaction of a packet bitmap into `out` (device count -> octr[ctr_idx])
@@ -1257,8 +1268,11 @@ struct Engine {
             k_commit_dev<W, MAXR><<<g, 256, 0, st>>>(ev.p, ev_cap, dc, rough, d_stamp, ob);
             k_si_open<<<g, 256, 0, st>>>(dc, d_si, ob);
             k_order_classify<<<g, 256, 0, st>>>(dc, cset.p, cset_cap - 1, ob);
+            const cudaEvent_t tf = timer_start();
+            k_resolve_flagged<<<1, 1024, 0, st>>>(dc, cset.p, cset_cap - 1, ob);
+            timer_stop(tf, kTimeSerial);
             check_launch();
-            launched(4);
+            launched(5);
             emit_bitmap(bm_new.p, n, d_recs, newlist.p, kOcNew);
             if (collect_pushed) emit_bitmap(bm_push.p, n, d_recs, pushlist.p, kOcPushList);
             CK(cudaMemcpyAsync(pin_octr.p, octr.p, kOcCount * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -1279,13 +1293,16 @@ struct Engine {
         stats.sampled_events += n_ev;
         stats.crossings += X;
         const OrderBufs ob = order_bufs(false);
-        if (nf) {  // ordered resolution needed: the sorted path from the crossing keys
+        if (pc[kOcFallback]) {  // many flagged hosts: the sorted path from the crossing keys
             const auto w = std::chrono::steady_clock::now();
             CK(cudaMemsetAsync(ctr.p, 0, 16 * sizeof(uint32_t), st));
             order_tail(X);
             timing.order_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w).count();
         } else {
             stats.first_crossings += Hn;
+            stats.flagged += nf;
+            timing.serial_kernel_launches += 1;
+            timing.flagged_hosts += nf;
             stats.pushed += np;
             if (Hn) {
                 k_order_si_set<<<blocks(Hn), 256, 0, st>>>(dc, d_si, ob, Hn);
@@ -1411,7 +1428,7 @@ struct Engine {
             if (n <= serial_max && !overlap && cfg.rows <= 8) {
                 if (cfg.rows <= 4) scan_chunk_serial<W, 4>(d_recs, n);
                 else scan_chunk_serial<W, 8>(d_recs, n);
-            } else if (fast_order && !overlap && cfg.rows <= 8) {
+            } else if (fast_order && !overlap && cfg.rows <= kOrderRows) {
                 if (cfg.rows <= 4) scan_chunk_fast<W, 4>(d_recs, n);
                 else scan_chunk_fast<W, 8>(d_recs, n);
             } else if (cfg.rows <= 4) {
@@ -2521,6 +2538,8 @@ srla_status srla_estimate_from(const srla_engine* e, uint32_t weight, double fil
                                int* has_estimate) {
     return guard([&] {
         const auto& x = CE(e);
+        if (fill_product >= 1.0 - 1e-12 && weight > x.cfg.linear_slots)  // linear_estimate (estimators.hpp:142)
+            throw srla::Error(SRLA_E_INVALID, "weight exceeds slot count");
         double v = 0.0;
         const bool h = srla_host::corrected_estimate(x.cfg.linear_slots, weight, fill_product, &v);
         if (estimate) *estimate = h ? v : 0.0;

@@ -41,7 +41,8 @@ enum OrderCtr : uint32_t {
     kOcNew = 5,      // inserted hosts not yet candidates
     kOcPushList = 6, // pushes emitted (collect mode)
     kOcTuples = 7,   // distinct open (row, col, bit) keys
-    kOcCount = 8
+    kOcFallback = 8, // too many flagged hosts for the on-device resolution
+    kOcCount = 12
 };
 
 __device__ __forceinline__ uint64_t ht_hash(uint64_t key) { return avalanche64(key * 0x9E3779B97F4A7C15ull); }
@@ -90,11 +91,16 @@ struct OrderBufs {
     uint32_t* host_a;              // per listed host: aip, P, open rows, status
     uint32_t* host_p;
     uint64_t* host_f;
+    uint32_t* host_cols;           // per listed host: its column in each row (rows <= kOrderRows)
+    uint32_t* flist;               // flagged hosts (indices into the host list)
     uint8_t* status;               // 0 suppressed, 1 inserted, 2 flagged
     uint32_t* bm_new;              // bitmaps over the chunk's packets
     uint32_t* bm_push;             // (nullptr unless pushes are collected)
     uint32_t cap;                  // event capacity (bounds every list)
 };
+
+constexpr uint32_t kOrderRows = 8;       // rows handled by the device-count ordering
+constexpr uint32_t kFlaggedOnDevice = 64; // more flagged hosts than this: sorted fallback
 
 __device__ __forceinline__ bool order_overflow(const OrderBufs& o) { return o.ctr[kOcEvents] > o.cap; }
 
@@ -163,6 +169,7 @@ __global__ void __launch_bounds__(256) k_si_open(DevCfg c, const uint16_t* __res
         uint64_t F = 0;
         for (uint32_t i = 0; i < c.rows; ++i) {
             const uint32_t col = column_of(c, i, a);
+            o.host_cols[static_cast<uint64_t>(h) * kOrderRows + i] = col;
             if (si[static_cast<uint64_t>(i) * c.cols + col] & (1u << b)) continue;
             F |= 1ull << i;
             bool fresh = false;
@@ -174,6 +181,23 @@ __global__ void __launch_bounds__(256) k_si_open(DevCfg c, const uint16_t* __res
         o.host_p[h] = p;
         o.host_f[h] = F;
     }
+}
+
+// an inserted host: a sink push at packet P, and a new candidate unless the
+// list already holds it (CandidateList::insert, sea.hpp:58-62)
+__device__ __forceinline__ void mark_inserted(uint32_t a, uint32_t p, const unsigned long long* __restrict__ cset,
+                                              uint64_t cset_mask, const OrderBufs& o) {
+    atomicAdd(o.ctr + kOcPushed, 1u);
+    if (o.bm_push) atomicOr(o.bm_push + (p >> 5), 1u << (p & 31u));
+    const unsigned long long key = static_cast<unsigned long long>(a) + 1ull;
+    uint64_t s = avalanche64(a) & cset_mask;  // kernels.cuh cset_slot
+    while (true) {
+        const unsigned long long v = cset[s];
+        if (v == 0ull) break;
+        if (v == key) return;
+        s = (s + 1) & cset_mask;
+    }
+    atomicOr(o.bm_new + (p >> 5), 1u << (p & 31u));
 }
 
 // K4c: classify; inserted hosts mark the packet bitmaps
@@ -199,24 +223,64 @@ __global__ void __launch_bounds__(256) k_order_classify(DevCfg c, const unsigned
             }
         }
         o.status[h] = st;
-        if (st == 2) atomicAdd(o.ctr + kOcFlagged, 1u);
+        if (st == 2) o.flist[atomicAdd(o.ctr + kOcFlagged, 1u)] = h;
         if (st != 1) continue;
-        atomicAdd(o.ctr + kOcPushed, 1u);
-        if (o.bm_push) atomicOr(o.bm_push + (p >> 5), 1u << (p & 31u));
-        // CandidateList::insert (sea.hpp:58-62): only hosts not yet listed are appended
-        const unsigned long long key = static_cast<unsigned long long>(a) + 1ull;
-        uint64_t s = avalanche64(a) & cset_mask;  // kernels.cuh cset_slot
-        bool present = false;
-        while (true) {
-            const unsigned long long v = cset[s];
-            if (v == 0ull) break;
-            if (v == key) {
-                present = true;
-                break;
+        mark_inserted(a, p, cset, cset_mask, o);
+    }
+}
+
+// On-device ordered resolution of the (few) flagged hosts, ascending P: a
+// flagged host is inserted iff in some open row no host inserted before it
+// (smaller P) shares its (row, col, bit) — the reference's "bit not in the
+// row's indicator" test at P (sea.hpp:185-190), as kernels.cuh k_serial
+// decides it. Hosts sharing a key share the row's open state, so the test
+// needs only the hosts' columns, bits and statuses. One block; hosts already
+// decided are final, earlier flagged hosts are resolved first.
+__global__ void __launch_bounds__(1024) k_resolve_flagged(DevCfg c, const unsigned long long* __restrict__ cset,
+                                                          uint64_t cset_mask, OrderBufs o) {
+    if (order_overflow(o)) return;
+    const uint32_t nf = o.ctr[kOcFlagged];
+    if (nf == 0) return;
+    if (nf > kFlaggedOnDevice) {
+        if (threadIdx.x == 0) o.ctr[kOcFallback] = 1;
+        return;
+    }
+    __shared__ uint32_t s_f[kFlaggedOnDevice];
+    if (threadIdx.x == 0) {  // ascending P (insertion sort of <= 64 entries)
+        for (uint32_t i = 0; i < nf; ++i) {
+            const uint32_t h = o.flist[i];
+            uint32_t j = i;
+            while (j > 0 && o.host_p[s_f[j - 1]] > o.host_p[h]) {
+                s_f[j] = s_f[j - 1];
+                --j;
             }
-            s = (s + 1) & cset_mask;
+            s_f[j] = h;
         }
-        if (!present) atomicOr(o.bm_new + (p >> 5), 1u << (p & 31u));
+    }
+    __syncthreads();
+    const uint32_t hn = o.ctr[kOcHosts];
+    for (uint32_t f = 0; f < nf; ++f) {
+        const uint32_t h = s_f[f];
+        const uint32_t a = o.host_a[h], p = o.host_p[h];
+        const uint32_t b = indicator_bit_index(c, a);
+        uint64_t F = o.host_f[h];
+        bool inserted = false;
+        while (F && !inserted) {
+            const uint32_t i = __ffsll(F) - 1;
+            F &= F - 1;
+            const uint32_t col = o.host_cols[static_cast<uint64_t>(h) * kOrderRows + i];
+            bool blocked = false;
+            for (uint32_t q = threadIdx.x; q < hn && !blocked; q += blockDim.x)
+                blocked = o.status[q] == 1 && o.host_p[q] < p && ((o.host_f[q] >> i) & 1ull) &&
+                          o.host_cols[static_cast<uint64_t>(q) * kOrderRows + i] == col &&
+                          indicator_bit_index(c, o.host_a[q]) == b;
+            inserted = !__syncthreads_or(blocked);
+        }
+        if (threadIdx.x == 0) {
+            o.status[h] = inserted ? 1 : 0;
+            if (inserted) mark_inserted(a, p, cset, cset_mask, o);
+        }
+        __syncthreads();
     }
 }
 

@@ -143,6 +143,38 @@ static void test_corrected_estimate() {
     const double up = 0.25 * 0.25 * 0.25 * 0.25;
     CHECK(std::abs(sea.corrected_estimate_from(300, up).value() - 350.99291022602281) < 350.99291022602281 * 1e-12);
     CHECK(sea.corrected_estimate_from(100, 1.0 - 1e-13) == linear_estimate(100, 1024));
+    // linear_estimate rejects a weight above the slot count (estimators.hpp:142)
+    CHECK_THROWS_AS(sea.corrected_estimate_from(1025, 1.0), std::invalid_argument);
+    WindowConfig wc;  // trace.hpp:78-87
+    wc.window = 300;
+    wc.recorder_bits = 8;
+    CHECK_THROWS_AS(wc.validate(), std::invalid_argument);
+    wc.recorder_bits = 16;
+    wc.validate();
+}
+
+// DetectPipeline::run on a binary trace: the device front end reports a
+// timestamp regression with for_each_record's text (trace.hpp:116-118).
+static void test_run_regression_message() {
+    const std::string path = (std::filesystem::temp_directory_path() / "srla_regress.bin").string();
+    {
+        std::ofstream f(path, std::ios::binary);
+        f.write("SRLT\x01", 5);
+        const uint32_t recs[3][3] = {{100, 0x0A000001, 0x64000001}, {105, 0x0A000002, 0x64000002}, {103, 0x0A000003, 0x64000003}};
+        f.write(reinterpret_cast<const char*>(recs), sizeof recs);
+    }
+    RunConfig rc;
+    rc.sea = small_config();
+    rc.slice_seconds = 1;
+    DetectPipeline<uint8_t> pipe(rc);
+    std::string msg;
+    try {
+        pipe.run(path, {});
+    } catch (const InputError& e) {
+        msg = e.what();
+    }
+    CHECK(msg == "timestamp regression at record 2 of " + path + " (103 after 105)");
+    std::filesystem::remove(path);
 }
 
 static void test_slide() {
@@ -392,6 +424,7 @@ int main(int argc, char** argv) {
     test_order_independence();
     test_snapshot_round_trip();
     test_pipeline_validation();
+    test_run_regression_message();
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }

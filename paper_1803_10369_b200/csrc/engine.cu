@@ -956,7 +956,7 @@ struct Engine {
                 const uint32_t sparse_max = stamp_sparse_max;
                 const uint32_t sp = cfg.rows <= kStampWarpRows && lin_words % 4 == 0 ? sparse_max : 0u;
                 if (sp && stamp_cells && fcfg.shift >= 9 && fcfg.shift <= 16) {
-                    k_stamp_cells<<<sms * 4, 256, stamp_cells_smem(fcfg.shift), st>>>(
+                    k_stamp_cells<<<sms * 3, 256, stamp_cells_smem(fcfg.shift), st>>>(
                         static_cast<uint8_t*>(d_lin), lin_words, fcfg, sp, cur_epoch, cfg.window, cfg.rows, hist.p);
                     check_launch();
                     launched();

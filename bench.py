@@ -478,6 +478,19 @@ def run_engine(args):
                "srla_scan_batch(host, pinned) + srla_end_slice_async/wait"}
         del host
 
+    # the reference's own entry point through the drop-in headers (C++):
+    # DetectPipeline<uint8_t>::process_slice with host records, in its own process
+    e2e_dropin = None
+    dropin = os.path.join(ROOT, "paper_1803_10369_b200", "lib", "bench_dropin")
+    if rank == 0 and world == 1 and not args.no_e2e and args.workload == "c2" and os.path.exists(dropin):
+        try:
+            r = subprocess.run([dropin, str(args.steps), str(args.warmup), str(args.packets)], capture_output=True,
+                               text=True, timeout=900)
+            e2e_dropin = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else \
+                {"error": (r.stderr or r.stdout)[-300:]}
+        except Exception as ex:  # noqa: BLE001 (reported, not fatal)
+            e2e_dropin = {"error": str(ex)[:300]}
+
     # the reference on this box's host cores, steady state on the same slices
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
@@ -531,6 +544,7 @@ def run_engine(args):
             "flagged_hosts_per_step": tm["flagged_hosts"] / args.steps,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_dropin": e2e_dropin,
             "c3": c3,
             "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
             "library_launches": int(st1["library_launches"] - st0["library_launches"]),

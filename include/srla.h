@@ -372,6 +372,7 @@ srla_status srla_shard_last_report(srla_shard* s, srla_entry* out, uint64_t cap,
 srla_status srla_device_alloc(int device, uint64_t bytes, void** out);
 srla_status srla_device_free(int device, void* p);
 srla_status srla_copy_to_device(int device, void* dst, const void* src, uint64_t bytes);
+srla_status srla_copy_to_host(int device, void* dst, const void* src, uint64_t bytes);
 
 /* ---- ingest front end on the device (trace.hpp) ----
  * All buffers are device memory; `stream` is a cudaStream_t (NULL: default). */

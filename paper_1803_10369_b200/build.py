@@ -10,6 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsrla_b200.so")
+DROPIN_BENCH = os.path.join(LIBDIR, "bench_dropin")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["engine.cu", "generator.cu", "shard.cu", "ingest.cu"]
@@ -22,6 +23,11 @@ def _sources():
     ] + [os.path.join(ROOT, "include", "srla.h")]
 
 
+def _dropin_sources():
+    inc = os.path.join(ROOT, "include", "sspread")
+    return [LIB, os.path.join(ROOT, "tools", "bench_dropin.cpp")] + [os.path.join(inc, f) for f in os.listdir(inc)]
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
@@ -31,6 +37,9 @@ def up_to_date() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
+        if not os.path.exists(DROPIN_BENCH) or any(os.path.getmtime(f) > os.path.getmtime(DROPIN_BENCH)
+                                                   for f in _dropin_sources()):
+            build_dropin_bench()
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     objs, jobs = [], []
@@ -57,7 +66,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], check=True)
     for o in objs:
         os.remove(o)
+    build_dropin_bench()
     return LIB
+
+
+def build_dropin_bench() -> str:
+    """tools/bench_dropin.cpp: DetectPipeline::process_slice through the drop-in
+    headers, linked against the library (bench.py's e2e_dropin)."""
+    src = os.path.join(ROOT, "tools", "bench_dropin.cpp")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-L", LIBDIR,
+                    "-lsrla_b200", "-Wl,-rpath,$ORIGIN", "-o", DROPIN_BENCH], check=True)
+    return DROPIN_BENCH
 
 
 if __name__ == "__main__":

@@ -294,8 +294,6 @@ struct Engine {
     // epoch-stamp linear table (epoch.cuh): u8 stamps, O(1) slide
     bool epoch = false;
     uint32_t stamp_sparse_max = 1024;  // SRLA_STAMP_SPARSE, read per engine at setup
-    // sparse slices: piece-staged stamps (k_stamp_cells) or in-place byte stamps (k_stamp_warp, SRLA_STAMP_CELLS=0)
-    bool stamp_cells = [] { const char* v = std::getenv("SRLA_STAMP_CELLS"); return !(v && v[0] == '0'); }();
     uint32_t cur_epoch = 0;
     DevBuf<unsigned long long> hist;  // rows x 256
     PinBuf<unsigned long long> pin_hist;
@@ -789,7 +787,6 @@ struct Engine {
         });
         if (const char* v = std::getenv("SRLA_STAMP_SPARSE")) stamp_sparse_max = static_cast<uint32_t>(std::atoi(v));
         raise_smem_cap(k_stamp_warp, static_cast<int>(stamp_claim_bytes(fs)));
-        if (fs >= 9 && fs <= 16) raise_smem_cap(k_stamp_cells, static_cast<int>(stamp_cells_smem(fs)));
         if (nib) {
             if (nib_apply_smem() > 200 * 1024) return false;  // two stages must fit in shared memory
             raise_smem_cap(k_slice_apply_nib, static_cast<int>(nib_apply_smem()));
@@ -955,12 +952,7 @@ struct Engine {
                 // sparse slices warp by warp in place, dense ones through shared memory
                 const uint32_t sparse_max = stamp_sparse_max;
                 const uint32_t sp = cfg.rows <= kStampWarpRows && lin_words % 4 == 0 ? sparse_max : 0u;
-                if (sp && stamp_cells && fcfg.shift >= 9 && fcfg.shift <= 16) {
-                    k_stamp_cells<<<sms * 3, 256, stamp_cells_smem(fcfg.shift), st>>>(
-                        static_cast<uint8_t*>(d_lin), lin_words, fcfg, sp, cur_epoch, cfg.window, cfg.rows, hist.p);
-                    check_launch();
-                    launched();
-                } else if (sp) {
+                if (sp) {
                     k_stamp_warp<<<sms * 5, 256, stamp_claim_bytes(fcfg.shift), st>>>(static_cast<uint8_t*>(d_lin), lin_words, fcfg, sp, cur_epoch,
                                                          cfg.window, cfg.rows, hist.p);
                     check_launch();

@@ -294,155 +294,6 @@ __global__ void __launch_bounds__(256, 5) k_stamp_warp(uint8_t* __restrict__ lin
     }
 }
 
-// Sparse slices, piece by piece (C3: ~200 marks per 32 KB slice, clustered on
-// the ~2 active sources' 1 KB cells): one WARP per slice stages each touched
-// piece (2^(shift-5) bytes: a g' = 1024 cell at 32 KB slices) in shared
-// memory, stamps its marks there (a shared CAS per mark: duplicates see `cur`
-// and are not counted twice) and writes the piece back with coalesced 16-byte
-// stores. Every touched DRAM sector moves once in each direction as part of a
-// full piece, instead of one L2 read-modify-write per mark (k_stamp_warp).
-// Software pipeline per warp: while slice i is stamped, slice i+1's marks are
-// in registers and its pieces are in flight (cp.async into the other stage).
-// Slices touching more than kCellBatch pieces (rare) stamp in place in HBM
-// with a CAS per mark (mark_epoch_global).
-constexpr int kCellBatch = 4;
-constexpr int kCellU = 8;  // marks per lane held in registers (256 per slice)
-inline uint32_t stamp_cells_smem(uint32_t shift) { return 8u * 2u * kCellBatch * (1u << (shift - 5)); }
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-__global__ void __launch_bounds__(256, 3) k_stamp_cells(uint8_t* __restrict__ lin, uint64_t row_words, FineCfg f,
-                                                     uint32_t sparse_max, uint32_t cur, uint32_t k, uint32_t rows,
-                                                     unsigned long long* __restrict__ hist) {
-    __shared__ int32_t s_h[kStampWarpRows][128];  // net transitions by (row, age)
-    __shared__ unsigned long long s_moved;         // piece bytes read (= written), statistics
-    extern __shared__ __align__(16) uint8_t s_cells[];
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t ps = f.shift - 5;  // log2 piece bytes (32 pieces per slice)
-    const uint32_t pbytes = 1u << ps, pvecs = pbytes >> 4;
-    uint8_t* stage[2] = {s_cells + (2 * warp) * kCellBatch * pbytes, s_cells + (2 * warp + 1) * kCellBatch * pbytes};
-    for (uint32_t q = threadIdx.x; q < kStampWarpRows * 128; q += blockDim.x) (&s_h[0][0])[q] = 0;
-    if (threadIdx.x == 0) s_moved = 0;
-    __syncthreads();
-    uint32_t moved = 0;
-    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-
-    // a slice in the pipeline: its marks (first 32 * kCellU in registers,
-    // two u16 per register), count and touched-piece mask
-    struct Slice {
-        uint32_t fb, n, mask, wide;
-        uint32_t m[kCellU / 2];
-    };
-    auto load = [&](uint32_t fb) -> Slice {
-        Slice x{fb, 0u, 0u, 0u, {}};
-        if (fb >= f.nfine) return x;
-        const uint32_t n = min(__ldg(f.count + fb), f.cap);
-        if (n == 0 || n > sparse_max) return x;  // empty, or k_slice_stamp's
-        x.n = n;
-        const uint16_t* e = f.bins + static_cast<uint64_t>(fb) * f.cap;
-        uint32_t mask = 0;
-#pragma unroll
-        for (int u = 0; u < kCellU; u += 2) {
-            const uint32_t q0 = lane + 32u * u, q1 = q0 + 32u;
-            const uint32_t lo = q0 < n ? __ldg(e + q0) : 0xFFFFu, hi = q1 < n ? __ldg(e + q1) : 0xFFFFu;
-            x.m[u / 2] = lo | (hi << 16);
-            if (q0 < n) mask |= 1u << (lo >> ps);
-            if (q1 < n) mask |= 1u << (hi >> ps);
-        }
-        for (uint32_t q = lane + 32u * kCellU; q < n; q += 32) mask |= 1u << (static_cast<uint32_t>(__ldg(e + q)) >> ps);
-        x.mask = __reduce_or_sync(0xFFFFFFFFu, mask);
-        if (__popc(x.mask) > kCellBatch) {  // too spread out for the stage: in place
-            x.wide = 1;
-            x.mask = 0;
-        }
-        return x;
-    };
-    auto issue = [&](const Slice& x, uint8_t* buf) {
-        const uint8_t* g = lin + (static_cast<uint64_t>(x.fb) << f.shift);
-        uint32_t bm = x.mask;
-        for (int j = 0; bm; ++j, bm &= bm - 1) {
-            const uint32_t pc = __ffs(bm) - 1;
-            for (uint32_t q = lane; q < pvecs; q += 32)
-                cp_async16(buf + j * pbytes + 16u * q, g + (static_cast<uint64_t>(pc) << ps) + 16u * q);
-        }
-        cp_async_commit();  // one group per slice (possibly empty)
-    };
-
-    Slice cur_s = load(blockIdx.x * (blockDim.x >> 5) + warp);
-    issue(cur_s, stage[0]);
-    for (uint32_t it = 0; cur_s.fb < f.nfine; ++it) {
-        const Slice nxt = load(cur_s.fb + nwarps);
-        issue(nxt, stage[(it + 1) & 1]);
-        cp_async_wait1();  // this slice's pieces have landed
-        __syncwarp();
-        if (cur_s.wide) {
-            const uint64_t w0 = static_cast<uint64_t>(cur_s.fb) << f.shift;
-            const uint16_t* e = f.bins + static_cast<uint64_t>(cur_s.fb) * f.cap;
-            for (uint32_t q = lane; q < cur_s.n; q += 32) mark_epoch_global(lin, w0 + __ldg(e + q), row_words, cur, hist);
-        } else if (cur_s.n) {
-            uint8_t* buf = stage[it & 1];
-            const uint64_t w0 = static_cast<uint64_t>(cur_s.fb) << f.shift;
-            const uint32_t row_a = static_cast<uint32_t>(w0 / row_words);
-            const uint64_t split = (static_cast<uint64_t>(row_a) + 1) * row_words - w0;  // offsets >= split: next row
-            const uint16_t* e = f.bins + static_cast<uint64_t>(cur_s.fb) * f.cap;
-            uint32_t fresh_a = 0, fresh_b = 0;  // transitions onto `cur` in rows row_a, row_a + 1
-            for (uint32_t q0 = 0; q0 < cur_s.n; q0 += 32) {  // warp-uniform trip count (match_any below)
-                const uint32_t q = q0 + lane;
-                uint32_t key = 0xFFFFFFFFu;
-                if (q < cur_s.n) {
-                    const uint32_t j = q0 >> 5;
-                    const uint32_t off = j < kCellU ? (cur_s.m[j >> 1] >> (16 * (j & 1))) & 0xFFFFu
-                                                    : static_cast<uint32_t>(__ldg(e + q));
-                    const uint32_t pc = off >> ps;
-                    const uint32_t slot = __popc(cur_s.mask & ((1u << pc) - 1u));
-                    const uint32_t old = stamp_byte_shared(buf + slot * pbytes, off & (pbytes - 1u), cur);
-                    if (old != cur) {
-                        const uint32_t second = off >= split ? 1u : 0u;
-                        fresh_a += second ^ 1u;
-                        fresh_b += second;
-                        const uint32_t age = (cur - old) & 0xFFu;
-                        if (age < k) key = ((row_a + second) << 8) | age;
-                    }
-                }
-                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
-                if (key != 0xFFFFFFFFu && lane == __ffs(peers) - 1u)
-                    atomicSub(&s_h[(key >> 8) & 3u][key & 0xFFu], __popc(peers));
-            }
-            __syncwarp();
-            uint8_t* g = lin + w0;
-            uint32_t bm = cur_s.mask;
-            for (int j = 0; bm; ++j, bm &= bm - 1) {
-                const uint32_t pc = __ffs(bm) - 1;
-                uint4* dst = reinterpret_cast<uint4*>(g + (static_cast<uint64_t>(pc) << ps));
-                const uint4* src = reinterpret_cast<const uint4*>(buf + j * pbytes);
-                for (uint32_t q = lane; q < pvecs; q += 32) __stcs(dst + q, src[q]);
-            }
-            moved += __popc(cur_s.mask);
-            fresh_a = __reduce_add_sync(0xFFFFFFFFu, fresh_a);
-            fresh_b = __reduce_add_sync(0xFFFFFFFFu, fresh_b);
-            if (lane == 0) {
-                if (fresh_a) atomicAdd(&s_h[row_a & 3u][0], static_cast<int32_t>(fresh_a));
-                if (fresh_b) atomicAdd(&s_h[(row_a + 1u) & 3u][0], static_cast<int32_t>(fresh_b));
-            }
-        }
-        __syncwarp();  // the stage is read out before slice i+2's pieces land in it
-        cur_s = nxt;
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    if (lane == 0 && moved) atomicAdd(&s_moved, static_cast<unsigned long long>(moved) << ps);
-    __syncthreads();
-    for (uint32_t q = threadIdx.x; q < rows * k; q += blockDim.x) {
-        const uint32_t h = q / k, age = q % k;
-        const int32_t v = s_h[h][age];
-        if (v) atomicAdd(hist + h * 256ull + ((cur - age) & 0xFFu), static_cast<unsigned long long>(static_cast<long long>(v)));
-    }
-    if (threadIdx.x == 0 && s_moved) atomicAdd(f.streamed, s_moved);
-}
-
 // Sweep [w0, w0+n) of the table: stamps with age >= expired become age
 // exactly `expired` (no histogram change: such recorders are outside every
 // window, k <= expired).

@@ -164,6 +164,13 @@ srla_status srla_copy_to_device(int device, void* dst, const void* src, uint64_t
     return SRLA_OK;
 }
 
+srla_status srla_copy_to_host(int device, void* dst, const void* src, uint64_t bytes) {
+    if (bytes && (!dst || !src)) return srla_internal_set_error(SRLA_E_INVALID, "null argument");
+    ING_CK(cudaSetDevice(device));
+    if (bytes) ING_CK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return SRLA_OK;
+}
+
 srla_status srla_parse_srlt(const void* d_bytes, uint64_t nbytes, srla_record* d_out, uint64_t* n_out, void* stream) {
     if (!n_out || (nbytes && !d_bytes)) return srla_internal_set_error(SRLA_E_INVALID, "null argument");
     *n_out = 0;

@@ -166,7 +166,7 @@ EXPORTED_SYMBOLS = (
     "srla_copy_to_device", "srla_state_blocks", "srla_block_sums", "srla_scan_device",
     "srla_nccl_unique_id", "srla_transport_nccl", "srla_transport_nccl_destroy", "srla_shard_create",
     "srla_shard_destroy", "srla_shard_engine", "srla_shard_last_report", "srla_shard_process_slice",
-    "srla_export_range", "srla_import_range", "srla_host_alloc", "srla_host_free",
+    "srla_export_range", "srla_import_range", "srla_host_alloc", "srla_host_free", "srla_copy_to_host",
 )
 
 

@@ -14,5 +14,6 @@ timeout 900 python bench.py --workload c3 --no-cpu-baseline > $O/bench_c3.jsonl 
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $O/launches_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_scan_bin|k_split|k_slice_apply' -s 30 -c 3 \
-   -o $O/prof_scan python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $O/prof_scan.log 2>&1
+   -o /tmp/prof_scan python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > $O/prof_scan.log 2>&1
+ncu -i /tmp/prof_scan.ncu-rep --page raw --csv > $O/prof_scan.raw.csv 2>/dev/null   # gpurun brings back <= 64 MiB
 ls -la $O

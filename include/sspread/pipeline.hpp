@@ -218,7 +218,7 @@ class DetectPipeline {
         if (due) {
             const srla_status s = srla_candidates(sea_.eng(), nullptr, 0, &cands);
             if (s != SRLA_OK && s != SRLA_E_CAPACITY) detail::raise_status(s, "srla_candidates");
-            if (entries_.size() < cands) entries_.resize(cands + cands / 4);
+            entries_.reserve(cands);
         }
         uint64_t n_out = 0, kept = 0;
         detail::check(srla_end_slice(sea_.eng(), slice_id, due ? 1 : 0, entries_.data(), entries_.size(), &n_out, &kept),
@@ -240,7 +240,7 @@ class DetectPipeline {
 
     RunConfig cfg_;
     EstimatorArray<W> sea_;
-    std::vector<srla_entry> entries_;  // report hand-off buffer, reused across slices
+    detail::PinnedEntries entries_;  // report hand-off buffer (pinned: entries mapped on the device, one DMA)
     mutable CandidateList csip_;
     mutable bool csip_valid_ = false;
     OrientStats stats_;

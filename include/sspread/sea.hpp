@@ -111,6 +111,37 @@ struct WindowReport {
 
 namespace detail {
 
+[[noreturn]] inline void raise_status(srla_status st, const char* call);
+
+// Page-locked buffer of report entries (srla_host_alloc): the engine maps
+// (host, weight) to entries on the device and hands them off in one DMA.
+class PinnedEntries {
+  public:
+    PinnedEntries() = default;
+    PinnedEntries(const PinnedEntries&) = delete;
+    PinnedEntries& operator=(const PinnedEntries&) = delete;
+    ~PinnedEntries() { srla_host_free(p_); }
+    void reserve(uint64_t n) {
+        if (n <= cap_) return;
+        srla_host_free(p_);
+        p_ = nullptr;
+        cap_ = 0;
+        void* q = nullptr;
+        const uint64_t c = std::max<uint64_t>(n + n / 4, 1024);
+        const srla_status s = srla_host_alloc(c * sizeof(srla_entry), &q);
+        if (s != SRLA_OK) raise_status(s, "srla_host_alloc");
+        p_ = static_cast<srla_entry*>(q);
+        cap_ = c;
+    }
+    srla_entry* data() const noexcept { return p_; }
+    uint64_t size() const noexcept { return cap_; }
+    const srla_entry& operator[](uint64_t i) const noexcept { return p_[i]; }
+
+  private:
+    srla_entry* p_ = nullptr;
+    uint64_t cap_ = 0;
+};
+
 [[noreturn]] inline void raise_status(srla_status st, const char* call) {
     const std::string msg = srla_last_error();
     if (st == SRLA_E_INVALID) throw std::invalid_argument(msg);

@@ -402,6 +402,27 @@ srla_status srla_orient_records(const srla_record* d_in, uint64_t n, uint32_t pr
 srla_status srla_slice_bounds(const srla_record* d_recs, uint64_t n, uint32_t slice_seconds, uint64_t* offsets,
                               uint64_t cap, uint64_t* n_slices, void* stream);
 
+/* ---- exact sliding-window cardinalities on the device (ground truth;
+ * oracle.hpp:45-203). SliceRingStore semantics: pairs
+ * observed in the current slice, a ring of the last max_window slices, a
+ * window [t, t+k) observable only at the end of slice t+k-1 (SRLA_E_RANGE
+ * with the reference's message otherwise). */
+typedef struct srla_exact srla_exact;
+srla_status srla_exact_create(uint32_t max_window, int device, srla_exact** out);
+srla_status srla_exact_destroy(srla_exact* x);
+/* SliceRingStore::observe for a batch: (src = aip, dst = bip) of every record
+ * joins the current slice (host or device records, like srla_scan_batch). */
+srla_status srla_exact_observe(srla_exact* x, const srla_record* recs, uint64_t n, int on_device);
+srla_status srla_exact_end_slice(srla_exact* x);
+srla_status srla_exact_current_slice(srla_exact* x, uint64_t* slice);
+/* PairRecorderStore::pair_count: distinct pairs live in the ring. */
+srla_status srla_exact_pair_count(srla_exact* x, uint64_t* n);
+/* cardinalities(t, k): every host with a nonzero distinct count, ascending by
+ * address, and its count. hosts = NULL (or cap too small) returns
+ * SRLA_E_CAPACITY with *n_out = the number of hosts. */
+srla_status srla_exact_cardinalities(srla_exact* x, uint64_t window_start, uint32_t window, uint32_t* hosts,
+                                     uint64_t* counts, uint64_t cap, uint64_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,8 +5,8 @@
 // full and a sink is set, slide; pipeline.hpp:110-129) but the record batch
 // crosses to the device once and the candidate list stays in HBM between
 // slices. process_slice_device() is an addition for records already resident
-// on the GPU. Exact-cardinality ground truth (run_oracle, oracle.hpp) is not
-// part of the hot path and is not provided.
+// on the GPU. Exact-cardinality ground truth (run_oracle) runs on the device
+// store of oracle.hpp.
 #pragma once
 
 #include <algorithm>
@@ -22,6 +22,7 @@
 #include <thread>
 #include <vector>
 
+#include "oracle.hpp"
 #include "sea.hpp"
 #include "trace.hpp"
 
@@ -249,6 +250,52 @@ class DetectPipeline {
     double total_scan_ms_ = 0;
     double total_estimate_ms_ = 0;
 };
+
+/// Ground-truth record for one window (pipeline.hpp:183-187).
+struct TruthEntry {
+    uint64_t window_start = 0;
+    uint32_t host = 0;
+    uint64_t cardinality = 0;
+};
+
+enum class OracleEngine { ring, pair_recorders, both };
+
+inline constexpr uint64_t kOraclePairGuard = 100'000'000;
+
+/// pipeline.hpp:189-247: exact sliding-window cardinalities over a trace —
+/// per complete window, every host reaching `min_cardinality`, sorted by
+/// address. Both reference engines are the same device store here
+/// (oracle.hpp), so OracleEngine::both has nothing to cross-check; the pair
+/// guard and its message are the reference's.
+inline void run_oracle(const RunConfig& cfg, const std::string& trace_path, OracleEngine engine,
+                       uint64_t min_cardinality, const std::function<void(const TruthEntry&)>& sink,
+                       uint64_t max_pairs = kOraclePairGuard) {
+    cfg.validate();
+    const uint32_t k = cfg.sea.window;
+    if (engine != OracleEngine::ring) RecorderModel::with_bits(cfg.sea.recorder_bits).validate_window(k);
+    SliceRingStore store(k, cfg.device);
+    OrientStats stats;
+    uint64_t observed = 0;
+    const auto on_slice = [&](uint64_t id, std::vector<TraceRecord>&& records) {
+        for (const auto& r : records) store.observe(r.src, r.dst);
+        if (id + 1 >= k) {
+            const uint64_t t = id + 1 - k;
+            for (const auto& [host, n] : store.cardinalities(t, k))  // ascending by address
+                if (n >= min_cardinality) sink(TruthEntry{t, host, n});
+        }
+        store.end_slice();
+    };
+    SlicePartitioner partitioner(cfg.slice_seconds);
+    for_each_record(trace_path, [&](const TraceRecord& r) {
+        const auto oriented = orient_record(r, cfg.a_network, stats);
+        if (!oriented) return;
+        if (++observed > max_pairs)
+            throw InputError("trace exceeds the oracle pair guard (" + std::to_string(max_pairs) +
+                             " records); raise --max-pairs for a machine that can hold it");
+        partitioner.push(*oriented, on_slice);
+    });
+    partitioner.finish(on_slice);
+}
 
 // Runtime width -> storage word (pipeline.hpp:173-180).
 template <typename Fn>

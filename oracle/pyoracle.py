@@ -151,6 +151,12 @@ class Checker:
         if self.prefix == "ref":  # reference-only: parallel slice generator, record-order flow
             sigs.update({
                 "pipeline_save_snapshot": (i32, [vp, C.c_char_p, C.c_char_p, C.c_size_t]),
+                "exact_create": (vp, [i32, u32, u32, C.c_char_p, C.c_size_t]),
+                "exact_destroy": (None, [vp]),
+                "exact_observe": (None, [vp, vp, u64]),
+                "exact_end_slice": (None, [vp]),
+                "exact_pair_count": (u64, [vp]),
+                "exact_cardinalities": (u64, [vp, u64, u32, vp, vp, C.c_char_p, C.c_size_t]),
                 "generate_slice": (u64, [C.POINTER(OrcSpec), u64, u32, vp, C.c_char_p, C.c_size_t]),
                 "flow_create": (vp, [C.POINTER(OrcConfig), u32, C.c_char_p, C.c_size_t]),
                 "flow_destroy": (None, [vp]),
@@ -476,3 +482,39 @@ class Flow:
         out = np.empty(max(1, nb), np.uint64)
         self.chk.f("flow_state_blocks")(self.h, row, kind, _ptr(out))
         return out[:nb]
+
+
+class ExactRef:
+    """The reference's exact stores (oracle.hpp): SliceRingStore (engine "ring")
+    or PairRecorderStore (engine "pairs"). Reference checker only."""
+
+    def __init__(self, chk: Checker, engine: str, max_window: int, recorder_bits: int = 8):
+        err = C.create_string_buffer(256)
+        self.chk = chk
+        self.h = chk.f("exact_create")(0 if engine == "ring" else 1, recorder_bits, max_window, err, 256)
+        if not self.h:
+            raise ValueError(err.value.decode())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.chk.f("exact_destroy")(self.h)
+            self.h = None
+
+    def observe(self, recs):
+        recs = np.ascontiguousarray(recs, dtype=np.uint32).reshape(-1, 3)
+        self.chk.f("exact_observe")(self.h, _ptr(recs), len(recs))
+
+    def end_slice(self):
+        self.chk.f("exact_end_slice")(self.h)
+
+    def pair_count(self):
+        return self.chk.f("exact_pair_count")(self.h)
+
+    def cardinalities(self, t, k):
+        err = C.create_string_buffer(256)
+        n = self.chk.f("exact_cardinalities")(self.h, t, k, None, None, err, 256)
+        if n == 0xFFFFFFFFFFFFFFFF:
+            raise IndexError(err.value.decode())
+        hosts, counts = np.empty(max(1, n), np.uint32), np.empty(max(1, n), np.uint64)
+        self.chk.f("exact_cardinalities")(self.h, t, k, _ptr(hosts), _ptr(counts), err, 256)
+        return hosts[:n], counts[:n]

@@ -6,6 +6,7 @@
 // reference arm. No reference source is copied here; this file only calls the
 // reference's public API with the same entry points as srla_oracle.h
 // (prefix `ref_` instead of `orc_`).
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -16,6 +17,7 @@
 #include <vector>
 
 #include "sspread/generator.hpp"
+#include "sspread/oracle.hpp"
 #include "sspread/pipeline.hpp"
 #include "sspread/sea.hpp"
 #include "sspread/snapshot.hpp"
@@ -515,6 +517,58 @@ void ref_flow_state_blocks(void* f, uint32_t row, int kind, uint64_t* out) {
 // the same block sums over any byte buffer (records, exported rows)
 void ref_block_sums(const void* p, uint64_t bytes, uint32_t threads, uint64_t* out) {
     block_sums(static_cast<const uint8_t*>(p), bytes, threads, out);
+}
+
+// ---- the reference's exact stores (oracle.hpp): ring (engine 0) or pair recorders (engine 1)
+struct ExactRef {
+    std::unique_ptr<SliceRingStore> ring;
+    std::unique_ptr<PairRecorderStore> pairs;
+};
+void* ref_exact_create(int engine, uint32_t recorder_bits, uint32_t max_window, char* err, size_t errlen) {
+    try {
+        auto* x = new ExactRef();
+        if (engine == 0) x->ring = std::make_unique<SliceRingStore>(max_window);
+        else x->pairs = std::make_unique<PairRecorderStore>(recorder_bits, max_window);
+        return x;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return nullptr;
+    }
+}
+void ref_exact_destroy(void* h) { delete static_cast<ExactRef*>(h); }
+void ref_exact_observe(void* h, const uint32_t* recs, uint64_t n) {
+    auto* x = static_cast<ExactRef*>(h);
+    for (uint64_t i = 0; i < n; ++i) {
+        if (x->ring) x->ring->observe(recs[3 * i + 1], recs[3 * i + 2]);
+        else x->pairs->observe(recs[3 * i + 1], recs[3 * i + 2]);
+    }
+}
+void ref_exact_end_slice(void* h) {
+    auto* x = static_cast<ExactRef*>(h);
+    if (x->ring) x->ring->end_slice();
+    else x->pairs->end_slice();
+}
+uint64_t ref_exact_pair_count(void* h) {
+    auto* x = static_cast<ExactRef*>(h);
+    return x->pairs ? x->pairs->pair_count() : 0;
+}
+// cardinalities(t, k) sorted by host; returns the count (-1 as UINT64_MAX on a throw: err holds the message)
+uint64_t ref_exact_cardinalities(void* h, uint64_t t, uint32_t k, uint32_t* hosts, uint64_t* counts, char* err,
+                                 size_t errlen) {
+    auto* x = static_cast<ExactRef*>(h);
+    try {
+        auto c = x->ring ? x->ring->cardinalities(t, k) : x->pairs->cardinalities(t, k);
+        std::sort(c.begin(), c.end());
+        if (hosts)
+            for (size_t i = 0; i < c.size(); ++i) {
+                hosts[i] = c[i].first;
+                counts[i] = c[i].second;
+            }
+        return c.size();
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return UINT64_MAX;
+    }
 }
 
 // ---- ingest front end: the reference's own orient_record / SlicePartitioner / for_each_record

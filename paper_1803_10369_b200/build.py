@@ -13,7 +13,7 @@ LIB = os.path.join(LIBDIR, "libsrla_b200.so")
 DROPIN_BENCH = os.path.join(LIBDIR, "bench_dropin")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["engine.cu", "generator.cu", "shard.cu", "ingest.cu"]
+CU_SOURCES = ["engine.cu", "generator.cu", "shard.cu", "ingest.cu", "exact.cu"]
 CXX_SOURCES = ["host_math.cpp"]
 
 

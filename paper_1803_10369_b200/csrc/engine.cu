@@ -717,9 +717,11 @@ struct Engine {
         const bool small = total_words * wb < (256ull << 20);
         if (!forced && small) return false;
         uint32_t shift = 0;
-        // 16 MB coarse regions: K1's fan-out (regions per tile) against the
-        // split's (fine slices per region); measured best on C2 (8-64 MB swept)
-        uint64_t region_bytes = 16ull << 20;
+        // 8 MB coarse regions: K1's fan-out (regions per tile) against the
+        // split's (fine slices per region); measured best on C2 with the
+        // device-count ordering and a full-GPU early split (4-64 MB swept,
+        // profiles/r02/ab_region_waves.txt)
+        uint64_t region_bytes = 8ull << 20;
         if (const char* rm = std::getenv("SRLA_REGION_MB")) region_bytes = std::strtoull(rm, nullptr, 10) << 20;
         while (lin_bytes(1ull << (shift + 1)) <= region_bytes) ++shift;
         if (forced)
@@ -911,7 +913,7 @@ struct Engine {
         with_w([&](auto w) {
             using W = decltype(w);
             // an early split leaves room for the ordering phase's kernels
-            static const uint32_t waves = [] { const char* v = std::getenv("SRLA_SPLIT_WAVES"); return v ? static_cast<uint32_t>(std::atoi(v)) : 2u; }();
+            static const uint32_t waves = [] { const char* v = std::getenv("SRLA_SPLIT_WAVES"); return v ? static_cast<uint32_t>(std::atoi(v)) : 16u; }();
             const uint64_t max_tiles = pending_entries / kSplitTile + R;
             k_split<W><<<static_cast<uint32_t>(std::min<uint64_t>(max_tiles, sms * (s == st ? 8u : waves))), kSplitThreads, split_smem, s>>>(
                 bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg, ecfg(),

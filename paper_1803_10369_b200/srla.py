@@ -141,6 +141,13 @@ def load_library(path: str = LIB_PATH):
         "srla_parse_srlt": (i32, [vp, u64, vp, C.POINTER(u64), vp]),
         "srla_orient_records": (i32, [vp, u64, u32, u32, vp, C.POINTER(u64), C.POINTER(COrientStats), vp]),
         "srla_slice_bounds": (i32, [vp, u64, u32, vp, u64, C.POINTER(u64), vp]),
+        "srla_exact_create": (i32, [u32, i32, C.POINTER(vp)]),
+        "srla_exact_destroy": (i32, [vp]),
+        "srla_exact_observe": (i32, [vp, vp, u64, i32]),
+        "srla_exact_end_slice": (i32, [vp]),
+        "srla_exact_current_slice": (i32, [vp, C.POINTER(u64)]),
+        "srla_exact_pair_count": (i32, [vp, C.POINTER(u64)]),
+        "srla_exact_cardinalities": (i32, [vp, u64, u32, vp, vp, u64, C.POINTER(u64)]),
         "srla_export_range": (i32, [vp, u32, i32, u64, vp, u64]),
         "srla_import_range": (i32, [vp, u32, i32, u64, vp, u64]),
         "srla_scan_device": (i32, [vp, vp, u64, vp, vp, u64, C.POINTER(u64)]),
@@ -167,6 +174,8 @@ EXPORTED_SYMBOLS = (
     "srla_nccl_unique_id", "srla_transport_nccl", "srla_transport_nccl_destroy", "srla_shard_create",
     "srla_shard_destroy", "srla_shard_engine", "srla_shard_last_report", "srla_shard_process_slice",
     "srla_export_range", "srla_import_range", "srla_host_alloc", "srla_host_free", "srla_copy_to_host",
+    "srla_exact_create", "srla_exact_destroy", "srla_exact_observe", "srla_exact_end_slice",
+    "srla_exact_current_slice", "srla_exact_pair_count", "srla_exact_cardinalities",
 )
 
 
@@ -544,6 +553,55 @@ class DeviceTraceGenerator:
         t = torch.empty((max(1, n), 3), dtype=torch.int32, device=f"cuda:{self.device}")
         self.generate_into(s, t.data_ptr(), n, torch.cuda.current_stream(self.device).cuda_stream)
         return t[:n]
+
+
+class ExactStore:
+    """Exact sliding-window cardinalities on the device (srla_exact_*): the
+    reference's SliceRingStore (oracle.hpp:136-203) over HBM-resident sorted
+    pair sets."""
+
+    def __init__(self, max_window: int, device: int = 0):
+        lib = load_library()
+        h = C.c_void_p()
+        _check(lib.srla_exact_create(max_window, device, C.byref(h)))
+        self._h, self.max_window, self.device = h, max_window, device
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.srla_exact_destroy(self._h)
+            self._h = None
+
+    def observe(self, recs):
+        if _is_torch_cuda(recs):
+            ptr, n, on_dev = recs.data_ptr(), recs.shape[0], 1
+        else:
+            recs = _as_records(recs)
+            ptr, n, on_dev = recs.ctypes.data, recs.shape[0], 0
+        _check(_lib.srla_exact_observe(self._h, C.c_void_p(ptr), n, on_dev))
+
+    def end_slice(self):
+        _check(_lib.srla_exact_end_slice(self._h))
+
+    @property
+    def current_slice(self) -> int:
+        v = C.c_uint64()
+        _check(_lib.srla_exact_current_slice(self._h, C.byref(v)))
+        return v.value
+
+    def pair_count(self) -> int:
+        v = C.c_uint64()
+        _check(_lib.srla_exact_pair_count(self._h, C.byref(v)))
+        return v.value
+
+    def cardinalities(self, t: int, k: int):
+        """-> (hosts ascending, counts) of every host with a nonzero count in [t, t+k)."""
+        n = C.c_uint64()
+        rc = _lib.srla_exact_cardinalities(self._h, t, k, None, None, 0, C.byref(n))
+        if rc not in (OK, E_CAPACITY):
+            _check(rc)
+        hosts, counts = np.empty(max(1, n.value), np.uint32), np.empty(max(1, n.value), np.uint64)
+        _check(_lib.srla_exact_cardinalities(self._h, t, k, _ptr(hosts), _ptr(counts), len(hosts), C.byref(n)))
+        return hosts[: n.value], counts[: n.value]
 
 
 def block_sums(t) -> np.ndarray:

@@ -5,6 +5,7 @@
 //   R <window_start> <window> <n>
 //   <host> <weight> <has_estimate> <estimate as u64 bits> <super>   (n lines)
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <iostream>
@@ -13,7 +14,42 @@
 
 #include "sspread/report_io.hpp"
 
+// report_lines truth <truth.csv> <reports.jsonl> <out.txt>: read_truth +
+// write_truth_line, then evaluate_windows of the reports against the truth
+// (report_io.hpp:87-171); errors are printed as their message.
+static int truth_mode(char** argv) {
+    std::ofstream out(argv[4]);
+    char buf[128];
+    try {
+        const auto truth = sspread::read_truth(argv[2]);
+        for (const auto& t : truth) sspread::write_truth_line(out, t);
+        const auto reports = sspread::read_report(argv[3]);
+        const auto ev = sspread::evaluate_windows(reports, truth);
+        for (const auto& w : ev.windows) {
+            out << "window " << w.window_start;
+            if (w.metrics) {
+                const auto& m = *w.metrics;
+                out << ' ' << m.truth_size << ' ' << m.detected_size << ' ' << m.false_positives << ' '
+                    << m.false_negatives;
+                for (double v : {m.fpr, m.fnr, m.tfr}) {
+                    std::snprintf(buf, sizeof buf, " %.17g", v);
+                    out << buf;
+                }
+            } else {
+                out << " undefined";
+            }
+            out << '\n';
+        }
+        std::snprintf(buf, sizeof buf, "%.17g %.17g %.17g", ev.mean_fpr, ev.mean_fnr, ev.mean_tfr);
+        out << "mean " << ev.defined_windows << ' ' << buf << '\n';
+    } catch (const std::exception& e) {
+        out << "error " << e.what() << '\n';
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc == 5 && std::string(argv[1]) == "truth") return truth_mode(argv);
     if (argc != 4) return 2;
     std::ifstream in(argv[1]);
     std::ofstream out(argv[2]);

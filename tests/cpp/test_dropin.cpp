@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "sspread/oracle.hpp"
 #include "sspread/pipeline.hpp"
 #include "sspread/sea.hpp"
 #include "sspread/snapshot.hpp"
@@ -328,6 +329,99 @@ static void test_pipeline_validation() {
     CHECK_THROWS_AS(rc.validate(), ConfigError);
 }
 
+// exact stores (oracle.hpp), the reference's test_oracle.cpp cases restated
+static void test_exact_stores() {
+    {
+        PairRecorderStore store(8, 4);
+        store.observe(1, 100);
+        store.observe(1, 100);  // a repeated pair counts once
+        CHECK(store.cardinality(1, 0, 1) == 1);
+        CHECK(store.pair_count() == 1);
+        for (uint32_t b = 0; b < 7; ++b) store.observe(2, b);
+        CHECK(store.cardinality(2, 0, 1) == 7);
+        CHECK(store.cardinality(3, 0, 1) == 0);
+        CHECK(store.pair_count() == 8);
+    }
+    {
+        PairRecorderStore store(8, 4);  // 25 new peers of host 7 in each of 4 slices
+        for (uint32_t s = 0; s < 4; ++s) {
+            for (uint32_t b = 0; b < 25; ++b) store.observe(7, s * 25 + b);
+            if (s < 3) store.end_slice();
+        }
+        CHECK(store.cardinality(7, 0, 4) == 100);
+        CHECK(store.cardinality(7, 3, 1) == 25);
+        CHECK(store.cardinality(7, 2, 2) == 50);
+        store.end_slice();
+        CHECK(store.cardinality(7, 1, 4) == 75);
+        CHECK_THROWS_AS(store.cardinality(7, 0, 4), std::out_of_range);
+        CHECK_THROWS_AS(store.cardinality(7, 4, 5), std::out_of_range);
+    }
+    {
+        SliceRingStore ring(2);
+        for (uint32_t b = 0; b < 10; ++b) ring.observe(1, b);
+        for (uint32_t b = 0; b < 9; ++b) ring.observe(2, b);
+        for (uint32_t b = 0; b < 30; ++b) ring.observe(3, 100 + b);
+        CHECK(ring.super_points(0, 1, 10) == (std::set<uint32_t>{1, 3}));
+    }
+    CHECK_THROWS_AS(PairRecorderStore(1, 4), std::invalid_argument);  // window beyond a 1-bit recorder
+    // both stores against a brute-force recount on random slices
+    std::mt19937_64 rng(0x5EED);
+    for (int trial = 0; trial < 12; ++trial) {
+        const uint32_t k = 1 + static_cast<uint32_t>(rng() % 5);
+        PairRecorderStore pairs(8, k);
+        SliceRingStore ring(k);
+        std::vector<std::vector<std::pair<uint32_t, uint32_t>>> slices;
+        const int total = 3 + static_cast<int>(rng() % 6);
+        for (int s = 0; s < total; ++s) {
+            std::vector<std::pair<uint32_t, uint32_t>> sl;
+            for (int i = static_cast<int>(rng() % 150); i > 0; --i) {
+                const uint32_t a = static_cast<uint32_t>(rng() % 9), b = static_cast<uint32_t>(rng() % 50);
+                pairs.observe(a, b);
+                ring.observe(a, b);
+                sl.push_back({a, b});
+            }
+            slices.push_back(sl);
+            const uint32_t kk = std::min<uint32_t>(k, static_cast<uint32_t>(s + 1));
+            const uint64_t t = static_cast<uint64_t>(s) + 1 - kk;
+            std::vector<std::set<uint32_t>> seen(9);
+            for (uint64_t w = t; w <= static_cast<uint64_t>(s); ++w)
+                for (const auto& [a, b] : slices[w]) seen[a].insert(b);
+            for (uint32_t a = 0; a < 9; ++a) {
+                CHECK(pairs.cardinality(a, t, kk) == seen[a].size());
+                CHECK(ring.cardinality(a, t, kk) == seen[a].size());
+            }
+            CHECK(pairs.super_points(t, kk, 5) == ring.super_points(t, kk, 5));
+            pairs.end_slice();
+            ring.end_slice();
+        }
+    }
+    // score (oracle.hpp:30-43)
+    CHECK(!score({1, 2}, {}).has_value());
+    const auto m = score({1, 2, 5}, {2, 3, 5, 8});
+    CHECK(m && m->false_positives == 1 && m->false_negatives == 2 && m->truth_size == 4 && m->detected_size == 3);
+    CHECK(m->fpr == 0.25 && m->fnr == 0.5 && m->tfr == 0.75);
+}
+
+// test_dropin oracle <trace.bin> <out.txt> rows cols g gl bits k theta seed:
+// run_oracle (pipeline.hpp:189-247) over the device store, min cardinality 1
+static int oracle_mode(int argc, char** argv) {
+    if (argc != 12) return 2;
+    RunConfig rc;
+    rc.sea.rows = std::stoul(argv[4]);
+    rc.sea.cols = std::stoul(argv[5]);
+    rc.sea.rough_slots = std::stoul(argv[6]);
+    rc.sea.linear_slots = std::stoul(argv[7]);
+    rc.sea.recorder_bits = std::stoul(argv[8]);
+    rc.sea.window = std::stoul(argv[9]);
+    rc.sea.theta = std::stoul(argv[10]);
+    rc.sea.seed = std::stoull(argv[11], nullptr, 0);
+    rc.slice_seconds = 1;
+    std::ofstream out(argv[3]);
+    run_oracle(rc, argv[2], OracleEngine::both, 1,
+               [&](const TruthEntry& t) { out << t.window_start << ' ' << t.host << ' ' << t.cardinality << '\n'; });
+    return 0;
+}
+
 static int replay(int argc, char** argv) {
     if (argc != 12) {
         std::fprintf(stderr, "usage: replay trace out rows cols g gl bits k theta seed\n");
@@ -414,6 +508,7 @@ static int run_mode(int argc, char** argv) {
 int main(int argc, char** argv) {
     if (argc > 1 && std::string(argv[1]) == "replay") return replay(argc, argv);
     if (argc > 1 && std::string(argv[1]) == "run") return run_mode(argc, argv);
+    if (argc > 1 && std::string(argv[1]) == "oracle") return oracle_mode(argc, argv);
     test_single_pair();
     test_indicator_suppression();
     test_union_view();
@@ -425,6 +520,7 @@ int main(int argc, char** argv) {
     test_snapshot_round_trip();
     test_pipeline_validation();
     test_run_regression_message();
+    test_exact_stores();
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }

@@ -190,3 +190,31 @@ def test_dropin_snapshot_bytes_equal_reference(gpu, ref, oracle, dropin_bin, tmp
     assert _sha_file(mine) == _sha_file(theirs)
     os.remove(mine)
     os.remove(theirs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["pipeline_small", "c1_shape"])
+def test_dropin_run_oracle_matches_reference_ring(gpu, ref, oracle, dropin_bin, tmp_path, name):
+    """run_oracle (device exact store) over an SRLT trace: every complete
+    window's (host, cardinality) list equals the reference SliceRingStore's."""
+    from oracle.pyoracle import ExactRef
+    c, _ = S.SCENARIOS[name]
+    slices = [np.array(x, dtype=np.uint32).reshape(-1, 3).copy() for x in GF.scenario_slices(name, oracle)]
+    for s, x in enumerate(slices):
+        x[:, 0] = 1700000000 + s
+    trace = tmp_path / "t.bin"
+    _write_srlt(trace, np.concatenate(slices))
+    out = tmp_path / "truth.txt"
+    subprocess.run([dropin_bin, "oracle", str(trace), str(out), str(c.rows), str(c.cols), str(c.rough_slots),
+                    str(c.linear_slots), str(c.recorder_bits), str(c.window), str(c.theta), hex(c.seed)],
+                   check=True, timeout=600)
+    got = [tuple(map(int, ln.split())) for ln in open(out) if ln.strip()]
+    ring = ExactRef(ref, "ring", c.window)
+    want = []
+    for s, recs in enumerate(slices):
+        ring.observe(recs)
+        if s + 1 >= c.window:
+            h, n = ring.cardinalities(s + 1 - c.window, c.window)
+            want += [(s + 1 - c.window, int(a), int(b)) for a, b in zip(h, n)]
+        ring.end_slice()
+    assert got == want and len(want) > 0

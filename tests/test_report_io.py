@@ -85,3 +85,51 @@ def test_report_lines_byte_identical_to_reference(dropin_bin, tmp_path, seed):
             if has:
                 assert np.uint64(bits).view(np.float64) == np.uint64(e[3]).view(np.float64) or bits == e[3]
         i += 1 + len(ent)
+
+
+def _truth_case(tmp_path, seed, malformed=None):
+    """A truth CSV and a report file over the same windows (some windows only in
+    the report, hosts partly detected)."""
+    rng = np.random.default_rng(seed)
+    reps = []
+    truth_lines = []
+    for w in range(8):
+        hosts = sorted(set(int(x) for x in rng.integers(0, 2**32, int(rng.integers(0, 30)))))
+        ent = [(h, int(rng.integers(0, 1025)), 1, int(np.float64(rng.random() * 3000).view(np.uint64)),
+                int(rng.random() < 0.5)) for h in hosts]
+        reps.append((w, 10, ent))
+        if w % 3 != 2:  # windows 2 and 5: report only -> undefined
+            for h in hosts[: len(hosts) // 2] + [int(x) for x in rng.integers(0, 2**32, 3)]:
+                truth_lines.append(f"{w},{'.'.join(str((h >> s) & 255) for s in (24, 16, 8, 0))},"
+                                   f"{int(rng.integers(1024, 20000))}")
+    if malformed:
+        truth_lines.insert(len(truth_lines) // 2, malformed)
+    truth = tmp_path / "truth.csv"
+    truth.write_text("\n".join(truth_lines) + "\n\n")
+    return reps, truth
+
+
+@pytest.mark.parametrize("case", ["ok0", "ok1", "bad_ip", "short", "bad_num", "missing_window"])
+def test_truth_io_and_evaluation_match_reference(dropin_bin, tmp_path, case):
+    """read_truth / write_truth_line / evaluate_windows (report_io.hpp:87-171):
+    the drop-in and the reference header print identical results, errors
+    included."""
+    if not os.path.exists(REF_BIN):
+        pytest.skip("oracle/_ref/report_ref not built")
+    malformed = {"bad_ip": "3,10.0.300.1,77", "short": "3,10.0.0.1", "bad_num": "x,10.0.0.1,5"}.get(case)
+    reps, truth = _truth_case(tmp_path, 7 if case == "ok1" else 3, malformed)
+    if case == "missing_window":
+        reps = reps[:-2]
+    inp = tmp_path / "in.txt"
+    _write_input(inp, reps)
+    outs = {}
+    for tag, exe in (("ref", REF_BIN), ("dropin", dropin_bin)):
+        subprocess.run([exe, str(inp), str(tmp_path / f"{tag}.jsonl"), str(tmp_path / f"{tag}.back")], check=True)
+        subprocess.run([exe, "truth", str(truth), str(tmp_path / f"{tag}.jsonl"), str(tmp_path / f"{tag}.eval")],
+                       check=True)
+        outs[tag] = open(tmp_path / f"{tag}.eval").read()
+    assert outs["dropin"] == outs["ref"]
+    if case.startswith("ok"):
+        assert "window 2 undefined" in outs["ref"] and "mean 6 " in outs["ref"]
+    else:
+        assert "\nerror " in "\n" + outs["ref"]

@@ -744,6 +744,9 @@ struct Engine {
         }
         bcfg.region_shift = shift;
         bcfg.nregions = static_cast<uint32_t>((total_words + (1ull << shift) - 1) >> shift);
+        // K1 stages (region, offset) as one word when the table has <= 2^32 recorders (C2: exactly)
+        bcfg.pack = shift < 32 && (uint64_t(bcfg.nregions) << shift) <= (1ull << 32) ? 1u : 0u;
+        if (const char* pk = std::getenv("SRLA_K1_PACK"); pk && pk[0] == '0') bcfg.pack = 0;
         // forced-binned small tables (tests): tiny bins, so the overflow paths run
         uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);
         if (const char* be = std::getenv("SRLA_SMALL_BIN_ENTRIES"); be && small) coarse_total = std::strtoull(be, nullptr, 10);

@@ -66,6 +66,7 @@ struct BinCfg {
     uint32_t nib;           // linear recorders packed two per byte (nibble.cuh)
     uint32_t no_direct;     // a bin overflow sets *overflow instead of marking the table directly
     uint32_t* overflow;
+    uint32_t pack;          // region << region_shift | offset fits 32 bits (tables of <= 2^32 words)
 };
 
 constexpr int kBinThreads = 512;
@@ -272,8 +273,12 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                 if (rr[q][i] != 0xFFFFFFFFu) {
                     const uint32_t reg = rr[q][i] >> 16;
                     const uint32_t p = s_lbase[reg] + (rr[q][i] & 0xFFFFu);
-                    s_off[p] = off[q][i];
-                    s_reg[p] = static_cast<uint16_t>(reg);
+                    if (b.pack) {  // region and offset in one word: the write pass loads one value
+                        s_off[p] = (reg << b.region_shift) | off[q][i];
+                    } else {
+                        s_off[p] = off[q][i];
+                        s_reg[p] = static_cast<uint16_t>(reg);
+                    }
                 }
         __syncthreads();
 
@@ -281,8 +286,15 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
         // consecutive bin slots
         bool ovf = false;
         for (uint32_t idx = tid; idx < total; idx += kBinThreads) {
-            const uint2 wv = s_win[s_reg[idx]];
-            if (idx < wv.y) b.bins[wv.x + idx] = s_off[idx];
+            uint32_t v = s_off[idx], r;
+            if (b.pack) {
+                r = v >> b.region_shift;
+                v &= rmask;
+            } else {
+                r = s_reg[idx];
+            }
+            const uint2 wv = s_win[r];
+            if (idx < wv.y) b.bins[wv.x + idx] = v;
             else ovf = true;
         }
         if (__syncthreads_or(ovf)) {  // a bin is full: mark the rest directly (marks commute)
@@ -292,15 +304,16 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                 continue;
             }
             for (uint32_t idx = tid; idx < total; idx += kBinThreads) {
-                const uint32_t r = s_reg[idx];
+                const uint32_t r = b.pack ? s_off[idx] >> b.region_shift : s_reg[idx];
                 if (idx < s_win[r].y) continue;
+                const uint32_t o = b.pack ? s_off[idx] & rmask : s_off[idx];
                 if (ep.on)
-                    mark_epoch_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << b.region_shift) + s_off[idx],
+                    mark_epoch_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << b.region_shift) + o,
                                       ep.row_words, ep.cur, ep.hist);
                 else if (b.nib)
-                    mark_nibble_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << b.region_shift) + s_off[idx]);
+                    mark_nibble_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << b.region_shift) + o);
                 else
-                    mark_word<W>(lin + (static_cast<uint64_t>(r) << b.region_shift), s_off[idx]);
+                    mark_word<W>(lin + (static_cast<uint64_t>(r) << b.region_shift), o);
             }
         }
         __syncthreads();

@@ -798,8 +798,8 @@ struct Engine {
         }
         with_w([&](auto w) {
             using W = decltype(w);
-            raise_smem_cap(k_scan_bin<W, 4>, kBinSmem);
-            raise_smem_cap(k_scan_bin<W, 0>, kBinSmem);
+            raise_smem_cap(k_scan_bin<W, 4>, bin_smem(bcfg.nregions));
+            raise_smem_cap(k_scan_bin<W, 0>, bin_smem(bcfg.nregions));
         });
         // bulk (TMA) slices need 16-byte slices and rows at least one slice long
         const uint64_t slice_words = 1ull << fs;
@@ -1057,10 +1057,10 @@ struct Engine {
         CK(cudaEventRecord(t_scan0, sk));
         const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
         if (cfg.rows == 4)
-            k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, sk>>>(
+            k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), sk>>>(
                 d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
         else
-            k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, sk>>>(
+            k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), sk>>>(
                 d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
         CK(cudaGetLastError());
         CK(cudaEventRecord(t_scan1, sk));
@@ -1243,9 +1243,9 @@ struct Engine {
             if (use_bins && MAXR <= kBinRows) {
                 const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
                 if (cfg.rows == 4)
-                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
+                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
                 else
-                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
+                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
             } else {
                 k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, evc, vec);
             }
@@ -1362,9 +1362,9 @@ struct Engine {
             if (use_bins && MAXR <= kBinRows) {
                 const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
                 if (cfg.rows == 4)
-                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
                 else
-                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, kBinSmem, st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             } else {
                 k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             }

@@ -74,8 +74,9 @@ constexpr int kBinPerThread = 4;                            // packets per threa
 constexpr int kBinTile = kBinThreads * kBinPerThread;       // packets per tile
 constexpr int kBinRows = 4;                                 // rows handled by the binned path
 constexpr int kBinEntries = kBinTile * kBinRows;
-constexpr int kMaxRegions = 1024;
-constexpr int kBinSmem = kMaxRegions * 16 + kBinEntries * 6;  // k_scan_bin dynamic shared memory
+constexpr int kMaxRegions = 4096;
+// k_scan_bin dynamic shared memory for `nregions` regions (2 blocks per SM up to kMaxRegions)
+constexpr int bin_smem(uint32_t nregions) { return static_cast<int>(nregions) * 16 + kBinEntries * 6; }
 
 // Epoch-stamp mode of the linear table (epoch.cuh): marks write the current
 // epoch instead of 0 and keep per-row stamp histograms.
@@ -140,15 +141,15 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                                                          BinCfg b, EpochCfg ep, W* __restrict__ lin,
                                                          uint32_t* __restrict__ stamp, uint32_t* __restrict__ ev,
                                                          uint32_t ev_cap, uint32_t* __restrict__ ev_count, int vec) {
-    // dynamic shared memory (kBinSmem bytes):
-    //   win[kMaxRegions] (uint2) | cnt | lbase | off[kBinEntries] | reg[kBinEntries] (u16)
+    // dynamic shared memory (bin_smem(nregions) bytes):
+    //   win[nregions] (uint2) | cnt[nregions] | lbase[nregions] | off[kBinEntries] | reg[kBinEntries] (u16)
     // win: per region {bin slot of staging entry idx = x + idx (mod 2^32; nregions * cap < 2^32),
     //                  first staging index that no longer fits the region's bin}
     extern __shared__ __align__(16) uint8_t s_bin_raw[];
     uint2* s_win = reinterpret_cast<uint2*>(s_bin_raw);
-    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_win + kMaxRegions);
-    uint32_t* s_lbase = s_cnt + kMaxRegions;
-    uint32_t* s_off = s_lbase + kMaxRegions;
+    uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_win + b.nregions);
+    uint32_t* s_lbase = s_cnt + b.nregions;
+    uint32_t* s_off = s_lbase + b.nregions;
     uint16_t* s_reg = reinterpret_cast<uint16_t*>(s_off + kBinEntries);
     __shared__ uint32_t s_warp[kBinThreads / 32];
 
@@ -550,24 +551,27 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
 __global__ void __launch_bounds__(1024) k_split_prefix(const uint32_t* __restrict__ count, uint32_t nregions,
                                                        uint32_t cap, uint32_t* __restrict__ prefix) {
     __shared__ uint32_t s_w[32];
-    const uint32_t r = threadIdx.x;  // nregions <= kMaxRegions = 1024
-    const uint32_t n = r < nregions ? min(count[r], cap) : 0u;
-    const uint32_t tiles = (n + kSplitTile - 1) / kSplitTile;
-    uint32_t incl = tiles;
+    const uint32_t per = (nregions + 1023) / 1024;  // regions per thread (nregions <= kMaxRegions)
+    const uint32_t r0 = threadIdx.x * per;
+    uint32_t mine = 0;
+    for (uint32_t r = r0; r < min(r0 + per, nregions); ++r) mine += (min(count[r], cap) + kSplitTile - 1) / kSplitTile;
+    uint32_t incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if ((r & 31) >= static_cast<uint32_t>(o)) incl += t;
+        if ((threadIdx.x & 31) >= static_cast<uint32_t>(o)) incl += t;
     }
-    if ((r & 31) == 31) s_w[r >> 5] = incl;
+    if ((threadIdx.x & 31) == 31) s_w[threadIdx.x >> 5] = incl;
     __syncthreads();
-    uint32_t base = 0;
-    for (uint32_t j = 0; j < (r >> 5); ++j) base += s_w[j];
-    if (r < nregions) {
-        prefix[r] = base + incl - tiles;
+    uint32_t run = incl - mine;
+    for (uint32_t j = 0; j < (threadIdx.x >> 5); ++j) run += s_w[j];
+    for (uint32_t r = r0; r < min(r0 + per, nregions); ++r) {
+        const uint32_t n = min(count[r], cap);
+        prefix[r] = run;
         prefix[nregions + 1 + r] = n;
+        run += (n + kSplitTile - 1) / kSplitTile;
     }
-    if (r == nregions - 1) prefix[nregions] = base + incl;
+    if (threadIdx.x == 1023) prefix[nregions] = run;
 }
 
 // mode 0: apply marks (slices without marks are skipped); 1: apply + age;

@@ -93,6 +93,13 @@ def test_c2_fullsize_bit_exact_vs_reference(gpu):
     print("c2 stats:", st)
 
 
+def test_c2_fullsize_sorted_ordering_bit_exact(gpu, monkeypatch):
+    """The same slices through the sorted, host-synchronised ordering phase
+    (SRLA_ORDER=legacy), the fallback of the device-count one."""
+    monkeypatch.setenv("SRLA_ORDER", "legacy")
+    run_fullsize("c2")
+
+
 def test_c2_fullsize_compact_handoff_bit_exact(gpu):
     """The bench's report hand-off (srla_end_slice_compact: hosts + weights +
     the window's Eq. 9 table) reconstructs the same entries."""

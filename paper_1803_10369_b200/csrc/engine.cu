@@ -722,11 +722,15 @@ struct Engine {
         // device-count ordering and a full-GPU early split (4-64 MB swept,
         // profiles/r02/ab_region_waves.txt)
         uint64_t region_bytes = 8ull << 20;
-        if (const char* rm = std::getenv("SRLA_REGION_MB")) region_bytes = std::strtoull(rm, nullptr, 10) << 20;
+        const char* rm = std::getenv("SRLA_REGION_MB");
+        if (rm) region_bytes = std::strtoull(rm, nullptr, 10) << 20;
         while (lin_bytes(1ull << (shift + 1)) <= region_bytes) ++shift;
         if (forced)
             while (shift > 4 && (total_words >> shift) < 8) --shift;  // ~8 regions even for tiny tables
-        while (((total_words + (1ull << shift) - 1) >> shift) > kMaxRegions) ++shift;
+        // at most 1024 regions by default (more costs K1 coalescing: C3 with 4096 regions
+        // 4.9 ms vs 2.6 ms with 1024, profiles/r02/ab_region_waves.txt); kMaxRegions if asked for
+        const uint64_t max_regions = rm ? kMaxRegions : 1024;
+        while (((total_words + (1ull << shift) - 1) >> shift) > max_regions) ++shift;
         // fine slices (u16 offsets): 32 KB, or larger so one region splits into <= 4096
         uint32_t fs = 0;
         uint64_t fine_bytes = 32ull << 10;  // 32 KB: two buffers per block

@@ -149,6 +149,195 @@ __global__ void __launch_bounds__(256) k_slice_apply_nib(uint8_t* __restrict__ l
     if (tid == 0) bulk_wait_all();
 }
 
+// End-of-slice split + apply in ONE persistent kernel (nibble tables): the
+// split (coarse region bins -> fine-slice bins, shared-memory bound) and the
+// apply (fine slices streamed through shared memory, HBM bound) overlap
+// instead of running back to back. Work items are claimed in order from two
+// global counters: every split tile first (region-major), then every fine
+// slice (region-major). A fine slice of region r is applied once all of r's
+// split tiles are done (work->done[r], released with a fence after each
+// tile). Waiting is deadlock-free: when a block claims a slice, every split
+// tile has already been claimed by a running block. Shared memory holds the
+// split's stages in the first phase and the apply's stages in the second.
+struct FusedWork {
+    unsigned int next_tile;
+    unsigned int next_slice;
+    unsigned int done[1];  // nregions entries (allocated with the struct)
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kSplitThreads, 2) k_split_apply_nib(
+    const uint32_t* __restrict__ coarse, uint32_t coarse_cap, const uint32_t* __restrict__ tile_prefix,
+    const uint32_t* __restrict__ coarse_n, uint32_t nregions, uint32_t region_shift, FineCfg f,
+    uint8_t* __restrict__ lin, uint64_t row_words, int mode, uint32_t k, uint32_t expired,
+    unsigned long long* __restrict__ counts, FusedWork* __restrict__ work) {
+    extern __shared__ __align__(128) uint8_t s_raw[];
+    __shared__ uint32_t s_warp[kSplitThreads / 32];
+    __shared__ uint32_t s_region[2], s_n[2], s_item[2];
+    __shared__ __align__(8) uint64_t s_bar[4];
+    __shared__ unsigned long long s_part[2][kSplitThreads / 32];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t T = tile_prefix[nregions];
+    if (tid == 0)
+        for (int j = 0; j < 4; ++j) mbar_init(&s_bar[j], 1);
+    __syncthreads();
+
+    // ---------------- phase A: split tiles
+    {
+        uint32_t* s_stage = reinterpret_cast<uint32_t*>(s_raw);
+        uint32_t* s_cnt = s_stage + 2 * kSplitTile;
+        uint32_t* s_lbase = s_cnt + f.per_region;
+        uint2* s_win = reinterpret_cast<uint2*>(s_lbase + f.per_region);
+        auto issue = [&](uint32_t t, uint32_t b) {  // thread 0 (k_split's)
+            uint32_t lo = 0, hi = nregions;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) / 2;
+                if (tile_prefix[mid] <= t) lo = mid;
+                else hi = mid;
+            }
+            const uint32_t begin = (t - tile_prefix[lo]) * kSplitTile;
+            const uint32_t n = min(coarse_n[lo] - begin, static_cast<uint32_t>(kSplitTile));
+            s_region[b] = lo;
+            s_n[b] = n;
+            const uint32_t bytes = (n * 4u + 15u) & ~15u;
+            mbar_expect_tx(&s_bar[b], bytes);
+            bulk_load(s_stage + b * kSplitTile, coarse + static_cast<uint64_t>(lo) * coarse_cap + begin, bytes, &s_bar[b]);
+        };
+        if (tid == 0) {
+            const uint32_t t0 = atomicAdd(&work->next_tile, 1u);
+            s_item[0] = t0;
+            if (t0 < T) issue(t0, 0);
+        }
+        __syncthreads();
+        uint32_t t = s_item[0];
+        for (uint32_t it = 0; t < T; ++it) {
+            const uint32_t sb = it & 1u;
+            if (tid == 0) {  // claim and load the next tile while this one is sorted
+                const uint32_t t2 = atomicAdd(&work->next_tile, 1u);
+                s_item[sb ^ 1u] = t2;
+                if (t2 < T) issue(t2, sb ^ 1u);
+            }
+            for (uint32_t i = tid; i < f.per_region; i += kSplitThreads) s_cnt[i] = 0;
+            mbar_wait(&s_bar[sb], (it >> 1) & 1u);
+            __syncthreads();
+            const uint32_t r = s_region[sb];
+            split_tile<uint8_t>(s_stage + sb * kSplitTile, r, s_n[sb], s_cnt, s_lbase, s_win, s_warp, region_shift, f,
+                                EpochCfg{0u, 0u, nullptr, 0ull}, lin);
+            if (tid == 0) {  // this tile's fine-bin writes (and any in-place marks) before the count
+                __threadfence();
+                atomicAdd(&work->done[r], 1u);
+            }
+            t = s_item[sb ^ 1u];
+        }
+    }
+    __syncthreads();
+
+    // ---------------- phase B: apply fine slices (k_slice_apply_nib's stages)
+    const uint32_t slice_bytes = (1u << f.shift) >> 1;
+    const uint32_t stage = slice_bytes + f.cap * 2u;  // slice | marks (f.cap is a multiple of 8)
+    const uint32_t k4 = k * 0x01010101u, e8 = expired * kNibOne;
+    uint64_t* bar = s_bar + 2;
+    auto gaddr = [&](uint32_t fb) { return lin + ((static_cast<uint64_t>(fb) << f.shift) >> 1); };
+    auto issue = [&](uint32_t fb, uint32_t b) {  // thread 0: wait for fb's region, then load slice + marks
+        const uint32_t r = fb / f.per_region;
+        const uint32_t need = r < nregions ? tile_prefix[r + 1] - tile_prefix[r] : 0u;
+        while (ld_acquire_gpu(&work->done[r < nregions ? r : 0]) < need) __nanosleep(256);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy bin writes -> TMA reads
+        const uint32_t n = min(ld_acquire_gpu(f.count + fb), f.cap);
+        const uint32_t mb = (n * 2u + 15u) & ~15u;
+        s_n[b] = n;
+        mbar_expect_tx(&bar[b], slice_bytes + mb);
+        bulk_load(s_raw + b * stage, gaddr(fb), slice_bytes, &bar[b]);
+        if (mb) bulk_load(s_raw + b * stage + slice_bytes, f.bins + static_cast<uint64_t>(fb) * f.cap, mb, &bar[b]);
+    };
+    if (tid == 0) {
+        const uint32_t c0 = atomicAdd(&work->next_slice, 1u);
+        s_item[0] = c0;
+        if (c0 < f.nfine) issue(c0, 0);
+    }
+    __syncthreads();
+    uint32_t cur = s_item[0];
+    for (uint32_t i = 0; cur < f.nfine; ++i) {
+        const uint32_t b = i & 1u;
+        if (tid == 0) {
+            const uint32_t nxt = atomicAdd(&work->next_slice, 1u);
+            s_item[b ^ 1u] = nxt;
+            if (nxt < f.nfine) {
+                bulk_wait_read_all();  // the other buffer's store (slice i-1) has left shared memory
+                issue(nxt, b ^ 1u);
+            }
+        }
+        mbar_wait(&bar[b], (i >> 1) & 1u);
+        if (tid == 0) atomicAdd(f.streamed, static_cast<unsigned long long>(slice_bytes));
+        uint8_t* sbuf = s_raw + b * stage;
+        unsigned int* s32 = reinterpret_cast<unsigned int*>(sbuf);
+        __syncthreads();  // s_n[b] (written by thread 0 before the barrier's arrival)
+        const uint32_t n = s_n[b];
+        const uint16_t* e = reinterpret_cast<const uint16_t*>(sbuf + slice_bytes);
+        const uint4* ev = reinterpret_cast<const uint4*>(e);
+        auto mark = [&](uint32_t o) { atomicAnd(s32 + (o >> 3), ~(0xFu << (4u * (o & 7u)))); };
+        for (uint32_t q = tid; q < n / 8; q += blockDim.x) {
+            const uint4 x = ev[q];
+            mark(x.x & 0xFFFF); mark(x.x >> 16);
+            mark(x.y & 0xFFFF); mark(x.y >> 16);
+            mark(x.z & 0xFFFF); mark(x.z >> 16);
+            mark(x.w & 0xFFFF); mark(x.w >> 16);
+        }
+        for (uint32_t q = (n / 8) * 8 + tid; q < n; q += blockDim.x) mark(e[q]);
+        __syncthreads();
+        const uint64_t w0 = static_cast<uint64_t>(cur) << f.shift;
+        const uint64_t row_a = w0 / row_words;
+        const uint64_t split = (row_a + 1) * row_words;  // first word of the next row
+        unsigned long long acc_a = 0, acc_b = 0;
+        uint4* sv = reinterpret_cast<uint4*>(sbuf);
+        const uint32_t nv = slice_bytes / 16;
+        for (uint32_t q = tid; q < nv; q += blockDim.x) {
+            uint4 x = sv[q];
+            if (mode == 2) {
+                const uint32_t c = nib_count_lt(x.x, k4) + nib_count_lt(x.y, k4) + nib_count_lt(x.z, k4) +
+                                   nib_count_lt(x.w, k4);
+                if (w0 + static_cast<uint64_t>(q) * 32 < split) acc_a += c;  // 32 recorders per vector
+                else acc_b += c;
+            }
+            x.x = nib_age(x.x, e8);
+            x.y = nib_age(x.y, e8);
+            x.z = nib_age(x.z, e8);
+            x.w = nib_age(x.w, e8);
+            sv[q] = x;
+        }
+        if (mode == 2) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                acc_a += __shfl_xor_sync(0xFFFFFFFFu, acc_a, o);
+                acc_b += __shfl_xor_sync(0xFFFFFFFFu, acc_b, o);
+            }
+            if ((tid & 31) == 0) {
+                s_part[0][tid >> 5] = acc_a;
+                s_part[1][tid >> 5] = acc_b;
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (mode == 2 && tid == 0) {
+            unsigned long long sa = 0, sb2 = 0;
+            for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+                sa += s_part[0][w];
+                sb2 += s_part[1][w];
+            }
+            if (sa) atomicAdd(counts + row_a, sa);
+            if (sb2) atomicAdd(counts + row_a + 1, sb2);
+        }
+        if (tid == 0) bulk_store(gaddr(cur), sbuf, slice_bytes);
+        cur = s_item[b ^ 1u];
+    }
+    if (tid == 0) bulk_wait_all();
+}
+
 // union_linear_weight (sea.hpp:232-243) on a nibble table: slot j counts
 // iff max over rows of recorder j < kthr. A cell of g' recorders is g'/2
 // bytes, so a half-warp takes a candidate (two vectors per row per lane in

@@ -406,6 +406,93 @@ constexpr int kSplitThreads = 512;
 constexpr int kSplitPerThread = 16;
 constexpr int kSplitTile = kSplitThreads * kSplitPerThread;  // 8192 entries
 
+// One k_split tile: the n entries of region r staged at s_sorted (loaded
+// there; sorted in place) -> fine-slice bins. s_cnt must be zero on entry.
+// Ends with a block barrier.
+template <typename W>
+__device__ __forceinline__ void split_tile(uint32_t* s_sorted, uint32_t r, uint32_t n, uint32_t* s_cnt,
+                                           uint32_t* s_lbase, uint2* s_win, uint32_t* s_warp,
+                                           uint32_t region_shift, const FineCfg& f, const EpochCfg& ep,
+                                           W* __restrict__ lin) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t fmask = (1u << f.shift) - 1u;
+    const uint32_t per_thread = (f.per_region + kSplitThreads - 1) / kSplitThreads;
+    uint32_t off[kSplitPerThread];
+    const uint32_t e0 = tid * kSplitPerThread;
+    const uint4* v = reinterpret_cast<const uint4*>(s_sorted + e0);
+#pragma unroll
+    for (int q = 0; q < kSplitPerThread / 4; ++q) {
+        const uint4 x = v[q];
+        off[4 * q] = e0 + 4 * q < n ? x.x : 0xFFFFFFFFu;
+        off[4 * q + 1] = e0 + 4 * q + 1 < n ? x.y : 0xFFFFFFFFu;
+        off[4 * q + 2] = e0 + 4 * q + 2 < n ? x.z : 0xFFFFFFFFu;
+        off[4 * q + 3] = e0 + 4 * q + 3 < n ? x.w : 0xFFFFFFFFu;
+    }
+    uint32_t rank[kSplitPerThread];
+#pragma unroll
+    for (int k = 0; k < kSplitPerThread; ++k)
+        if (off[k] != 0xFFFFFFFFu) rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
+    __syncthreads();
+    uint32_t mine = 0;
+    const uint32_t b0 = tid * per_thread;
+    for (uint32_t b = b0; b < min(b0 + per_thread, f.per_region); ++b) mine += s_cnt[b];
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint32_t run = incl - mine;
+    for (uint32_t w2 = 0; w2 < warp; ++w2) run += s_warp[w2];
+    const uint32_t fine0 = r * f.per_region;
+    for (uint32_t b = b0; b < min(b0 + per_thread, f.per_region); ++b) {
+        const uint32_t cn = s_cnt[b];
+        s_lbase[b] = run;
+        if (cn) {
+            const uint32_t g = atomicAdd(f.count + fine0 + b, cn);
+            const uint32_t fit = g >= f.cap ? 0u : min(cn, f.cap - g);
+            s_win[b] = make_uint2((fine0 + b) * f.cap + g - run, run + fit);
+        }
+        run += cn;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSplitPerThread; ++k)
+        if (off[k] != 0xFFFFFFFFu) {
+            const uint32_t b = off[k] >> f.shift;
+            s_sorted[s_lbase[b] + rank[k]] = (b << 16) | (off[k] & fmask);
+        }
+    __syncthreads();
+    bool ovf = false;
+    for (uint32_t i = tid; i < n; i += kSplitThreads) {
+        const uint32_t v = s_sorted[i];
+        const uint2 wv = s_win[v >> 16];
+        if (i < wv.y) f.bins[wv.x + i] = static_cast<uint16_t>(v);
+        else ovf = true;
+    }
+    if (__syncthreads_or(ovf)) {  // a fine bin is full: mark in place (marks commute)
+        for (uint32_t i = tid; i < n; i += kSplitThreads) {
+            const uint32_t v = s_sorted[i];
+            const uint32_t b = v >> 16;
+            if (i < s_win[b].y) continue;
+            if (ep.on)
+                mark_epoch_global(reinterpret_cast<uint8_t*>(lin),
+                                  (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift) +
+                                      (v & 0xFFFFu),
+                                  ep.row_words, ep.cur, ep.hist);
+            else if (f.nib)
+                mark_nibble_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << region_shift) +
+                                                                        (static_cast<uint64_t>(b) << f.shift) + (v & 0xFFFFu));
+            else
+                mark_word<W>(lin + (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift),
+                             v & 0xFFFFu);
+        }
+    }
+    __syncthreads();
+}
+
 // Re-bin coarse region bins by fine slice. One tile = 8192 consecutive entries
 // of one region: shared-memory counting sort by slice (ranks from shared
 // atomics), one global reservation per slice per tile, coalesced u16 writes.
@@ -430,10 +517,8 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
     __shared__ uint32_t s_warp[kSplitThreads / 32];
     __shared__ uint32_t s_region[2], s_n[2];
     __shared__ __align__(8) uint64_t s_bar[2];
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t tid = threadIdx.x;
     const uint32_t total_tiles = tile_prefix[nregions];
-    const uint32_t fmask = (1u << f.shift) - 1u;
-    const uint32_t per_thread = (f.per_region + kSplitThreads - 1) / kSplitThreads;
     // thread 0: locate tile t (region r with tile_prefix[r] <= t < tile_prefix[r+1]) and load it
     auto issue = [&](uint32_t t, uint32_t b) {
         uint32_t lo = 0, hi = nregions;
@@ -466,81 +551,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
         __syncthreads();
         const uint32_t r = s_region[sb];
         const uint32_t n = s_n[sb];
-        uint32_t* s_sorted = s_stage + sb * kSplitTile;  // (slice << 16) | offset within slice
-        uint32_t off[kSplitPerThread];
-        const uint32_t e0 = tid * kSplitPerThread;
-        const uint4* v = reinterpret_cast<const uint4*>(s_stage + sb * kSplitTile + e0);
-#pragma unroll
-        for (int q = 0; q < kSplitPerThread / 4; ++q) {
-            const uint4 x = v[q];
-            off[4 * q] = e0 + 4 * q < n ? x.x : 0xFFFFFFFFu;
-            off[4 * q + 1] = e0 + 4 * q + 1 < n ? x.y : 0xFFFFFFFFu;
-            off[4 * q + 2] = e0 + 4 * q + 2 < n ? x.z : 0xFFFFFFFFu;
-            off[4 * q + 3] = e0 + 4 * q + 3 < n ? x.w : 0xFFFFFFFFu;
-        }
-        uint32_t rank[kSplitPerThread];
-#pragma unroll
-        for (int k = 0; k < kSplitPerThread; ++k)
-            if (off[k] != 0xFFFFFFFFu) rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
-        __syncthreads();
-        uint32_t mine = 0;
-        const uint32_t b0 = tid * per_thread;
-        for (uint32_t b = b0; b < min(b0 + per_thread, f.per_region); ++b) mine += s_cnt[b];
-        uint32_t incl = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= static_cast<uint32_t>(o)) incl += v;
-        }
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        uint32_t run = incl - mine;
-        for (uint32_t w2 = 0; w2 < warp; ++w2) run += s_warp[w2];
-        const uint32_t fine0 = r * f.per_region;
-        for (uint32_t b = b0; b < min(b0 + per_thread, f.per_region); ++b) {
-            const uint32_t cn = s_cnt[b];
-            s_lbase[b] = run;
-            if (cn) {
-                const uint32_t g = atomicAdd(f.count + fine0 + b, cn);
-                const uint32_t fit = g >= f.cap ? 0u : min(cn, f.cap - g);
-                s_win[b] = make_uint2((fine0 + b) * f.cap + g - run, run + fit);
-            }
-            run += cn;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kSplitPerThread; ++k)
-            if (off[k] != 0xFFFFFFFFu) {
-                const uint32_t b = off[k] >> f.shift;
-                s_sorted[s_lbase[b] + rank[k]] = (b << 16) | (off[k] & fmask);
-            }
-        __syncthreads();
-        bool ovf = false;
-        for (uint32_t i = tid; i < n; i += kSplitThreads) {
-            const uint32_t v = s_sorted[i];
-            const uint2 wv = s_win[v >> 16];
-            if (i < wv.y) f.bins[wv.x + i] = static_cast<uint16_t>(v);
-            else ovf = true;
-        }
-        if (__syncthreads_or(ovf)) {  // a fine bin is full: mark in place (marks commute)
-            for (uint32_t i = tid; i < n; i += kSplitThreads) {
-                const uint32_t v = s_sorted[i];
-                const uint32_t b = v >> 16;
-                if (i < s_win[b].y) continue;
-                if (ep.on)
-                    mark_epoch_global(reinterpret_cast<uint8_t*>(lin),
-                                      (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift) +
-                                          (v & 0xFFFFu),
-                                      ep.row_words, ep.cur, ep.hist);
-                else if (f.nib)
-                    mark_nibble_global(reinterpret_cast<uint8_t*>(lin), (static_cast<uint64_t>(r) << region_shift) +
-                                                                            (static_cast<uint64_t>(b) << f.shift) + (v & 0xFFFFu));
-                else
-                    mark_word<W>(lin + (static_cast<uint64_t>(r) << region_shift) + (static_cast<uint64_t>(b) << f.shift),
-                                 v & 0xFFFFu);
-            }
-        }
-        __syncthreads();
+        split_tile<W>(s_stage + sb * kSplitTile, r, n, s_cnt, s_lbase, s_win, s_warp, region_shift, f, ep, lin);
     }
 }
 

@@ -799,7 +799,7 @@ struct Engine {
         if (nib) {
             if (nib_apply_smem() > 200 * 1024) return false;  // two stages must fit in shared memory
             raise_smem_cap(k_slice_apply_nib, static_cast<int>(nib_apply_smem()));
-            raise_smem_cap(k_split_apply_nib, std::max<size_t>(split_smem, nib_apply_smem()));
+            raise_smem_cap(k_split_apply_nib, 2 * fused_buf());
         }
         with_w([&](auto w) {
             using W = decltype(w);
@@ -952,18 +952,18 @@ struct Engine {
     // streamed apply (HBM bound) region by region.
     bool fused = [] { const char* v = std::getenv("SRLA_FUSED"); return !(v && v[0] == '0'); }();
     DevBuf<unsigned int> fused_work;
-    bool fused_ok() const { return fused && nib && bulk_ok && bulk_end == fcfg.nfine; }
+    bool fused_ok() const { return fused && nib && bulk_ok && bulk_end == fcfg.nfine && 2 * fused_buf() <= 200 * 1024; }
     void fused_flush(int mode) {
         const uint32_t R = bcfg.nregions;
         k_split_prefix<<<1, 1024, 0, st>>>(bin_count.p, R, bcfg.cap, tile_prefix.p);
-        fused_work.ensure(2 + R);
-        CK(cudaMemsetAsync(fused_work.p, 0, (2 + R) * sizeof(unsigned int), st));
+        fused_work.ensure(1 + R);
+        CK(cudaMemsetAsync(fused_work.p, 0, (1 + R) * sizeof(unsigned int), st));
         open_k1_gate();
         const cudaEvent_t t_apply = timer_start();
-        k_split_apply_nib<<<sms * 2, kSplitThreads, fused_smem(), st>>>(
+        k_split_apply_nib<<<sms * 2, kSplitThreads, 2 * fused_buf(), st>>>(
             bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg,
             static_cast<uint8_t*>(d_lin), lin_words, mode, cfg.window, dc.expired, d_counts.p,
-            reinterpret_cast<FusedWork*>(fused_work.p));
+            reinterpret_cast<FusedWork*>(fused_work.p), static_cast<uint32_t>(fused_buf()));
         check_launch();
         launched(2);
         timer_stop(t_apply, kTimeApply);
@@ -976,7 +976,13 @@ struct Engine {
         pending_entries = 0;
         fine_pending = 0;
     }
-    size_t fused_smem() const { return std::max<size_t>(split_smem, nib_apply_smem()); }
+    // one of the fused kernel's two buffers: a slice stage (slice + marks) or a
+    // split tile (entries + per-slice tables)
+    size_t fused_buf() const {
+        const size_t stage = lin_bytes(1ull << fcfg.shift) + size_t(fcfg.cap) * 2;
+        const size_t tile = size_t(kSplitTile) * 4 + size_t(fcfg.per_region) * 16;
+        return (std::max(stage, tile) + 127) & ~size_t(127);
+    }
 
     void flush_linear(int mode = 0) {
         if (!use_bins) return;

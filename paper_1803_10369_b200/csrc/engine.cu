@@ -799,7 +799,6 @@ struct Engine {
         if (nib) {
             if (nib_apply_smem() > 200 * 1024) return false;  // two stages must fit in shared memory
             raise_smem_cap(k_slice_apply_nib, static_cast<int>(nib_apply_smem()));
-            raise_smem_cap(k_split_apply_nib, 2 * fused_buf());
         }
         with_w([&](auto w) {
             using W = decltype(w);
@@ -947,50 +946,9 @@ struct Engine {
         split_in_flight = false;
     }
 
-    // End-of-slice split + apply of a nibble table as one persistent kernel
-    // (k_split_apply_nib): the split (shared-memory bound) overlaps the
-    // streamed apply (HBM bound) region by region.
-    bool fused = [] { const char* v = std::getenv("SRLA_FUSED"); return !(v && v[0] == '0'); }();
-    DevBuf<unsigned int> fused_work;
-    bool fused_ok() const { return fused && nib && bulk_ok && bulk_end == fcfg.nfine && 2 * fused_buf() <= 200 * 1024; }
-    void fused_flush(int mode) {
-        const uint32_t R = bcfg.nregions;
-        k_split_prefix<<<1, 1024, 0, st>>>(bin_count.p, R, bcfg.cap, tile_prefix.p);
-        fused_work.ensure(1 + R);
-        CK(cudaMemsetAsync(fused_work.p, 0, (1 + R) * sizeof(unsigned int), st));
-        open_k1_gate();
-        const cudaEvent_t t_apply = timer_start();
-        k_split_apply_nib<<<sms * 2, kSplitThreads, 2 * fused_buf(), st>>>(
-            bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg,
-            static_cast<uint8_t*>(d_lin), lin_words, mode, cfg.window, dc.expired, d_counts.p,
-            reinterpret_cast<FusedWork*>(fused_work.p), static_cast<uint32_t>(fused_buf()));
-        check_launch();
-        launched(2);
-        timer_stop(t_apply, kTimeApply);
-        timing.apply_kernel_launches += 1;
-        timing.split_entries += pending_entries;
-        timing.apply_entries += pending_entries + fine_pending;
-        CK(cudaMemsetAsync(bin_count.p, 0, R * sizeof(uint32_t), st));
-        CK(cudaMemcpyAsync(pin_streamed.p, d_streamed.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemsetAsync(fine_count.p, 0, fcfg.nfine * sizeof(uint32_t), st));
-        pending_entries = 0;
-        fine_pending = 0;
-    }
-    // one of the fused kernel's two buffers: a slice stage (slice + marks) or a
-    // split tile (entries + per-slice tables)
-    size_t fused_buf() const {
-        const size_t stage = lin_bytes(1ull << fcfg.shift) + size_t(fcfg.cap) * 2;
-        const size_t tile = size_t(kSplitTile) * 4 + size_t(fcfg.per_region) * 16;
-        return (std::max(stage, tile) + 127) & ~size_t(127);
-    }
-
     void flush_linear(int mode = 0) {
         if (!use_bins) return;
         join_maint_lin();
-        if (mode != 0 && fused_ok() && !split_in_flight) {
-            fused_flush(mode);
-            return;
-        }
         split_now(st);
         join_split();
         if (fine_pending == 0 && mode == 0) return;
@@ -1302,7 +1260,7 @@ struct Engine {
             timing.scan_kernel_launches += 1;
             timing.scan_kernel_records += n;
             // split the region bins now, concurrent with the ordering phase below
-            if (use_bins && early_split && !overlap_on && !fused_ok()) split_now(ssplit);
+            if (use_bins && early_split && !overlap_on) split_now(ssplit);
             const auto w_order = std::chrono::steady_clock::now();
             join_maint();  // rough aging, indicators and the candidate hash of the last slide
             const OrderBufs ob = order_bufs(collect_pushed);
@@ -1431,7 +1389,7 @@ struct Engine {
         }
         stats.sampled_events += n_ev;
         // split the region bins now, concurrent with the ordering phase below
-        if (use_bins && early_split && !overlap_on && !fused_ok()) split_now(ssplit);
+        if (use_bins && early_split && !overlap_on) split_now(ssplit);
         trace("scan: K1");
         if (!n_ev) return;
         const auto w_order = std::chrono::steady_clock::now();

@@ -149,224 +149,6 @@ __global__ void __launch_bounds__(256) k_slice_apply_nib(uint8_t* __restrict__ l
     if (tid == 0) bulk_wait_all();
 }
 
-// End-of-slice split + apply in ONE persistent kernel (nibble tables): the
-// split (coarse region bins -> fine-slice bins, shared-memory bound) and the
-// apply (fine slices streamed through shared memory, HBM bound) run at the
-// same time on every SM. Work items are claimed in order from one counter
-// over an interleaved sequence — split tiles of region 0, of region 1, the
-// fine slices of region 0, tiles of region 2, slices of region 1, ... — so
-// slices of region r are applied while later regions are still being split.
-// A slice of region r is applied once all of r's tiles are done (done[r],
-// released with a fence after each tile). Deadlock-free: all tiles of r are
-// claimed before any slice of r, and a block only ever waits on a slice it is
-// about to process, so every wait chain descends to lower regions. Each of
-// the two shared-memory buffers holds either a tile (its entries, then the
-// split's per-slice tables) or a slice stage (the slice, then its marks); the
-// next item loads into the other buffer while the current one is processed.
-struct FusedWork {
-    unsigned int next;     // items claimed
-    unsigned int done[1];  // nregions entries follow: split tiles finished per region
-};
-
-__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
-    unsigned int v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__global__ void __launch_bounds__(kSplitThreads, 2) k_split_apply_nib(
-    const uint32_t* __restrict__ coarse, uint32_t coarse_cap, const uint32_t* __restrict__ tile_prefix,
-    const uint32_t* __restrict__ coarse_n, uint32_t nregions, uint32_t region_shift, FineCfg f,
-    uint8_t* __restrict__ lin, uint64_t row_words, int mode, uint32_t k, uint32_t expired,
-    unsigned long long* __restrict__ counts, FusedWork* __restrict__ work, uint32_t buf_bytes) {
-    extern __shared__ __align__(128) uint8_t s_raw[];
-    __shared__ uint32_t s_warp[kSplitThreads / 32];
-    __shared__ uint32_t s_type[2], s_id[2], s_n[2], s_ready[2];
-    __shared__ __align__(8) uint64_t s_bar[2];
-    __shared__ unsigned long long s_part[2][kSplitThreads / 32];
-    const uint32_t tid = threadIdx.x;
-    const uint32_t T = tile_prefix[nregions];
-    const uint32_t P = f.per_region;
-    const uint32_t total = T + f.nfine;
-    const uint32_t slice_bytes = (1u << f.shift) >> 1;
-    const uint32_t k4 = k * 0x01010101u, e8 = expired * kNibOne;
-    auto gaddr = [&](uint32_t fb) { return lin + ((static_cast<uint64_t>(fb) << f.shift) >> 1); };
-    // slices in regions [0, r)
-    auto slices_below = [&](uint32_t r) { return min(r * P, f.nfine); };
-    // item i of the interleaved sequence -> (type 1 tile / 2 slice, id); type 0 = none.
-    // Group r: the tiles of region r, then the slices of region r - 1 (the last
-    // group also the slices of region R - 1); before(r) items precede group r.
-    auto locate = [&](uint32_t i, uint32_t& type, uint32_t& id) {
-        type = 0;
-        if (i >= total) return;
-        auto before = [&](uint32_t r) { return tile_prefix[r] + (r >= 1 ? slices_below(r - 1) : 0u); };
-        uint32_t lo = 0, hi = nregions;  // the last r with before(r) <= i
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) / 2;
-            if (before(mid) <= i) lo = mid;
-            else hi = mid;
-        }
-        const uint32_t off = i - before(lo), nt = tile_prefix[lo + 1] - tile_prefix[lo];
-        if (off < nt) {
-            type = 1;
-            id = tile_prefix[lo] + off;
-        } else {
-            type = 2;
-            id = (lo >= 1 ? slices_below(lo - 1) : 0u) + (off - nt);
-        }
-    };
-    // thread 0: the region of tile t
-    auto tile_region = [&](uint32_t t) {
-        uint32_t lo = 0, hi = nregions;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) / 2;
-            if (tile_prefix[mid] <= t) lo = mid;
-            else hi = mid;
-        }
-        return lo;
-    };
-    auto region_done = [&](uint32_t fb) {
-        const uint32_t r = fb / P;
-        return ld_acquire_gpu(&work->done[r]) >= tile_prefix[r + 1] - tile_prefix[r];
-    };
-    // thread 0: start loading item (type, id) into buffer b (slices only once their region is split)
-    auto load = [&](uint32_t b) {
-        uint8_t* buf = s_raw + b * buf_bytes;
-        s_ready[b] = 1;
-        if (s_type[b] == 1) {
-            const uint32_t t = s_id[b];
-            const uint32_t r = tile_region(t);
-            const uint32_t begin = (t - tile_prefix[r]) * kSplitTile;
-            const uint32_t n = min(coarse_n[r] - begin, static_cast<uint32_t>(kSplitTile));
-            s_n[b] = n;
-            const uint32_t bytes = (n * 4u + 15u) & ~15u;
-            mbar_expect_tx(&s_bar[b], bytes);
-            bulk_load(buf, coarse + static_cast<uint64_t>(r) * coarse_cap + begin, bytes, &s_bar[b]);
-        } else if (s_type[b] == 2) {
-            const uint32_t fb = s_id[b];
-            if (!region_done(fb)) {
-                s_ready[b] = 0;  // loaded when it is processed
-                return;
-            }
-            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy bin writes -> TMA reads
-            const uint32_t n = min(ld_acquire_gpu(f.count + fb), f.cap);
-            const uint32_t mb = (n * 2u + 15u) & ~15u;
-            s_n[b] = n;
-            mbar_expect_tx(&s_bar[b], slice_bytes + mb);
-            bulk_load(buf, gaddr(fb), slice_bytes, &s_bar[b]);
-            if (mb) bulk_load(buf + slice_bytes, f.bins + static_cast<uint64_t>(fb) * f.cap, mb, &s_bar[b]);
-        }
-    };
-    auto claim = [&](uint32_t b) {  // thread 0
-        uint32_t type, id = 0;
-        locate(atomicAdd(&work->next, 1u), type, id);
-        s_type[b] = type;
-        s_id[b] = id;
-    };
-    if (tid == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
-        claim(0);
-        load(0);
-    }
-    __syncthreads();
-    uint32_t phase[2] = {0u, 0u};
-    for (uint32_t b = 0; s_type[b] != 0; b ^= 1u) {
-        if (tid == 0) {
-            bulk_wait_read_all();  // the other buffer's last slice store has left shared memory
-            claim(b ^ 1u);
-            load(b ^ 1u);
-            if (!s_ready[b]) {  // a slice whose region was still being split when it was claimed
-                while (!region_done(s_id[b])) __nanosleep(256);
-                load(b);
-            }
-        }
-        __syncthreads();
-        mbar_wait(&s_bar[b], phase[b]);
-        phase[b] ^= 1u;
-        uint8_t* buf = s_raw + b * buf_bytes;
-        const uint32_t n = s_n[b];
-        if (s_type[b] == 1) {  // split tile: entries | cnt[P] | lbase[P] | win[P]
-            uint32_t* s_sorted = reinterpret_cast<uint32_t*>(buf);
-            uint32_t* s_cnt = s_sorted + kSplitTile;
-            uint32_t* s_lbase = s_cnt + P;
-            uint2* s_win = reinterpret_cast<uint2*>(s_lbase + P);
-            for (uint32_t i = tid; i < P; i += kSplitThreads) s_cnt[i] = 0;
-            __syncthreads();
-            const uint32_t r = tile_region(s_id[b]);
-            split_tile<uint8_t>(s_sorted, r, n, s_cnt, s_lbase, s_win, s_warp, region_shift, f,
-                                EpochCfg{0u, 0u, nullptr, 0ull}, lin);
-            if (tid == 0) {  // this tile's fine-bin writes (and in-place marks) before the count
-                __threadfence();
-                atomicAdd(&work->done[r], 1u);
-            }
-        } else {  // fine slice: marks, count, age, store
-            const uint32_t fb = s_id[b];
-            if (tid == 0) atomicAdd(f.streamed, static_cast<unsigned long long>(slice_bytes));
-            unsigned int* s32 = reinterpret_cast<unsigned int*>(buf);
-            const uint16_t* e = reinterpret_cast<const uint16_t*>(buf + slice_bytes);
-            const uint4* ev = reinterpret_cast<const uint4*>(e);
-            auto mark = [&](uint32_t o) { atomicAnd(s32 + (o >> 3), ~(0xFu << (4u * (o & 7u)))); };
-            for (uint32_t q = tid; q < n / 8; q += blockDim.x) {
-                const uint4 x = ev[q];
-                mark(x.x & 0xFFFF); mark(x.x >> 16);
-                mark(x.y & 0xFFFF); mark(x.y >> 16);
-                mark(x.z & 0xFFFF); mark(x.z >> 16);
-                mark(x.w & 0xFFFF); mark(x.w >> 16);
-            }
-            for (uint32_t q = (n / 8) * 8 + tid; q < n; q += blockDim.x) mark(e[q]);
-            __syncthreads();
-            const uint64_t w0 = static_cast<uint64_t>(fb) << f.shift;
-            const uint64_t row_a = w0 / row_words;
-            const uint64_t split = (row_a + 1) * row_words;  // first word of the next row
-            unsigned long long acc_a = 0, acc_b = 0;
-            uint4* sv = reinterpret_cast<uint4*>(buf);
-            const uint32_t nv = slice_bytes / 16;
-            for (uint32_t q = tid; q < nv; q += blockDim.x) {
-                uint4 x = sv[q];
-                if (mode == 2) {
-                    const uint32_t c = nib_count_lt(x.x, k4) + nib_count_lt(x.y, k4) + nib_count_lt(x.z, k4) +
-                                       nib_count_lt(x.w, k4);
-                    if (w0 + static_cast<uint64_t>(q) * 32 < split) acc_a += c;  // 32 recorders per vector
-                    else acc_b += c;
-                }
-                x.x = nib_age(x.x, e8);
-                x.y = nib_age(x.y, e8);
-                x.z = nib_age(x.z, e8);
-                x.w = nib_age(x.w, e8);
-                sv[q] = x;
-            }
-            if (mode == 2) {
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    acc_a += __shfl_xor_sync(0xFFFFFFFFu, acc_a, o);
-                    acc_b += __shfl_xor_sync(0xFFFFFFFFu, acc_b, o);
-                }
-                if ((tid & 31) == 0) {
-                    s_part[0][tid >> 5] = acc_a;
-                    s_part[1][tid >> 5] = acc_b;
-                }
-            }
-            fence_proxy_async_smem();
-            __syncthreads();
-            if (tid == 0) {
-                if (mode == 2) {
-                    unsigned long long sa = 0, sb2 = 0;
-                    for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
-                        sa += s_part[0][w];
-                        sb2 += s_part[1][w];
-                    }
-                    if (sa) atomicAdd(counts + row_a, sa);
-                    if (sb2) atomicAdd(counts + row_a + 1, sb2);
-                }
-                bulk_store(gaddr(fb), buf, slice_bytes);
-            }
-        }
-        __syncthreads();  // buffer b is free for the load after next; s_type/s_id of b^1 are set
-    }
-    if (tid == 0) bulk_wait_all();
-}
-
 // union_linear_weight (sea.hpp:232-243) on a nibble table: slot j counts
 // iff max over rows of recorder j < kthr. A cell of g' recorders is g'/2
 // bytes, so a half-warp takes a candidate (two vectors per row per lane in

@@ -40,12 +40,12 @@ __device__ __forceinline__ uint32_t nib_count_lt(uint32_t x, uint32_t k4) {
 // recorders share a byte); mode 0 apply / 1 apply + age / 2 apply + count
 // active (pre-age) + age; the slice is bulk-stored back.
 // Shared memory: 2 x (slice bytes + f.cap x 2 B).
-__global__ void __launch_bounds__(256) k_slice_apply_nib(uint8_t* __restrict__ lin, uint64_t row_words, FineCfg f,
+__global__ void __launch_bounds__(1024) k_slice_apply_nib(uint8_t* __restrict__ lin, uint64_t row_words, FineCfg f,
                                                          uint32_t f_end, int mode, uint32_t k, uint32_t expired,
                                                          unsigned long long* __restrict__ counts) {
     extern __shared__ __align__(128) uint8_t s_raw[];
     __shared__ __align__(8) uint64_t s_bar[2];
-    __shared__ unsigned long long s_part[2][8];
+    __shared__ unsigned long long s_part[2][32];
     __shared__ uint32_t s_n[2];
     const uint32_t tid = threadIdx.x;
     const uint32_t slice_bytes = (1u << f.shift) >> 1;

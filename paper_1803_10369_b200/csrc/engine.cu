@@ -2328,6 +2328,12 @@ srla_status guard(Fn&& fn) {
     }
 }
 
+// the engine's call mutex (a null engine is an argument error, not a crash)
+std::mutex& lock_of(srla_engine* e) {
+    if (!e || !e->impl) throw srla::Error(SRLA_E_INVALID, "null engine");
+    return e->mu;
+}
+
 srla::Engine& E(srla_engine* e, bool join = true) {
     if (!e || !e->impl) throw srla::Error(SRLA_E_INVALID, "null engine");
     CK(cudaSetDevice(e->impl->device));
@@ -2407,7 +2413,7 @@ namespace {
 srla_status scan_batch_impl(srla_engine* e, const srla_record* recs, uint64_t n, int on_device, cudaStream_t producer,
                             uint32_t* pushed, uint64_t cap, uint64_t* n_pushed) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         auto& x = E(e, /*join=*/false);  // joins a pending async end-of-slice after staging copies
         if (n && !recs) throw srla::Error(SRLA_E_INVALID, "null records");
         x.collect_pushed = pushed != nullptr || n_pushed != nullptr;
@@ -2435,7 +2441,7 @@ srla_status srla_scan_device(srla_engine* e, const srla_record* d_recs, uint64_t
 
 srla_status srla_candidates(srla_engine* e, uint32_t* out, uint64_t cap, uint64_t* n) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         auto& x = E(e);
         std::vector<uint32_t> v;
         x.candidates(v);
@@ -2448,7 +2454,7 @@ srla_status srla_candidates(srla_engine* e, uint32_t* out, uint64_t cap, uint64_
 
 srla_status srla_set_candidates(srla_engine* e, const uint32_t* hosts, uint64_t n) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         if (n && !hosts) throw srla::Error(SRLA_E_INVALID, "null hosts");
         E(e).set_candidates(hosts, n);
     });
@@ -2456,7 +2462,7 @@ srla_status srla_set_candidates(srla_engine* e, const uint32_t* hosts, uint64_t 
 
 srla_status srla_report(srla_engine* e, srla_entry* out, uint64_t cap, uint64_t* n_out, double* fill_product) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         auto& x = E(e);
         check_capacity(x.ncsip, out, cap, n_out);
         x.report(out, fill_product);
@@ -2465,7 +2471,7 @@ srla_status srla_report(srla_engine* e, srla_entry* out, uint64_t cap, uint64_t*
 
 srla_status srla_slide(srla_engine* e, uint64_t* n_retained) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         auto& x = E(e);
         x.slide();
         if (n_retained) *n_retained = x.ncsip;
@@ -2486,7 +2492,7 @@ srla_status srla_end_slice_compact(srla_engine* e, uint64_t slice_id, int want_r
                                    uint32_t* weights, uint64_t cap, uint64_t* n_out, double* est_lut,
                                    uint8_t* flags_lut, uint64_t* n_retained) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         auto& x = E(e);
         const bool due = want_report && slice_id + 1 >= x.cfg.window;
         if (n_out) *n_out = due ? x.ncsip : 0;
@@ -2502,14 +2508,14 @@ srla_status srla_end_slice_compact(srla_engine* e, uint64_t slice_id, int want_r
 srla_status srla_end_slice_async(srla_engine* e, uint64_t slice_id, int want_report, srla_entry* out,
                                  uint64_t cap) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         E(e).end_slice_async(slice_id, want_report != 0, out, cap);
     });
 }
 
 srla_status srla_end_slice_wait(srla_engine* e, uint64_t* n_out, uint64_t* n_retained) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         auto& x = E(e);
         if (!x.eos.pending) throw srla::Error(SRLA_E_INVALID, "no srla_end_slice_async pending");
         x.eos.pending = false;
@@ -2522,7 +2528,7 @@ srla_status srla_end_slice_wait(srla_engine* e, uint64_t* n_out, uint64_t* n_ret
 srla_status srla_union_weights(srla_engine* e, const uint32_t* hosts, uint64_t n, uint32_t* rough_w,
                                uint32_t* linear_w) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         if (n && !hosts) throw srla::Error(SRLA_E_INVALID, "null hosts");
         E(e).union_weights(hosts, n, rough_w, linear_w);
     });
@@ -2530,7 +2536,7 @@ srla_status srla_union_weights(srla_engine* e, const uint32_t* hosts, uint64_t n
 
 srla_status srla_union_view(srla_engine* e, uint32_t aip, uint16_t* indicator, uint32_t* rough, uint32_t* linear) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         if (!indicator || !rough) throw srla::Error(SRLA_E_INVALID, "null output");
         E(e).union_view(aip, indicator, rough, linear);
     });
@@ -2538,7 +2544,7 @@ srla_status srla_union_view(srla_engine* e, uint32_t aip, uint16_t* indicator, u
 
 srla_status srla_row_active(srla_engine* e, uint64_t* counts) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         if (!counts) throw srla::Error(SRLA_E_INVALID, "null output");
         E(e).row_active(counts);
     });
@@ -2563,14 +2569,14 @@ srla_status srla_row_bytes(const srla_engine* e, int kind, uint64_t* bytes) {
 
 srla_status srla_export_row(srla_engine* e, uint32_t row, int kind, void* buf, uint64_t bytes) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         E(e).export_row(row, kind, buf, bytes);
     });
 }
 
 srla_status srla_import_row(srla_engine* e, uint32_t row, int kind, const void* buf, uint64_t bytes) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         E(e).import_row(row, kind, buf, bytes);
     });
 }
@@ -2602,7 +2608,7 @@ srla_status srla_block_sums(const void* d_buf, uint64_t bytes, uint64_t* out, ui
 
 srla_status srla_export_range(srla_engine* e, uint32_t row, int kind, uint64_t offset, void* buf, uint64_t bytes) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         if (bytes && !buf) throw srla::Error(SRLA_E_INVALID, "null buffer");
         E(e).export_range(row, kind, offset, buf, bytes);
     });
@@ -2610,7 +2616,7 @@ srla_status srla_export_range(srla_engine* e, uint32_t row, int kind, uint64_t o
 
 srla_status srla_import_range(srla_engine* e, uint32_t row, int kind, uint64_t offset, const void* buf, uint64_t bytes) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         if (bytes && !buf) throw srla::Error(SRLA_E_INVALID, "null buffer");
         E(e).import_range(row, kind, offset, buf, bytes);
     });
@@ -2646,7 +2652,7 @@ srla_status srla_timing_get(const srla_engine* e, srla_timing* out) {
 
 srla_status srla_timing_reset(srla_engine* e) {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(e->mu);
+        std::lock_guard<std::mutex> lk(lock_of(e));
         E(e).timing_clear();
     });
 }

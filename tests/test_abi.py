@@ -75,3 +75,25 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "pyoracle" not in txt and "srla_oracle" not in txt and "oracle/" not in txt, f
+
+
+def test_new_entry_points_validate_arguments_without_a_gpu(srla_lib):
+    """Round-2 entry points reject bad arguments before touching a device:
+    the sharded pipeline, the exact store, range export/import, digests."""
+    import ctypes as C
+    from paper_1803_10369_b200 import srla
+    lib = srla.load_library()
+    from paper_1803_10369_b200.shard import CTransport, _lib as shard_lib
+    shard_lib()
+    out = C.c_void_p()
+    cfg = srla.SeaConfig(rows=2, cols=16, linear_slots=32, recorder_bits=8, window=4, theta=8).to_c()
+    t = CTransport()  # no callbacks
+    assert lib.srla_shard_create(C.byref(cfg), 0, C.byref(t), C.byref(out)) == srla.E_INVALID
+    assert lib.srla_shard_process_slice(None, 0, None, 0, 0, 0, 0, None, 0, None, None) == srla.E_INVALID
+    assert lib.srla_exact_create(0, 0, C.byref(out)) == srla.E_INVALID
+    assert b"window" in lib.srla_last_error()
+    assert lib.srla_exact_observe(None, None, 0, 0) == srla.E_INVALID
+    assert lib.srla_transport_nccl(None, 0, 1, 0, None) == srla.E_INVALID
+    buf = (C.c_uint8 * 16)()
+    assert lib.srla_export_range(None, 0, 2, 0, buf, 16) != srla.OK
+    assert lib.srla_state_blocks(None, 0, 2, None, 0, None) != srla.OK

@@ -1628,14 +1628,7 @@ struct Engine {
             return;
         }
         if (epoch) {
-            static const bool tma = [] { const char* v = std::getenv("SRLA_GATHER_TMA"); return !(v && v[0] == '0'); }();
-            if (tma && cfg.rows <= 4 && cfg.linear_slots % 16 == 0 && cfg.linear_slots <= 4096) {
-                const uint32_t sm = gather_tma_smem(cfg.linear_slots);
-                raise_smem_cap(k_union_linear_epoch_tma, sm);
-                const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((n + kGatherWarps - 1) / kGatherWarps, uint64_t(sms) * 16));
-                k_union_linear_epoch_tma<<<grid, kGatherWarps * 32, sm, st>>>(d_hosts, n, dc, static_cast<const uint8_t*>(d_lin),
-                                                                           cur_epoch, d_out);
-            } else if (cfg.rows <= 4)
+            if (cfg.rows <= 4)
                 k_union_linear_epoch<4><<<blocks(uint64_t(n) * 32, 256, 16), 256, 0, st>>>(d_hosts, n, dc, static_cast<const uint8_t*>(d_lin), cur_epoch, d_out);
             else
                 k_union_linear_epoch<64><<<blocks(uint64_t(n) * 32, 256, 16), 256, 0, st>>>(d_hosts, n, dc, static_cast<const uint8_t*>(d_lin), cur_epoch, d_out);

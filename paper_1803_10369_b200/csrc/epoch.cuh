@@ -389,70 +389,6 @@ __global__ void __launch_bounds__(256) k_row_hist(const uint8_t* __restrict__ ro
     if (c) atomicAdd(hist + threadIdx.x, sign < 0 ? 0ull - c : c);
 }
 
-// The same union weight with the candidates' cells moved by the TMA engine:
-// each warp owns a two-stage ring in shared memory; lane 0 bulk-loads the u
-// cells (g' bytes each) of the warp's next candidate while the warp reduces
-// the current one from shared memory, so ~8 KB per warp are in flight without
-// holding them in registers. For 16-byte multiples g' <= 4096 and u <= 4.
-constexpr int kGatherWarps = 4;
-__host__ __device__ constexpr uint32_t gather_tma_smem(uint32_t gl) { return kGatherWarps * 2u * 4u * gl; }
-__global__ void __launch_bounds__(kGatherWarps * 32) k_union_linear_epoch_tma(const uint32_t* __restrict__ hosts,
-                                                                           uint32_t n, DevCfg c,
-                                                                           const uint8_t* __restrict__ lin,
-                                                                           uint32_t cur, uint32_t* __restrict__ weight) {
-    extern __shared__ __align__(128) uint8_t s_cells[];
-    __shared__ __align__(8) uint64_t s_bar[kGatherWarps][2];
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t gl = c.gl, rows = c.rows;
-    uint8_t* ring = s_cells + warp * 2u * 4u * gl;
-    const uint64_t lrow = static_cast<uint64_t>(c.cols) * gl;
-    const uint32_t cur4 = cur * 0x01010101u, k4 = c.k * 0x01010101u;
-    const uint32_t nwarps = gridDim.x * kGatherWarps;
-    if (lane == 0) {
-        mbar_init(&s_bar[warp][0], 1);
-        mbar_init(&s_bar[warp][1], 1);
-    }
-    __syncwarp();
-    // lane i < rows hashes row i's column; lane 0 issues the row copies
-    auto issue = [&](uint32_t h, uint32_t b) {
-        const uint32_t a = hosts[h];
-        const uint32_t col = lane < rows ? column_of(c, lane, a) : 0u;
-        uint32_t cols[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) cols[i] = __shfl_sync(0xFFFFFFFFu, col, i);
-        if (lane == 0) {
-            mbar_expect_tx(&s_bar[warp][b], rows * gl);
-            for (uint32_t i = 0; i < rows; ++i)
-                bulk_load(ring + (b * 4u + i) * gl, lin + i * lrow + static_cast<uint64_t>(cols[i]) * gl, gl, &s_bar[warp][b]);
-        }
-    };
-    uint32_t h = blockIdx.x * kGatherWarps + warp;
-    if (h < n) issue(h, 0);
-    for (uint32_t it = 0; h < n; ++it, h += nwarps) {
-        const uint32_t b = it & 1u;
-        if (h + nwarps < n) issue(h + nwarps, b ^ 1u);  // the other stage was read out last iteration
-        mbar_wait(&s_bar[warp][b], (it >> 1) & 1u);
-        uint32_t acc = 0;
-        const uint32_t nv = gl / 16;
-        for (uint32_t q = lane; q < nv; q += 32) {
-            uint4 m = make_uint4(~0u, ~0u, ~0u, ~0u);
-            for (uint32_t i = 0; i < rows; ++i) {
-                const uint4 x = reinterpret_cast<const uint4*>(ring + (b * 4u + i) * gl)[q];
-                m.x &= __vcmpltu4(__vsub4(cur4, x.x), k4);
-                m.y &= __vcmpltu4(__vsub4(cur4, x.y), k4);
-                m.z &= __vcmpltu4(__vsub4(cur4, x.z), k4);
-                m.w &= __vcmpltu4(__vsub4(cur4, x.w), k4);
-            }
-            acc += __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
-        }
-        acc >>= 3;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-        if (lane == 0) weight[h] = acc;
-        __syncwarp();  // stage b is read out before it is refilled
-    }
-}
-
 // Union linear weight over epoch stamps: slot j counts iff every row's stamp
 // is younger than k (max over rows of the recorder value < k).
 template <int MAXR>

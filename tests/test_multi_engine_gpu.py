@@ -1,4 +1,4 @@
-"""Two ranks, each running the CUDA engine through the C ABI's sharded
+"""Two or three ranks, each running the CUDA engine through the C ABI's sharded
 pipeline (srla_shard_*), on one GPU over gloo (NCCL refuses two ranks on one
 device; the transport is the only difference from the NCCL path).
 
@@ -62,22 +62,23 @@ def _worker(rank, world, port, outdir, name, mode, force_bins):
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-@pytest.mark.parametrize("name,force_bins", [("contended", False), ("c1_shape", False), ("drift_evict", True)])
-def test_two_rank_engine_shards_match_reference(gpu, oracle, name, force_bins, mode):
+@pytest.mark.parametrize("name,force_bins,world", [("contended", False, 2), ("c1_shape", False, 2),
+                                                    ("drift_evict", True, 2), ("pipeline_small_3000", False, 3)])
+def test_engine_shards_match_reference(gpu, oracle, name, force_bins, world, mode):
     from paper_1803_10369_b200.shard import merge_reports, partition_host
     cfg, _ = S.SCENARIOS[name]
     slices = GF.scenario_slices(name, oracle)
     with tempfile.TemporaryDirectory() as d:
-        mp.start_processes(_worker, args=(2, _port(), d, name, mode, force_bins), nprocs=2, join=True,
+        mp.start_processes(_worker, args=(world, _port(), d, name, mode, force_bins), nprocs=world, join=True,
                            start_method="spawn")
-        got = [np.load(os.path.join(d, f"r{r}.npy"), allow_pickle=True) for r in range(2)]
+        got = [np.load(os.path.join(d, f"r{r}.npy"), allow_pickle=True) for r in range(world)]
     from oracle.pyoracle import SeaConfig as OC
-    pipes = [oracle.pipeline(OC(**cfg.as_dict())) for _ in range(2)]
+    pipes = [oracle.pipeline(OC(**cfg.as_dict())) for _ in range(world)]
     nonempty = 0
     for s, recs in enumerate(slices):
         parts = []
-        for r in range(2):
-            sub = partition_host(recs, cfg.seed, 2, r)
+        for r in range(world):
+            sub = partition_host(recs, cfg.seed, world, r)
             rep = pipes[r].process_slice(s, sub, True)
             assert got[r][2][s] == len(sub), f"slice {s} rank {r}: scanned {got[r][2][s]} of {len(sub)} owned"
             assert np.array_equal(got[r][1][s], pipes[r].candidates()), f"slice {s} rank {r}: candidates differ"
@@ -88,7 +89,7 @@ def test_two_rank_engine_shards_match_reference(gpu, oracle, name, force_bins, m
                 e["has_estimate"], e["is_super"] = rep["has_estimate"], rep["is_super"]
                 parts.append(e)
         want = merge_reports(parts) if parts else None
-        for r in range(2):
+        for r in range(world):
             g = got[r][0][s]
             if want is None:
                 assert g is None

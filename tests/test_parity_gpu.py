@@ -501,3 +501,34 @@ def test_state_blocks_match_exported_rows(gpu, oracle, mode, monkeypatch):
     for n in (1, 13, (1 << 20) + 3, 5 << 20):
         b = rng.integers(0, 256, n, dtype=np.uint8)
         assert np.array_equal(srla.block_sums(torch.from_numpy(b).cuda()), GF.block_sums_np(b)), n
+
+
+def test_device_records_contract(gpu, oracle):
+    """Device batches: read after the producer stream's work (torch's current
+    stream is passed as srla_scan_device's producer), and rejected unless
+    (n, 3) int32/uint32, contiguous, on the engine's GPU."""
+    import torch
+    name = "contended"
+    cfg, _ = S.SCENARIOS[name]
+    slices = GF.scenario_slices(name, oracle)[:3]
+    want = engine(cfg)
+    got = engine(cfg)
+    side = torch.cuda.Stream()
+    for s, recs in enumerate(slices):
+        host = torch.from_numpy(np.ascontiguousarray(recs, dtype=np.uint32).view(np.int32))
+        with torch.cuda.stream(side):  # produced (and scanned) on a non-default stream
+            torch.cuda._sleep(2_000_000)  # the copy lands well after the call is queued
+            dev = host.to("cuda", non_blocking=False)
+            got.scan(dev)
+        want.scan(recs)
+        a, _ = want.end_slice(s)
+        b, _ = got.end_slice(s)
+        assert (a is None and b is None) or a.tobytes() == b.tobytes()
+    assert np.array_equal(want.candidates(), got.candidates())
+    t = torch.zeros((10, 3), dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError, match="int32"):
+        got.scan(t)
+    with pytest.raises(ValueError, match="shape"):
+        got.scan(torch.zeros((10, 2), dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError, match="contiguous"):
+        got.scan(torch.zeros((3, 10), dtype=torch.int32, device="cuda").t())

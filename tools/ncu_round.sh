@@ -16,10 +16,10 @@ cap() {  # workload kernel
 }
 if [ "$W" != "c3" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c2.csv $B > $O/launches_c2.log 2>&1
-  for k in k_scan_bin "k_split<" k_slice_apply_nib k_union_linear_nib; do cap c2 "$k"; done
+  for k in k_scan_bin "^k_split$" k_slice_apply_nib k_union_linear_nib; do cap c2 "$k"; done
 fi
 if [ "$W" != "c2" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv $B --workload c3 > $O/launches_c3.log 2>&1
-  for k in k_scan_bin "k_split<" k_stamp_warp k_union_linear_epoch; do cap c3 "$k"; done
+  for k in k_scan_bin "^k_split$" k_stamp_warp k_union_linear_epoch; do cap c3 "$k"; done
 fi
 ls -la $O

@@ -423,7 +423,9 @@ struct Engine {
         CK(cudaEventCreateWithFlags(&ev_k1_gate, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_split_done, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_k1_done, cudaEventDisableTiming));
-        CK(cudaStreamCreateWithFlags(&ssplit, cudaStreamNonBlocking));
+        // the early split yields to the ordering phase on the engine stream: the
+        // split-first order measured 5.46 vs 5.19 ms per C2 step
+        CK(cudaStreamCreateWithPriority(&ssplit, cudaStreamNonBlocking, prio_low));
         CK(cudaEventRecord(ev_scan_done, st));
         ctr_k1.ensure(4);
         pin_k1.ensure(4);

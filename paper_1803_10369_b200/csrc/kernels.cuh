@@ -111,6 +111,31 @@ template <typename W, int MAXR>
 __device__ __forceinline__ uint32_t rough_weight(const DevCfg& c, const W* __restrict__ rough,
                                                  const uint32_t* __restrict__ stamp, uint32_t a,
                                                  uint32_t p, bool asof) {
+    if constexpr (sizeof(W) == 1 && MAXR <= 4) {
+        if (c.g == 8) {  // the configs of BASELINE.json: a rough cell is one 8-byte word per row
+            const uint64_t rrow = static_cast<uint64_t>(c.cols) * 8u;
+            const uint32_t k4 = c.k * 0x01010101u;
+            uint32_t act_lo = 0xFFFFFFFFu, act_hi = 0xFFFFFFFFu;  // 0xFF per slot active in every row so far
+#pragma unroll
+            for (int i = 0; i < MAXR; ++i) {
+                if (i >= static_cast<int>(c.rows)) break;
+                const uint64_t b = i * rrow + static_cast<uint64_t>(column_of(c, i, a)) * 8u;
+                const uint2 r = *reinterpret_cast<const uint2*>(rough + b);
+                uint32_t lo = __vcmpltu4(r.x, k4), hi = __vcmpltu4(r.y, k4);
+                if (asof && (lo & hi) != 0xFFFFFFFFu) {  // slots marked by this chunk's packets <= p count too
+                    const uint4 s0 = *reinterpret_cast<const uint4*>(stamp + b);
+                    const uint4 s1 = *reinterpret_cast<const uint4*>(stamp + b + 4);
+                    lo |= (s0.x <= p ? 0xFFu : 0u) | (s0.y <= p ? 0xFF00u : 0u) | (s0.z <= p ? 0xFF0000u : 0u) |
+                          (s0.w <= p ? 0xFF000000u : 0u);
+                    hi |= (s1.x <= p ? 0xFFu : 0u) | (s1.y <= p ? 0xFF00u : 0u) | (s1.z <= p ? 0xFF0000u : 0u) |
+                          (s1.w <= p ? 0xFF000000u : 0u);
+                }
+                act_lo &= lo;
+                act_hi &= hi;
+            }
+            return (__popc(act_lo) + __popc(act_hi)) >> 3;
+        }
+    }
     uint32_t cols[MAXR];
 #pragma unroll
     for (int i = 0; i < MAXR; ++i)

@@ -303,6 +303,10 @@ class EngineShard:
         """-> (merged report or None, records this rank scanned)."""
         from .srla import E_CAPACITY, _as_records, _check, _is_torch_cuda
         if _is_torch_cuda(recs):
+            import torch
+            # srla_shard_process_slice orders after the legacy default stream;
+            # records produced on another stream are waited for here
+            torch.cuda.current_stream(recs.device).synchronize()
             ptr, n, on_dev = recs.data_ptr(), recs.shape[0], 1
         else:
             recs = _as_records(recs)

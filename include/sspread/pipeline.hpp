@@ -215,15 +215,16 @@ class DetectPipeline {
         const uint32_t k = cfg_.sea.window;
         const bool due = slice_id + 1 >= k && static_cast<bool>(sink);
         const auto t1 = std::chrono::steady_clock::now();
-        uint64_t cands = 0;
-        if (due) {
-            const srla_status s = srla_candidates(sea_.eng(), nullptr, 0, &cands);
-            if (s != SRLA_OK && s != SRLA_E_CAPACITY) detail::raise_status(s, "srla_candidates");
-            entries_.reserve(cands);
-        }
+        // the hand-off buffer is sized from the first try: srla_end_slice
+        // rejects a short buffer (reporting the count) before doing any work
         uint64_t n_out = 0, kept = 0;
-        detail::check(srla_end_slice(sea_.eng(), slice_id, due ? 1 : 0, entries_.data(), entries_.size(), &n_out, &kept),
-                      "srla_end_slice");
+        srla_status es = srla_end_slice(sea_.eng(), slice_id, due ? 1 : 0, entries_.data(), entries_.size(), &n_out,
+                                        &kept);
+        if (es == SRLA_E_CAPACITY && due) {
+            entries_.reserve(n_out);
+            es = srla_end_slice(sea_.eng(), slice_id, 1, entries_.data(), entries_.size(), &n_out, &kept);
+        }
+        detail::check(es, "srla_end_slice");
         sea_.st_->mirror_valid = false;
         csip_valid_ = false;
         if (due) {
@@ -232,8 +233,7 @@ class DetectPipeline {
             WindowReport& report = report_;
             report.window_start = slice_id + 1 - k;
             report.window = k;
-            report.entries.resize(n_out);
-            for (uint64_t i = 0; i < n_out; ++i) report.entries[i] = detail::to_entry(entries_[i]);
+            detail::fill_entries(report.entries, entries_.data(), n_out);
             report.scan_ms = scan_ms;
             report.estimate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
             total_estimate_ms_ += report.estimate_ms;

@@ -27,6 +27,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -174,6 +175,24 @@ inline WindowEntry to_entry(const srla_entry& e) {
     if (e.has_estimate) w.estimate = e.estimate;
     w.is_super = e.is_super != 0;
     return w;
+}
+
+// Entries handed from the engine's buffer into a report: a single thread is
+// host-memory bound (~10 ns per entry: 24 B read + 32 B written), so large
+// reports (C2: ~750k entries) are converted on up to 16 threads.
+inline void fill_entries(std::vector<WindowEntry>& out, const srla_entry* in, uint64_t n) {
+    out.resize(n);
+    const uint64_t per = 65536;
+    const uint64_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint64_t t = std::min<uint64_t>({16, hw, (n + per - 1) / per});
+    auto run = [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t i = lo; i < hi; ++i) out[i] = to_entry(in[i]);
+    };
+    if (t <= 1) return run(0, n);
+    std::vector<std::thread> pool;
+    for (uint64_t w = 1; w < t; ++w) pool.emplace_back(run, n * w / t, n * (w + 1) / t);
+    run(0, n / t);
+    for (auto& th : pool) th.join();
 }
 
 }  // namespace detail
@@ -385,8 +404,7 @@ class EstimatorArray {
         std::vector<srla_entry> buf(n);
         double fp = 0.0;
         detail::check(srla_report(eng(), buf.data(), buf.size(), &n, &fp), "srla_report");
-        rep.entries.reserve(n);
-        for (uint64_t i = 0; i < n; ++i) rep.entries.push_back(detail::to_entry(buf[i]));
+        detail::fill_entries(rep.entries, buf.data(), n);
         rep.estimate_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         return rep;
     }

@@ -13,7 +13,9 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <filesystem>
 #include <fstream>
 #include <functional>
 #include <span>
@@ -91,9 +93,17 @@ class DetectPipeline {
     // the file crosses to HBM once; parsing, orientation and the slice
     // boundaries run on the GPU (srla_parse_srlt / srla_orient_records /
     // srla_slice_bounds) and every slice is scanned where it lies. CSV traces
-    // take the host path.
+    // take the host path, and so do binary traces above kDeviceTraceBytes
+    // (SRLA_DEVICE_TRACE_MAX overrides it): the device front end holds the
+    // file and two record copies in HBM, the host path streams the file one
+    // slice at a time, as the reference does.
+    static constexpr uint64_t kDeviceTraceBytes = 8ull << 30;
     void run(const std::string& trace_path, const ReportSink& sink) {
-        if (sniff_trace_format(trace_path) == TraceFormat::binary) {
+        uint64_t limit = kDeviceTraceBytes;
+        if (const char* v = std::getenv("SRLA_DEVICE_TRACE_MAX")) limit = std::strtoull(v, nullptr, 0);
+        std::error_code ec;
+        const auto fsize = std::filesystem::file_size(trace_path, ec);
+        if (sniff_trace_format(trace_path) == TraceFormat::binary && (ec || fsize <= limit)) {
             run_device(trace_path, sink);
             return;
         }

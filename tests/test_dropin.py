@@ -93,12 +93,14 @@ def test_dropin_pipeline_replay_matches_oracle(gpu, oracle, dropin_bin, tmp_path
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("front", ["device", "host"])
 @pytest.mark.parametrize("name", ["pipeline_small", "c1_shape"])
-def test_dropin_run_device_front_end_matches_oracle(gpu, oracle, dropin_bin, tmp_path, name):
+def test_dropin_run_device_front_end_matches_oracle(gpu, oracle, dropin_bin, tmp_path, name, front):
     """DetectPipeline::run on a raw SRLT file with far-side (flipped) and
     off-network records: the device front end (parse, orient, slice in HBM)
-    gives the reports and candidates of the reference pipeline fed the
-    host-oriented, partitioned records."""
+    and the streaming host path taken by traces above the device size limit
+    (forced here with SRLA_DEVICE_TRACE_MAX=0) give the reports and candidates
+    of the reference pipeline fed the host-oriented, partitioned records."""
     from oracle.pyoracle import SeaConfig as OCfg
     cfg, _ = S.SCENARIOS[name]
     slices = GF.scenario_slices(name, oracle)
@@ -114,9 +116,10 @@ def test_dropin_run_device_front_end_matches_oracle(gpu, oracle, dropin_bin, tmp
     _write_srlt(trace, raw)
     out = tmp_path / "run.txt"
     c = cfg
+    env = dict(os.environ, SRLA_DEVICE_TRACE_MAX="0") if front == "host" else None
     subprocess.run([dropin_bin, "run", str(trace), str(out), str(c.rows), str(c.cols), str(c.rough_slots),
                     str(c.linear_slots), str(c.recorder_bits), str(c.window), str(c.theta), hex(c.seed)],
-                   check=True, timeout=600)
+                   check=True, timeout=600, env=env)
     lines = open(out).read().split("\n")
     ori, st = oracle.orient(raw, 0x0A000000, 8)
     assert lines[-2] == "orient " + " ".join(str(int(x)) for x in st)

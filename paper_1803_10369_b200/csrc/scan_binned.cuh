@@ -285,18 +285,33 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
 
         // coalesced bin writes: consecutive staging entries of a region go to
         // consecutive bin slots
+        // four entries per thread per round, every shared load before the
+        // global stores (a generic-pointer store would otherwise order them)
         bool ovf = false;
-        for (uint32_t idx = tid; idx < total; idx += kBinThreads) {
-            uint32_t v = s_off[idx], r;
-            if (b.pack) {
-                r = v >> b.region_shift;
-                v &= rmask;
-            } else {
-                r = s_reg[idx];
+        constexpr int kWU = 4;
+        for (uint32_t idx0 = tid; idx0 < total; idx0 += kWU * kBinThreads) {
+            uint32_t v[kWU], r[kWU];
+            uint2 wv[kWU];
+#pragma unroll
+            for (int u = 0; u < kWU; ++u) {
+                const uint32_t idx = idx0 + u * kBinThreads;
+                v[u] = idx < total ? s_off[idx] : 0u;
+                if (b.pack) {
+                    r[u] = v[u] >> b.region_shift;
+                    v[u] &= rmask;
+                } else {
+                    r[u] = idx < total ? s_reg[idx] : 0u;
+                }
             }
-            const uint2 wv = s_win[r];
-            if (idx < wv.y) b.bins[wv.x + idx] = v;
-            else ovf = true;
+#pragma unroll
+            for (int u = 0; u < kWU; ++u) wv[u] = s_win[r[u]];
+#pragma unroll
+            for (int u = 0; u < kWU; ++u) {
+                const uint32_t idx = idx0 + u * kBinThreads;
+                if (idx >= total) break;
+                if (idx < wv[u].y) __stcg(b.bins + (wv[u].x + idx), v[u]);
+                else ovf = true;
+            }
         }
         if (__syncthreads_or(ovf)) {  // a bin is full: mark the rest directly (marks commute)
             if (b.no_direct) {  // the table is busy elsewhere: the caller reruns this scan

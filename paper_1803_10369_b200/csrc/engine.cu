@@ -964,7 +964,10 @@ struct Engine {
                 const uint32_t sparse_max = stamp_sparse_max;
                 const uint32_t sp = cfg.rows <= kStampWarpRows && lin_words % 4 == 0 ? sparse_max : 0u;
                 if (sp) {
-                    k_stamp_warp<<<sms * 5, 256, stamp_claim_bytes(fcfg.shift), st>>>(static_cast<uint8_t*>(d_lin), lin_words, fcfg, sp, cur_epoch,
+                    // 5 blocks fit an SM; 40 per SM make the warp-strided slice assignment
+                    // finer (C3: 3.28 vs 3.35 ms with 5; profiles/r02/ab_region_waves.txt)
+                    static const uint32_t stamp_per_sm = [] { const char* v = std::getenv("SRLA_STAMP_BLOCKS"); return v ? static_cast<uint32_t>(std::atoi(v)) : 40u; }();
+                    k_stamp_warp<<<sms * stamp_per_sm, 256, stamp_claim_bytes(fcfg.shift), st>>>(static_cast<uint8_t*>(d_lin), lin_words, fcfg, sp, cur_epoch,
                                                          cfg.window, cfg.rows, hist.p);
                     check_launch();
                     launched();
@@ -985,9 +988,13 @@ struct Engine {
             return;
         }
         if (nib) {
-            // 512 threads per slice block: 1.09 vs 1.12 ms (256) and 1.27 ms (1024) per C2 slice
+            // 512 threads per slice block: 1.09 vs 1.12 ms (256) and 1.27 ms (1024) per C2 slice.
+            // Two blocks fit an SM (112 KB of stages); the grid is 16 per SM so the
+            // strided slice assignment balances: 1.00 ms vs 1.09 ms with 3 per SM
+            // (2: 1.07, 4: 1.03, 8: 1.01, 24: 1.00; profiles/r02/ab_region_waves.txt)
             static const uint32_t apply_threads = [] { const char* v = std::getenv("SRLA_APPLY_THREADS"); return v ? static_cast<uint32_t>(std::atoi(v)) : 512u; }();
-            k_slice_apply_nib<<<std::min<uint32_t>(fcfg.nfine, sms * 3), apply_threads, nib_apply_smem(), st>>>(
+            static const uint32_t apply_per_sm = [] { const char* v = std::getenv("SRLA_APPLY_BLOCKS"); return v ? static_cast<uint32_t>(std::atoi(v)) : 16u; }();
+            k_slice_apply_nib<<<std::min<uint32_t>(fcfg.nfine, sms * apply_per_sm), apply_threads, nib_apply_smem(), st>>>(
                 static_cast<uint8_t*>(d_lin), lin_words, fcfg, fcfg.nfine, mode, cfg.window, dc.expired, d_counts.p);
             check_launch();
             launched();

@@ -100,11 +100,13 @@ int nccl_alltoallv(void* ctx, const void* send, const uint64_t* sb, const uint64
     const NcclApi& a = nccl();
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (a.group_start() != ncclSuccess) return 1;
+    bool ok = true;
     for (uint32_t j = 0; j < c->world; ++j) {  // grouped point-to-point: one all-to-all
-        if (sb[j]) a.send(static_cast<const char*>(send) + so[j], sb[j], ncclChar, static_cast<int>(j), c->comm, st);
-        if (rb[j]) a.recv(static_cast<char*>(recv) + ro[j], rb[j], ncclChar, static_cast<int>(j), c->comm, st);
+        if (sb[j]) ok &= a.send(static_cast<const char*>(send) + so[j], sb[j], ncclChar, static_cast<int>(j), c->comm, st) == ncclSuccess;
+        if (rb[j]) ok &= a.recv(static_cast<char*>(recv) + ro[j], rb[j], ncclChar, static_cast<int>(j), c->comm, st) == ncclSuccess;
     }
-    return a.group_end() == ncclSuccess ? 0 : 1;
+    const bool ended = a.group_end() == ncclSuccess;  // the group is closed even after a failed enqueue
+    return ok && ended ? 0 : 1;
 }
 
 // ---------------------------------------------------------------- shard kernels
@@ -269,18 +271,16 @@ struct srla_shard {
         keys2.ensure(std::max<uint64_t>(n, 1));
         part.ensure(std::max<uint64_t>(n, 1) * 12);
         starts.ensure(W + 1);
+        if (n > (1ull << 30)) throw std::runtime_error("shard range above 2^30 records");  // one sort call's int count
         if (n) {
             srla::k_owner_keys<<<grid(n), 256, 0, st>>>(reinterpret_cast<const srla::Rec12*>(d_in), n, sub3, W, keys.p);
             SK(cudaGetLastError());
             auto* vin = reinterpret_cast<const srla::Rec12*>(d_in);
             auto* vout = reinterpret_cast<srla::Rec12*>(part.p);
-            for (uint64_t o = 0; o < n; o += (1ull << 30)) {  // stable, so records keep slice order per owner
-                const int m = static_cast<int>(std::min<uint64_t>(1ull << 30, n - o));
-                cub_call([&](void* tp, size_t& b) {
-                    return cub::DeviceRadixSort::SortPairs(tp, b, keys.p + o, keys2.p + o, vin + o, vout + o, m, 0, end_bit, st);
-                });
-            }
-            if (n > (1ull << 30)) throw std::runtime_error("shard range above 2^30 records");
+            // stable, so records keep slice order per owner
+            cub_call([&](void* tp, size_t& b) {
+                return cub::DeviceRadixSort::SortPairs(tp, b, keys.p, keys2.p, vin, vout, static_cast<int>(n), 0, end_bit, st);
+            });
         }
         srla::k_bucket_starts<<<1, 256, 0, st>>>(keys2.p, n, W, starts.p);
         SK(cudaGetLastError());

@@ -294,6 +294,7 @@ struct Engine {
     // epoch-stamp linear table (epoch.cuh): u8 stamps, O(1) slide
     bool epoch = false;
     uint32_t stamp_sparse_max = 1024;  // SRLA_STAMP_SPARSE, read per engine at setup
+    int dedup_mode = -1;               // SRLA_K1_DEDUP: 1 on, 0 off, -1 on after the first bin overflow
     uint32_t cur_epoch = 0;
     DevBuf<unsigned long long> hist;  // rows x 256
     PinBuf<unsigned long long> pin_hist;
@@ -753,6 +754,12 @@ struct Engine {
         // K1 stages (region, offset) as one word when the table has <= 2^32 recorders (C2: exactly)
         bcfg.pack = shift < 32 && (uint64_t(bcfg.nregions) << shift) <= (1ull << 32) ? 1u : 0u;
         if (const char* pk = std::getenv("SRLA_K1_PACK"); pk && pk[0] == '0') bcfg.pack = 0;
+        // K1's duplicate-mark filter: off until a region bin overflows (then on
+        // for the engine's life); SRLA_K1_DEDUP=1 / 0 forces it
+        const char* dd = std::getenv("SRLA_K1_DEDUP");
+        dedup_mode = dd ? (dd[0] == '1' ? 1 : 0) : -1;
+        bcfg.dedup = bcfg.pack && dedup_mode == 1 ? 1u : 0u;
+        bcfg.seen_ovf = nullptr;  // set where K1 runs with the ordering counters
         // forced-binned small tables (tests): tiny bins, so the overflow paths run
         uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);
         if (const char* be = std::getenv("SRLA_SMALL_BIN_ENTRIES"); be && small) coarse_total = std::strtoull(be, nullptr, 10);
@@ -1072,10 +1079,10 @@ struct Engine {
         CK(cudaEventRecord(t_scan0, sk));
         const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
         if (cfg.rows == 4)
-            k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), sk>>>(
+            k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions, bcfg.dedup), sk>>>(
                 d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
         else
-            k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), sk>>>(
+            k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions, bcfg.dedup), sk>>>(
                 d_recs, n, dc, b2, EpochCfg{0u, 0u, nullptr, 0ull}, static_cast<W*>(d_lin), d_stamp, ev.p, ev_cap, ctr_k1.p, vec);
         CK(cudaGetLastError());
         CK(cudaEventRecord(t_scan1, sk));
@@ -1249,6 +1256,7 @@ struct Engine {
         while (true) {
             setup_order(ev_cap);
             CK(cudaMemsetAsync(octr.p, 0, kOcCount * sizeof(uint32_t), st));
+            bcfg.seen_ovf = octr.p + kOcBinOvf;
             if (use_bins) {
                 const uint64_t add = uint64_t(n) * cfg.rows;
                 if ((pending_entries + add) / bcfg.nregions * 13 / 10 + 8192 > bcfg.cap) flush_linear();
@@ -1258,9 +1266,9 @@ struct Engine {
             if (use_bins && MAXR <= kBinRows) {
                 const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
                 if (cfg.rows == 4)
-                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
+                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions, bcfg.dedup), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
                 else
-                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
+                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions, bcfg.dedup), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, evc, vec);
             } else {
                 k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, evc, vec);
             }
@@ -1294,6 +1302,7 @@ struct Engine {
             CK(cudaEventElapsedTime(&ms, t_scan0, t_scan1));
             timing.scan_kernel_ms += ms;
             timing.order_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w_order).count();
+            if (pc[kOcBinOvf] && dedup_mode < 0 && bcfg.pack) bcfg.dedup = 1;
             if (pc[kOcEvents] <= ev_cap) break;
             // event overflow: the ordering kernels did nothing; marks and rough
             // stamps are idempotent, so K1 reruns with room
@@ -1377,9 +1386,9 @@ struct Engine {
             if (use_bins && MAXR <= kBinRows) {
                 const uint32_t tiles = (n + kBinTile - 1) / kBinTile;
                 if (cfg.rows == 4)
-                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                    k_scan_bin<W, 4><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions, bcfg.dedup), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
                 else
-                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
+                    k_scan_bin<W, 0><<<std::min<uint32_t>(tiles, sms * 2), kBinThreads, bin_smem(bcfg.nregions, bcfg.dedup), st>>>(d_recs, n, dc, bcfg, ecfg(), lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             } else {
                 k_scan<W, MAXR><<<blocks((n + 3) / 4, 256, 16), 256, 0, st>>>(d_recs, n, dc, lin, d_stamp, ev.p, ev_cap, ctr.p, vec);
             }

@@ -42,6 +42,7 @@ enum OrderCtr : uint32_t {
     kOcPushList = 6, // pushes emitted (collect mode)
     kOcTuples = 7,   // distinct open (row, col, bit) keys
     kOcFallback = 8, // too many flagged hosts for the on-device resolution
+    kOcBinOvf = 9,   // a K1 region bin overflowed (k_scan_bin)
     kOcCount = 12
 };
 

@@ -67,6 +67,8 @@ struct BinCfg {
     uint32_t no_direct;     // a bin overflow sets *overflow instead of marking the table directly
     uint32_t* overflow;
     uint32_t pack;          // region << region_shift | offset fits 32 bits (tables of <= 2^32 words)
+    uint32_t dedup;         // drop marks this block staged before (needs pack; see k_scan_bin)
+    uint32_t* seen_ovf;     // set when a bin overflowed (the engine then turns dedup on)
 };
 
 constexpr int kBinThreads = 512;
@@ -75,8 +77,12 @@ constexpr int kBinTile = kBinThreads * kBinPerThread;       // packets per tile
 constexpr int kBinRows = 4;                                 // rows handled by the binned path
 constexpr int kBinEntries = kBinTile * kBinRows;
 constexpr int kMaxRegions = 4096;
+// duplicate-mark filter: a direct-mapped cache of 2^kDedupBits mark words per block
+constexpr int kDedupBits = 13;
 // k_scan_bin dynamic shared memory for `nregions` regions (2 blocks per SM up to kMaxRegions)
-constexpr int bin_smem(uint32_t nregions) { return static_cast<int>(nregions) * 16 + kBinEntries * 6; }
+constexpr int bin_smem(uint32_t nregions, uint32_t dedup = 1) {
+    return static_cast<int>(nregions) * 16 + kBinEntries * 6 + (dedup ? (4 << kDedupBits) : 0);
+}
 
 // Epoch-stamp mode of the linear table (epoch.cuh): marks write the current
 // epoch instead of 0 and keep per-row stamp histograms.
@@ -143,6 +149,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                                                          uint32_t ev_cap, uint32_t* __restrict__ ev_count, int vec) {
     // dynamic shared memory (bin_smem(nregions) bytes):
     //   win[nregions] (uint2) | cnt[nregions] | lbase[nregions] | off[kBinEntries] | reg[kBinEntries] (u16)
+    //   | seen[2^kDedupBits]
     // win: per region {bin slot of staging entry idx = x + idx (mod 2^32; nregions * cap < 2^32),
     //                  first staging index that no longer fits the region's bin}
     extern __shared__ __align__(16) uint8_t s_bin_raw[];
@@ -151,7 +158,15 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
     uint32_t* s_lbase = s_cnt + b.nregions;
     uint32_t* s_off = s_lbase + b.nregions;
     uint16_t* s_reg = reinterpret_cast<uint16_t*>(s_off + kBinEntries);
+    // Duplicate marks (same recorder word) are idempotent: with b.dedup a
+    // mark whose word this block staged earlier in the launch is dropped
+    // (adversarial skew: one host's 1e7 packets per slice hit the same 4
+    // cells and would overflow their region bins). The cache only ever holds
+    // words already staged, so a dropped mark is applied by its twin.
+    uint32_t* s_seen = reinterpret_cast<uint32_t*>(s_reg + kBinEntries);
     __shared__ uint32_t s_warp[kBinThreads / 32];
+    if (b.dedup)
+        for (uint32_t q = threadIdx.x; q < (1u << kDedupBits); q += kBinThreads) s_seen[q] = 0xFFFFFFFFu;
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint64_t lrow = static_cast<uint64_t>(c.cols) * c.gl;
@@ -207,7 +222,14 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                         const uint64_t w = i * lrow + static_cast<uint64_t>(col) * c.gl + lslot;
                         const uint32_t r = static_cast<uint32_t>(w >> b.region_shift);
                         off[q][i] = static_cast<uint32_t>(w) & rmask;
-                        rr[q][i] = (r << 16) | atomicAdd(&s_cnt[r], 1u);
+                        bool dup = false;
+                        if (b.dedup) {  // w < 2^32 (pack)
+                            const uint32_t key = static_cast<uint32_t>(w);
+                            uint32_t* slot = s_seen + ((key * 0x9E3779B1u) >> (32 - kDedupBits));
+                            dup = *slot == key;
+                            if (!dup) *slot = key;
+                        }
+                        if (!dup) rr[q][i] = (r << 16) | atomicAdd(&s_cnt[r], 1u);
                     }
                 }
                 if (live && (sample & c.tau_mask) == 0u) {  // sampled (1 in 2^tau): rough stamps
@@ -314,6 +336,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
             }
         }
         if (__syncthreads_or(ovf)) {  // a bin is full: mark the rest directly (marks commute)
+            if (tid == 0 && b.seen_ovf) atomicOr(b.seen_ovf, 1u);
             if (b.no_direct) {  // the table is busy elsewhere: the caller reruns this scan
                 if (tid == 0) atomicOr(b.overflow, 1u);
                 __syncthreads();

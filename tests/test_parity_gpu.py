@@ -43,14 +43,18 @@ def test_engine_matches_reference_golden(gpu, oracle, name, order, monkeypatch):
     assert msg is None, msg
 
 
+@pytest.mark.parametrize("dedup", ["auto", "0", "1"])
 @pytest.mark.parametrize("epoch", ["1", "0"])
 @pytest.mark.parametrize("name", [n for n in sorted(S.SCENARIOS) if S.SCENARIOS[n][0].rows <= 4])
-def test_binned_marks_match_reference_golden(gpu, oracle, name, epoch, monkeypatch):
+def test_binned_marks_match_reference_golden(gpu, oracle, name, epoch, dedup, monkeypatch):
     """Same goldens with the binned linear-mark path forced on (~8 regions,
     tiny bins so the overflow-to-direct-mark path runs too), with epoch-stamp
-    recorders (z <= 7) and with literal ones."""
+    recorders (z <= 7) and with literal ones; K1's duplicate-mark filter on
+    from the first bin overflow (auto), never, or always."""
     monkeypatch.setenv("SRLA_FORCE_BINS", "1")
     monkeypatch.setenv("SRLA_EPOCH", epoch)
+    if dedup != "auto":
+        monkeypatch.setenv("SRLA_K1_DEDUP", dedup)
     g = json.load(open(os.path.join(GOLD, f"{name}.json")))
     cfg, _ = S.SCENARIOS[name]
     slices = GF.scenario_slices(name, oracle)

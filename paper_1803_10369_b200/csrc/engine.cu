@@ -758,7 +758,7 @@ struct Engine {
         // for the engine's life); SRLA_K1_DEDUP=1 / 0 forces it
         const char* dd = std::getenv("SRLA_K1_DEDUP");
         dedup_mode = dd ? (dd[0] == '1' ? 1 : 0) : -1;
-        bcfg.dedup = fcfg.skew = bcfg.pack && dedup_mode == 1 ? 1u : 0u;
+        bcfg.dedup = bcfg.pack && dedup_mode == 1 ? 1u : 0u;
         bcfg.seen_ovf = nullptr;  // set where K1 runs with the ordering counters
         // forced-binned small tables (tests): tiny bins, so the overflow paths run
         uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);
@@ -1302,7 +1302,7 @@ struct Engine {
             CK(cudaEventElapsedTime(&ms, t_scan0, t_scan1));
             timing.scan_kernel_ms += ms;
             timing.order_wall_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w_order).count();
-            if (pc[kOcBinOvf] && dedup_mode < 0 && bcfg.pack) bcfg.dedup = fcfg.skew = 1;
+            if (pc[kOcBinOvf] && dedup_mode < 0 && bcfg.pack) bcfg.dedup = 1;
             if (pc[kOcEvents] <= ev_cap) break;
             // event overflow: the ordering kernels did nothing; marks and rough
             // stamps are idempotent, so K1 reruns with room

@@ -438,7 +438,6 @@ struct FineCfg {
     uint32_t nfine;       // total fine slices covering the table
     unsigned long long* streamed;  // table bytes read (= written) by the apply kernels (statistics)
     uint32_t nib;                  // linear recorders packed two per byte (nibble.cuh)
-    uint32_t skew;                 // rank entries warp-aggregated (hot fine slices; set with BinCfg::dedup)
 };
 
 constexpr int kSplitThreads = 512;
@@ -468,22 +467,9 @@ __device__ __forceinline__ void split_tile(uint32_t* s_sorted, uint32_t r, uint3
         off[4 * q + 3] = e0 + 4 * q + 3 < n ? x.w : 0xFFFFFFFFu;
     }
     uint32_t rank[kSplitPerThread];
-    if (f.skew) {  // one shared atomic per distinct slice per warp: a hot slice is not a 32-way conflict
-        const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-        for (int k = 0; k < kSplitPerThread; ++k) {
-            const uint32_t key = off[k] != 0xFFFFFFFFu ? off[k] >> f.shift : 0xFFFFFFFFu;
-            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, key);
-            const uint32_t leader = __ffs(peers) - 1u;
-            uint32_t base = 0;
-            if (key != 0xFFFFFFFFu && lane == leader) base = atomicAdd(&s_cnt[key], __popc(peers));
-            rank[k] = __shfl_sync(0xFFFFFFFFu, base, leader) + __popc(peers & lt);
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < kSplitPerThread; ++k)
-            if (off[k] != 0xFFFFFFFFu) rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
-    }
+    for (int k = 0; k < kSplitPerThread; ++k)
+        if (off[k] != 0xFFFFFFFFu) rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
     __syncthreads();
     uint32_t mine = 0;
     const uint32_t b0 = tid * per_thread;

@@ -97,3 +97,50 @@ def test_unaligned_device_records(gpu, oracle):
     got = GF.run_flow(Unaligned(_engine(cfg)), cfg, slices)
     msg = GF.compare(ref, got)
     assert msg is None, msg
+
+
+def _u32(seed, index, key):
+    """HashFamily::u32 (hash.hpp:53-62) in numpy: the sample hash of a bip."""
+    def av(x):
+        with np.errstate(over="ignore"):
+            x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            return x ^ (x >> np.uint64(31))
+    with np.errstate(over="ignore"):
+        sub = av(np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15) * np.uint64(index + 1))
+    return (av(sub ^ np.asarray(key, dtype=np.uint64)) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+
+def test_every_packet_sampled_overflows_event_list(gpu, oracle):
+    """Slices whose every destination passes the sampling test (ctz of the
+    sample hash >= tau): 1.2x more sampled packets than the event list sized for
+    an ordinary 2^27-record chunk (2^27 >> tau + ...), so the ordering phase
+    grows it and reruns K1; thousands of hosts cross at once. The hash the
+    destinations are picked with is checked against the reference's first."""
+    cfg, _ = S.SCENARIOS["contended"]
+    assert [int(x) for x in _u32(cfg.seed, 0, np.array([0, 1, 12345], np.uint64))] == \
+        [oracle.hash_u32(cfg.seed, 0, k) for k in (0, 1, 12345)]
+    e = _engine(cfg)
+    tau = e.tau
+    assert tau >= 5
+    rng = np.random.default_rng(11)
+    cand = rng.integers(0, 2**32, 8_000_000, dtype=np.uint64)
+    h = _u32(cfg.seed, 0, cand)
+    sampled = cand[(h & np.uint32((1 << tau) - 1)) == 0].astype(np.uint32)
+    assert len(sampled) > 20000
+    base = GF.scenario_slices("contended", oracle)
+    slices = []
+    # the fast path's initial event list (Engine::scan_chunk_fast), overshot by 20%
+    ev_cap = (1 << 27 >> tau) + (1 << 27 >> (tau + 3)) + 65536
+    for s in range(2):
+        n = ev_cap * 6 // 5
+        r = np.zeros((n, 3), np.uint32)
+        r[:, 1] = 0x0A000000 + rng.integers(0, 6000, n).astype(np.uint32)
+        r[:, 2] = sampled[rng.integers(0, len(sampled), n)]
+        slices.append(r)
+    slices += base[:cfg.window]
+    a = GF.run_flow(_oracle(oracle, cfg), cfg, slices)
+    b = GF.run_flow(GF.EngineBackend(e), cfg, slices)
+    msg = GF.compare(a, b)
+    assert msg is None, msg
+    assert a[0]["pushes"]["n"] > 1000

@@ -6,6 +6,9 @@ c5: configs[4] — adversarial skew: one host meeting 1e7 distinct peers in ever
     slice ahead of a uniform 1e8-pair scan storm (PlantSpec.window = 1, so the
     rotation does not split the peers, generator.hpp:135-137).
 c4 (configs[3]) is c2's shape at 1e9 packets/slice over 8 GPUs: bench.py --gpus N.
+c1: configs[0] — the SPEC default on the CPU reference (acceptance criterion 5,
+    acceptance_main.cpp:263-278): seeds 11-15, 120 one-second slices, k = 30,
+    z = 8, v = 65536; a parity case, not a bench line.
 """
 from __future__ import annotations
 
@@ -48,3 +51,15 @@ DESCRIPTIONS = {
     "c5": "C5: u=4 v=2^20 g=8 g'=1024 z=4 k=10 theta=1024 seed=0x5EA00001; trace seed 5, host 10.200.0.1 x 1e7 "
           "peers every slice ahead of 1e8 uniform pairs (12M sources, 16M destinations)",
 }
+
+
+def c1_sketch():
+    return dict(rows=4, cols=65536, rough_slots=8, linear_slots=1024, recorder_bits=8, window=30, theta=1024,
+                seed=SKETCH_SEED)
+
+
+def c1_spec(seed, slices=120):
+    """100,000 uniform sources, 65,536 Zipf(1.0) destinations, 8,000 background
+    pairs per slice and the 50 always-active plants."""
+    return dict(seed=seed, slices=slices, window=30, a_hosts=100_000, b_hosts=65_536, pairs_per_slice=8000,
+                skew=1.0, plants=[(0x0AC80001 + i, c, 0, 0xFFFFFFFF) for i, c in enumerate(plant_cards())])

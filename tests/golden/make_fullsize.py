@@ -1,5 +1,5 @@
 """Full-size parity digests from the REFERENCE (oracle/_ref, the unmodified
-headers): BASELINE.json's C2 / C3 / C5 workloads, every slice.
+headers): BASELINE.json's C1 (seeds 11-15) / C2 / C3 / C5 workloads, every slice.
 
 The reference is driven like DetectPipeline::process_slice with ONE scan worker
 (record order: pipeline.hpp:134-139, the parity definition of SURVEY.md §8c);
@@ -14,6 +14,7 @@ retained list and the recorder state (block digests of every indicator / rough
 / linear row in SSEA order, digest.cuh) — each as (n, sha256).
 
   python tests/golden/make_fullsize.py c2 [--slices 12] [--threads N]
+  python tests/golden/make_fullsize.py c1 --seed 11      (120 slices; seeds 11-15)
 
 C2 and C5 need ~5 GiB of host RAM; C3 (64 GiB of linear recorders) needs the
 GPU box's host: run it there through gpurun and commit the JSON it writes.
@@ -52,18 +53,24 @@ def state_digest_ref(flow, rows):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("workload", choices=["c2", "c3", "c5"])
-    ap.add_argument("--slices", type=int, default=12)
+    ap.add_argument("workload", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--slices", type=int, default=None, help="12 (c2/c3/c5), 120 (c1)")
+    ap.add_argument("--seed", type=int, default=11, help="c1 trace seed (11-15)")
     ap.add_argument("--pairs", type=int, default=WL.PAIRS)
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     ref = Checker("ref")
-    cfg = WL.sketch_cfg(WL.cols_of(a.workload))
-    spec = WL.trace_spec(a.pairs, slices=a.slices, workload=a.workload)
+    if a.workload == "c1":
+        a.slices = a.slices or 120
+        cfg, spec, name = WL.c1_sketch(), WL.c1_spec(a.seed, a.slices), f"c1_s{a.seed}"
+    else:
+        a.slices = a.slices or 12
+        cfg = WL.sketch_cfg(WL.cols_of(a.workload))
+        spec, name = WL.trace_spec(a.pairs, slices=a.slices, workload=a.workload), a.workload
     flow = ref.flow(SeaConfig(**cfg), threads=a.threads)
-    out = a.out or os.path.join(HERE, f"fullsize_{a.workload}.json")
-    doc = {"workload": a.workload, "cfg": cfg, "spec": spec, "slices": [],
+    out = a.out or os.path.join(HERE, f"fullsize_{name}.json")
+    doc = {"workload": name, "cfg": cfg, "spec": spec, "slices": [],
            "source": "oracle/_ref (unmodified reference headers), 1 scan worker, bulk passes chunked"}
     buf = None
     for s in range(a.slices):

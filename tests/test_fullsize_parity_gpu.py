@@ -1,5 +1,6 @@
-"""Full-size parity at BASELINE.json's named configs (C2 configs[1], C3
-configs[2], C5 configs[4]) against the REFERENCE, slice by slice.
+"""Full-size parity at BASELINE.json's named configs (C1 configs[0] with
+seeds 11-15, C2 configs[1], C3 configs[2], C5 configs[4]) against the
+REFERENCE, slice by slice.
 
 tests/golden/fullsize_<wl>.json holds what the unmodified reference headers
 (oracle/_ref) produce on the workload's trace when driven like
@@ -110,6 +111,14 @@ def test_c3_fullsize_bit_exact_vs_reference(gpu):
     """C3 (v = 2^24: 64 GiB of epoch-stamped linear recorders, ~1e6 candidates)."""
     st = run_fullsize("c3")
     print("c3 stats:", st)
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13, 14, 15])
+def test_c1_acceptance_bit_exact_vs_reference(gpu, seed):
+    """C1 (configs[0], acceptance criterion 5): v = 65536, z = 8, k = 30, 120
+    slices of 8,000 background pairs + 50 always-active plants, seeds 11-15."""
+    st = run_fullsize(f"c1_s{seed}")
+    print(f"c1 seed {seed} stats:", st)
 
 
 def test_c5_fullsize_bit_exact_vs_reference(gpu):

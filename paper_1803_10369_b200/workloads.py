@@ -8,7 +8,10 @@ c5: configs[4] — adversarial skew: one host meeting 1e7 distinct peers in ever
 c4 (configs[3]) is c2's shape at 1e9 packets/slice over 8 GPUs: bench.py --gpus N.
 c1: configs[0] — the SPEC default on the CPU reference (acceptance criterion 5,
     acceptance_main.cpp:263-278): seeds 11-15, 120 one-second slices, k = 30,
-    z = 8, v = 65536; a parity case, not a bench line.
+    z = 8, v = 65536; a parity case, not a bench line. Its discrete-window
+    variants (criteria 4 and 6, acceptance_main.cpp:347-400): three 300-second
+    slices, z = 1, k = 1, v = 65536 with 150,000 pairs (seeds 1-5) and
+    v = 1024 with 600,000 pairs (seeds 21-25).
 """
 from __future__ import annotations
 
@@ -63,3 +66,14 @@ def c1_spec(seed, slices=120):
     pairs per slice and the 50 always-active plants."""
     return dict(seed=seed, slices=slices, window=30, a_hosts=100_000, b_hosts=65_536, pairs_per_slice=8000,
                 skew=1.0, plants=[(0x0AC80001 + i, c, 0, 0xFFFFFFFF) for i, c in enumerate(plant_cards())])
+
+
+def discrete_sketch(cols):
+    return dict(rows=4, cols=cols, rough_slots=8, linear_slots=1024, recorder_bits=1, window=1, theta=1024,
+                seed=SKETCH_SEED)
+
+
+def discrete_spec(seed, pairs):
+    return dict(seed=seed, slices=3, window=1, slice_seconds=300, a_hosts=100_000, b_hosts=65_536,
+                pairs_per_slice=pairs, skew=1.0,
+                plants=[(0x0AC80001 + i, c, 0, 0xFFFFFFFF) for i, c in enumerate(plant_cards())])

@@ -15,6 +15,7 @@ retained list and the recorder state (block digests of every indicator / rough
 
   python tests/golden/make_fullsize.py c2 [--slices 12] [--threads N]
   python tests/golden/make_fullsize.py c1 --seed 11      (120 slices; seeds 11-15)
+  python tests/golden/make_fullsize.py crit4 --seed 1    (seeds 1-5; crit6: seeds 21-25)
 
 C2 and C5 need ~5 GiB of host RAM; C3 (64 GiB of linear recorders) needs the
 GPU box's host: run it there through gpurun and commit the JSON it writes.
@@ -53,7 +54,7 @@ def state_digest_ref(flow, rows):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("workload", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("workload", choices=["c1", "crit4", "crit6", "c2", "c3", "c5"])
     ap.add_argument("--slices", type=int, default=None, help="12 (c2/c3/c5), 120 (c1)")
     ap.add_argument("--seed", type=int, default=11, help="c1 trace seed (11-15)")
     ap.add_argument("--pairs", type=int, default=WL.PAIRS)
@@ -64,6 +65,10 @@ def main():
     if a.workload == "c1":
         a.slices = a.slices or 120
         cfg, spec, name = WL.c1_sketch(), WL.c1_spec(a.seed, a.slices), f"c1_s{a.seed}"
+    elif a.workload in ("crit4", "crit6"):  # acceptance criteria 4 / 6: 3 slices, z = 1, k = 1
+        a.slices = 3
+        cols, pairs = (65536, 150_000) if a.workload == "crit4" else (1024, 600_000)
+        cfg, spec, name = WL.discrete_sketch(cols), WL.discrete_spec(a.seed, pairs), f"{a.workload}_s{a.seed}"
     else:
         a.slices = a.slices or 12
         cfg = WL.sketch_cfg(WL.cols_of(a.workload))
@@ -73,10 +78,18 @@ def main():
     doc = {"workload": name, "cfg": cfg, "spec": spec, "slices": [],
            "source": "oracle/_ref (unmodified reference headers), 1 scan worker, bulk passes chunked"}
     buf = None
+    whole = None
+    if spec.get("slice_seconds", 1) != 1:  # generate_trace, then SlicePartitioner (trace.hpp:243-281)
+        recs_all = ref.generate(PlantSpec(**spec))
+        ids = (recs_all[:, 0].astype(np.int64) - int(recs_all[0, 0])) // spec["slice_seconds"]
+        whole = [recs_all[ids == k] for k in range(a.slices)]
     for s in range(a.slices):
         t0 = time.time()
-        recs = ref.generate_slice(PlantSpec(**spec), s, a.threads, out=buf)
-        buf = recs if buf is None else buf
+        if whole is not None:
+            recs = np.ascontiguousarray(whole[s])
+        else:
+            recs = ref.generate_slice(PlantSpec(**spec), s, a.threads, out=buf)
+            buf = recs if buf is None else buf
         rec = {"records": {"n": int(len(recs)), "sha": sha_blocks([ref.block_sums(recs, a.threads)])}}
         t1 = time.time()
         pushes = flow.scan(recs)

@@ -1,6 +1,6 @@
 """Full-size parity at BASELINE.json's named configs (C1 configs[0] with
-seeds 11-15, C2 configs[1], C3 configs[2], C5 configs[4]) against the
-REFERENCE, slice by slice.
+seeds 11-15 and its discrete-window variants, C2 configs[1], C3 configs[2],
+C5 configs[4]) against the REFERENCE, slice by slice.
 
 tests/golden/fullsize_<wl>.json holds what the unmodified reference headers
 (oracle/_ref) produce on the workload's trace when driven like
@@ -15,7 +15,9 @@ checked against the reference generator's — through the C ABI's production
 path (srla_scan_batch on device records, fused srla_end_slice), and every
 item must be identical. The recorder digests are computed on the device
 (srla_state_blocks), so the 64 GiB C3 table is compared every slice without
-leaving HBM. Nothing here reads the reference tree: only the committed digests.
+leaving HBM. Nothing here reads the reference tree: only the committed digests
+(300-second slices come from the oracle's restated generator, checked against
+the digests of the reference generator's records).
 """
 from __future__ import annotations
 
@@ -51,15 +53,28 @@ def _strip(d):  # compare counts and digests (lists too long to store verbatim)
     return None if d is None else {"n": d["n"], "sha": d["sha"]}
 
 
+def _host_slices(spec):
+    """Slices of a spec with slice_seconds != 1 (the device generator's domain
+    is 1-second slices): the restated generate_trace (pinned to the
+    reference's by test_oracle_golden.py), partitioned as SlicePartitioner
+    does (trace.hpp:243-281), moved to the device."""
+    import torch
+    from oracle.pyoracle import Checker, PlantSpec
+    recs = Checker("orc").generate(PlantSpec(**spec))
+    ids = (recs[:, 0].astype(np.int64) - int(recs[0, 0])) // spec["slice_seconds"]
+    return [torch.from_numpy(np.ascontiguousarray(recs[ids == k]).view(np.int32)).cuda() for k in range(spec["slices"])]
+
+
 def run_fullsize(wl, handoff="entries"):
     from paper_1803_10369_b200 import srla
     g = _golden(wl)
     cfg = g["cfg"]
     eng = srla.EstimatorArray(srla.SeaConfig(**cfg))
-    gen = srla.DeviceTraceGenerator(srla.PlantSpec(**g["spec"]))
+    host = _host_slices(g["spec"]) if g["spec"].get("slice_seconds", 1) != 1 else None
+    gen = None if host else srla.DeviceTraceGenerator(srla.PlantSpec(**g["spec"]))
     L = cfg["linear_slots"] + 1
     for s, want in enumerate(g["slices"]):
-        t = gen.slice_tensor(s)
+        t = host[s] if host else gen.slice_tensor(s)
         got = {"records": {"n": int(t.shape[0]), "sha": _sha_blocks([srla.block_sums(t)])}}
         assert got["records"] == want["records"], f"{wl} slice {s}: device generator differs from the reference's"
         pushes = eng.scan_collect(t)
@@ -119,6 +134,14 @@ def test_c1_acceptance_bit_exact_vs_reference(gpu, seed):
     slices of 8,000 background pairs + 50 always-active plants, seeds 11-15."""
     st = run_fullsize(f"c1_s{seed}")
     print(f"c1 seed {seed} stats:", st)
+
+
+@pytest.mark.parametrize("wl", [f"crit4_s{k}" for k in range(1, 6)] + [f"crit6_s{k}" for k in range(21, 26)])
+def test_discrete_window_criteria_bit_exact_vs_reference(gpu, wl):
+    """Acceptance criteria 4 and 6 (acceptance_main.cpp:347-400): three
+    300-second slices, z = 1 (expired = 1), k = 1; v = 65536 with 150,000
+    pairs per slice (seeds 1-5) and v = 1024 with 600,000 (seeds 21-25)."""
+    run_fullsize(wl)
 
 
 def test_c5_fullsize_bit_exact_vs_reference(gpu):

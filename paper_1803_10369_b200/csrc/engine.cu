@@ -295,6 +295,7 @@ struct Engine {
     bool epoch = false;
     uint32_t stamp_sparse_max = 1024;  // SRLA_STAMP_SPARSE, read per engine at setup
     int dedup_mode = -1;               // SRLA_K1_DEDUP: 1 on, 0 off, -1 on after the first bin overflow
+    uint32_t split_threads = 512;      // k_split block (SRLA_SPLIT_THREADS)
     uint32_t cur_epoch = 0;
     DevBuf<unsigned long long> hist;  // rows x 256
     PinBuf<unsigned long long> pin_hist;
@@ -796,10 +797,15 @@ struct Engine {
         fcfg.streamed = d_streamed.p;
         CK(cudaMemsetAsync(fine_count.p, 0, fine_count.cap * sizeof(uint32_t), st));
         const int smem = static_cast<int>(lin_bytes(1ull << fs));
-        split_smem = 2 * kSplitTile * 4 + fcfg.per_region * 16;  // two tile stages + per-slice tables
+        // 1024-thread split blocks (16384-entry tiles) for wide fan-outs: twice the
+        // entries per fine slice per tile, half the bin reservations (C3: 2048 slices per region)
+        split_threads = fcfg.per_region >= 1024 ? 1024u : 512u;
+        if (const char* v = std::getenv("SRLA_SPLIT_THREADS")) split_threads = std::atoi(v) == 1024 ? 1024u : 512u;
+        split_smem = 2 * uint64_t(split_threads) * kSplitPerThread * 4 + fcfg.per_region * 16;  // two tile stages + per-slice tables
         with_w([&](auto w) {
             using W = decltype(w);
-            raise_smem_cap(k_split<W>, static_cast<int>(split_smem));
+            raise_smem_cap(k_split<W, 512>, static_cast<int>(split_smem));
+            raise_smem_cap(k_split<W, 1024>, static_cast<int>(split_smem));
             raise_smem_cap(k_slice_apply<W>, std::max(smem, 16));
             raise_smem_cap(k_slice_apply_bulk<W>, std::max(2 * smem, 32));
         });
@@ -922,7 +928,8 @@ struct Engine {
         }
         if (split_in_flight) CK(cudaStreamWaitEvent(s, ev_split_done, 0));  // tile_prefix reuse
         split_in_flight = false;
-        k_split_prefix<<<1, 1024, 0, s>>>(bin_count.p, R, bcfg.cap, tile_prefix.p);
+        const uint32_t tile = split_threads * kSplitPerThread;
+        k_split_prefix<<<1, 1024, 0, s>>>(bin_count.p, R, bcfg.cap, tile, tile_prefix.p);
         check_launch();
         launched();
         const cudaEvent_t t0 = timer_start(s);
@@ -930,10 +937,14 @@ struct Engine {
             using W = decltype(w);
             // an early split leaves room for the ordering phase's kernels
             static const uint32_t waves = [] { const char* v = std::getenv("SRLA_SPLIT_WAVES"); return v ? static_cast<uint32_t>(std::atoi(v)) : 16u; }();
-            const uint64_t max_tiles = pending_entries / kSplitTile + R;
-            k_split<W><<<static_cast<uint32_t>(std::min<uint64_t>(max_tiles, sms * (s == st ? 8u : waves))), kSplitThreads, split_smem, s>>>(
-                bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R, bcfg.region_shift, fcfg, ecfg(),
-                static_cast<W*>(d_lin));
+            const uint64_t max_tiles = pending_entries / tile + R;
+            const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(max_tiles, sms * (s == st ? 8u : waves)));
+            if (split_threads == 1024)
+                k_split<W, 1024><<<grid, 1024, split_smem, s>>>(bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R,
+                                                                bcfg.region_shift, fcfg, ecfg(), static_cast<W*>(d_lin));
+            else
+                k_split<W, 512><<<grid, 512, split_smem, s>>>(bins.p, bcfg.cap, tile_prefix.p, tile_prefix.p + R + 1, R,
+                                                              bcfg.region_shift, fcfg, ecfg(), static_cast<W*>(d_lin));
         });
         check_launch();
         launched();

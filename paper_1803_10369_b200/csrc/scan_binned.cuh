@@ -440,21 +440,23 @@ struct FineCfg {
     uint32_t nib;                  // linear recorders packed two per byte (nibble.cuh)
 };
 
-constexpr int kSplitThreads = 512;
+constexpr int kSplitThreads = 512;  // default block; 1024 for fan-outs >= 1024 (Engine::setup_bins)
 constexpr int kSplitPerThread = 16;
 constexpr int kSplitTile = kSplitThreads * kSplitPerThread;  // 8192 entries
+template <int T>
+constexpr int split_tile_entries() { return T * kSplitPerThread; }
 
 // One k_split tile: the n entries of region r staged at s_sorted (loaded
 // there; sorted in place) -> fine-slice bins. s_cnt must be zero on entry.
 // Ends with a block barrier.
-template <typename W>
+template <typename W, int T>
 __device__ __forceinline__ void split_tile(uint32_t* s_sorted, uint32_t r, uint32_t n, uint32_t* s_cnt,
                                            uint32_t* s_lbase, uint2* s_win, uint32_t* s_warp,
                                            uint32_t region_shift, const FineCfg& f, const EpochCfg& ep,
                                            W* __restrict__ lin) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t fmask = (1u << f.shift) - 1u;
-    const uint32_t per_thread = (f.per_region + kSplitThreads - 1) / kSplitThreads;
+    const uint32_t per_thread = (f.per_region + T - 1) / T;
     uint32_t off[kSplitPerThread];
     const uint32_t e0 = tid * kSplitPerThread;
     const uint4* v = reinterpret_cast<const uint4*>(s_sorted + e0);
@@ -504,14 +506,14 @@ __device__ __forceinline__ void split_tile(uint32_t* s_sorted, uint32_t r, uint3
         }
     __syncthreads();
     bool ovf = false;
-    for (uint32_t i = tid; i < n; i += kSplitThreads) {
+    for (uint32_t i = tid; i < n; i += T) {
         const uint32_t v = s_sorted[i];
         const uint2 wv = s_win[v >> 16];
         if (i < wv.y) f.bins[wv.x + i] = static_cast<uint16_t>(v);
         else ovf = true;
     }
     if (__syncthreads_or(ovf)) {  // a fine bin is full: mark in place (marks commute)
-        for (uint32_t i = tid; i < n; i += kSplitThreads) {
+        for (uint32_t i = tid; i < n; i += T) {
             const uint32_t v = s_sorted[i];
             const uint32_t b = v >> 16;
             if (i < s_win[b].y) continue;
@@ -534,25 +536,26 @@ __device__ __forceinline__ void split_tile(uint32_t* s_sorted, uint32_t r, uint3
 // Re-bin coarse region bins by fine slice. One tile = 8192 consecutive entries
 // of one region: shared-memory counting sort by slice (ranks from shared
 // atomics), one global reservation per slice per tile, coalesced u16 writes.
-template <typename W>
-__global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __restrict__ coarse, uint32_t coarse_cap,
+template <typename W, int T>
+__global__ void __launch_bounds__(T, 1024 / T) k_split(const uint32_t* __restrict__ coarse, uint32_t coarse_cap,
                                                          const uint32_t* __restrict__ tile_prefix,
                                                          const uint32_t* __restrict__ coarse_n, uint32_t nregions,
                                                          uint32_t region_shift, FineCfg f, EpochCfg ep,
                                                          W* __restrict__ lin) {
     // dynamic shared memory, sized by the fan-out f.per_region (<= 4096):
-    //   stage[2][kSplitTile] | cnt[P] | lbase[P] | win[P] (uint2)
+    //   stage[2][T * kSplitPerThread] | cnt[P] | lbase[P] | win[P] (uint2)
     // A tile's entries are bulk-loaded into its stage while the block sorts
     // the previous tile (the coarse bins have >= 16 bytes of slack at the end);
     // once read into registers, the stage holds the tile's sorted entries.
+    constexpr uint32_t kTile = split_tile_entries<T>();
     extern __shared__ __align__(128) uint32_t s_dyn[];
     uint32_t* s_stage = s_dyn;
-    uint32_t* s_cnt = s_dyn + 2 * kSplitTile;
+    uint32_t* s_cnt = s_dyn + 2 * kTile;
     uint32_t* s_lbase = s_cnt + f.per_region;
     // per fine slice: {bin slot of sorted entry i = x + i (mod 2^32; nfine * cap < 2^32 by
     // construction, Engine::setup_bins), first sorted index that no longer fits its bin}
     uint2* s_win = reinterpret_cast<uint2*>(s_lbase + f.per_region);
-    __shared__ uint32_t s_warp[kSplitThreads / 32];
+    __shared__ uint32_t s_warp[T / 32];
     __shared__ uint32_t s_region[2], s_n[2];
     __shared__ __align__(8) uint64_t s_bar[2];
     const uint32_t tid = threadIdx.x;
@@ -565,13 +568,13 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
             if (tile_prefix[mid] <= t) lo = mid;
             else hi = mid;
         }
-        const uint32_t begin = (t - tile_prefix[lo]) * kSplitTile;
-        const uint32_t n = min(coarse_n[lo] - begin, static_cast<uint32_t>(kSplitTile));
+        const uint32_t begin = (t - tile_prefix[lo]) * kTile;
+        const uint32_t n = min(coarse_n[lo] - begin, kTile);
         s_region[b] = lo;
         s_n[b] = n;
         const uint32_t bytes = (n * 4u + 15u) & ~15u;
         mbar_expect_tx(&s_bar[b], bytes);
-        bulk_load(s_stage + b * kSplitTile, coarse + static_cast<uint64_t>(lo) * coarse_cap + begin, bytes, &s_bar[b]);
+        bulk_load(s_stage + b * kTile, coarse + static_cast<uint64_t>(lo) * coarse_cap + begin, bytes, &s_bar[b]);
     };
     if (tid == 0) {
         mbar_init(&s_bar[0], 1);
@@ -584,26 +587,26 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_split(const uint32_t* __re
         const uint32_t sb = it & 1u;
         // the other stage was last read by the previous tile, finished at its final barrier
         if (tid == 0 && t + gridDim.x < total_tiles) issue(t + gridDim.x, sb ^ 1u);
-        for (uint32_t i = tid; i < f.per_region; i += kSplitThreads) s_cnt[i] = 0;
+        for (uint32_t i = tid; i < f.per_region; i += T) s_cnt[i] = 0;
         mbar_wait(&s_bar[sb], (it >> 1) & 1u);
         __syncthreads();
         const uint32_t r = s_region[sb];
         const uint32_t n = s_n[sb];
-        split_tile<W>(s_stage + sb * kSplitTile, r, n, s_cnt, s_lbase, s_win, s_warp, region_shift, f, ep, lin);
+        split_tile<W, T>(s_stage + sb * kTile, r, n, s_cnt, s_lbase, s_win, s_warp, region_shift, f, ep, lin);
     }
 }
 
 // k_split's tile table on the device (no host round trip): per region the
 // clamped entry count n_r = min(count, cap) (overflow was marked directly)
-// and the exclusive prefix of its kSplitTile-entry tiles; prefix[R] = total
+// and the exclusive prefix of its `tile`-entry tiles; prefix[R] = total
 // tiles, which k_split reads. Out: prefix[0..R], n_r at prefix + R + 1.
 __global__ void __launch_bounds__(1024) k_split_prefix(const uint32_t* __restrict__ count, uint32_t nregions,
-                                                       uint32_t cap, uint32_t* __restrict__ prefix) {
+                                                       uint32_t cap, uint32_t tile, uint32_t* __restrict__ prefix) {
     __shared__ uint32_t s_w[32];
     const uint32_t per = (nregions + 1023) / 1024;  // regions per thread (nregions <= kMaxRegions)
     const uint32_t r0 = threadIdx.x * per;
     uint32_t mine = 0;
-    for (uint32_t r = r0; r < min(r0 + per, nregions); ++r) mine += (min(count[r], cap) + kSplitTile - 1) / kSplitTile;
+    for (uint32_t r = r0; r < min(r0 + per, nregions); ++r) mine += (min(count[r], cap) + tile - 1) / tile;
     uint32_t incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(1024) k_split_prefix(const uint32_t* __restric
         const uint32_t n = min(count[r], cap);
         prefix[r] = run;
         prefix[nregions + 1 + r] = n;
-        run += (n + kSplitTile - 1) / kSplitTile;
+        run += (n + tile - 1) / tile;
     }
     if (threadIdx.x == 1023) prefix[nregions] = run;
 }

@@ -476,6 +476,21 @@ def run_engine(args):
                "d2h_bytes_per_step": int(d2h / args.steps),
                "api": "srla_shard_process_slice(host records)" if shard is not None else
                "srla_scan_batch(host, pinned) + srla_end_slice_async/wait"}
+        # the ceiling of this path: plain pinned host->device copies of the same
+        # slice on this box (best of 3), against the copies inside the e2e loop
+        src = torch.from_numpy(host[0].reshape(-1).view(np.uint8))
+        dst = torch.empty(src.numel(), dtype=torch.uint8, device=torch.device("cuda", local))
+        best = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            best = max(best, src.numel() / (time.perf_counter() - t1) / 1e9)
+        del dst
+        achieved = h2d * args.steps / el / 1e9  # this rank's copies (each rank moves its own slices)
+        e2e["h2d"] = {"achieved_gbs_per_gpu": achieved, "pinned_copy_peak_gbs": best, "frac": achieved / best,
+                      "definition": "e2e H2D bytes / e2e time, over plain pinned H2D copies of one slice (best of 3)"}
         del host
 
     # the reference's own entry point through the drop-in headers (C++):

@@ -144,3 +144,26 @@ def test_every_packet_sampled_overflows_event_list(gpu, oracle):
     msg = GF.compare(a, b)
     assert msg is None, msg
     assert a[0]["pushes"]["n"] > 1000
+
+
+def test_large_host_batch_equals_device_batch(gpu):
+    """A 40M-record host batch (pinned and pageable) crosses in staged chunks —
+    full steps and a short final one — and must leave exactly the state, the
+    candidates and the report that the same records scanned from HBM leave."""
+    import torch
+    from paper_1803_10369_b200 import srla
+    from paper_1803_10369_b200 import workloads as WL
+    cfg = WL.sketch_cfg(1 << 16)
+    gen = srla.DeviceTraceGenerator(srla.PlantSpec(**WL.trace_spec(40_000_000, slices=2)))
+    t = gen.slice_tensor(0)
+    host = t.cpu().numpy().view(np.uint32)
+    pinned = torch.from_numpy(host.copy()).pin_memory().numpy()
+    out = []
+    for src in (t, host, pinned):
+        e = srla.EstimatorArray(srla.SeaConfig(**cfg))
+        pushes = e.scan_collect(src)
+        blocks = [e.state_blocks(i, k).tobytes() for i in range(cfg["rows"]) for k in (0, 1, 2)]
+        out.append((pushes.tolist(), e.candidates().tolist(), blocks))
+    assert out[0][0] == out[1][0] == out[2][0] and len(out[0][0]) > 0
+    assert out[0][1] == out[1][1] == out[2][1]
+    assert out[0][2] == out[1][2] == out[2][2]

@@ -147,9 +147,10 @@ def test_every_packet_sampled_overflows_event_list(gpu, oracle):
 
 
 def test_large_host_batch_equals_device_batch(gpu):
-    """A 40M-record host batch (pinned and pageable) crosses in staged chunks —
-    full steps and a short final one — and must leave exactly the state, the
-    candidates and the report that the same records scanned from HBM leave."""
+    """A 40M-record host batch (pinned and pageable) crosses in staged 16M-record
+    chunks, each scanned as it lands, and must leave exactly the pushes, the
+    candidates and the recorder state that the same records scanned from HBM
+    leave."""
     import torch
     from paper_1803_10369_b200 import srla
     from paper_1803_10369_b200 import workloads as WL

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                                                          BinCfg b, EpochCfg ep, W* __restrict__ lin,
                                                          uint32_t* __restrict__ stamp, uint32_t* __restrict__ ev,
                                                          uint32_t ev_cap, uint32_t* __restrict__ ev_count, int vec) {
-    // dynamic shared memory (bin_smem(nregions) bytes):
+    // dynamic shared memory (bin_smem(nregions, dedup) bytes):
     //   win[nregions] (uint2) | cnt[nregions] | lbase[nregions] | off[kBinEntries] | reg[kBinEntries] (u16)
     //   | seen[2^kDedupBits]
     // win: per region {bin slot of staging entry idx = x + idx (mod 2^32; nregions * cap < 2^32),
@@ -174,11 +174,12 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
     const uint32_t rmask = (1u << b.region_shift) - 1u;
     const uint32_t ntiles = (n + kBinTile - 1) / kBinTile;
     const uint32_t regs_per_thread = (b.nregions + kBinThreads - 1) / kBinThreads;
+    for (uint32_t r = tid; r < b.nregions; r += kBinThreads) s_cnt[r] = 0;
+    __syncthreads();
 
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (uint32_t r = tid; r < b.nregions; r += kBinThreads) s_cnt[r] = 0;
-        __syncthreads();
-
+        // s_cnt is zero here: cleared before the loop and by each region's
+        // owner thread once it has read the count (below)
         const uint32_t base = tile * kBinTile + tid * kBinPerThread;
         uint32_t src[kBinPerThread], dst[kBinPerThread];
         uint32_t valid = 0;
@@ -275,15 +276,40 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
         uint32_t wbase = 0;
         for (uint32_t w2 = 0; w2 < warp; ++w2) wbase += s_warp[w2];
         uint32_t run = wbase + incl - mine;
-        for (uint32_t r = r0; r < min(r0 + regs_per_thread, b.nregions); ++r) {
-            const uint32_t cn = s_cnt[r];
-            s_lbase[r] = run;
-            if (cn) {
-                const uint32_t g = atomicAdd(b.count + r, cn);
-                const uint32_t fit = g >= b.cap ? 0u : min(cn, b.cap - g);
-                s_win[r] = make_uint2(r * b.cap + g - run, run + fit);
+        // Each region's global bin reservation is issued here and its window
+        // stored only after the scatter below, which hides the atomic's round
+        // trip (owners of <= 2 regions; more regions per thread store at once).
+        // The owner clears its counts for the next tile once read.
+        constexpr int kDefer = 2;
+        uint32_t dg[kDefer], dcn[kDefer], dlb[kDefer];
+        const bool defer = regs_per_thread <= static_cast<uint32_t>(kDefer);
+        if (defer) {
+#pragma unroll
+            for (int j = 0; j < kDefer; ++j) {
+                const uint32_t r = r0 + j;
+                dcn[j] = 0;
+                if (static_cast<uint32_t>(j) < regs_per_thread && r < b.nregions) {
+                    const uint32_t cn = s_cnt[r];
+                    s_cnt[r] = 0;
+                    s_lbase[r] = run;
+                    dlb[j] = run;
+                    dcn[j] = cn;
+                    if (cn) dg[j] = atomicAdd(b.count + r, cn);
+                    run += cn;
+                }
             }
-            run += cn;
+        } else {
+            for (uint32_t r = r0; r < min(r0 + regs_per_thread, b.nregions); ++r) {
+                const uint32_t cn = s_cnt[r];
+                s_cnt[r] = 0;
+                s_lbase[r] = run;
+                if (cn) {
+                    const uint32_t g = atomicAdd(b.count + r, cn);
+                    const uint32_t fit = g >= b.cap ? 0u : min(cn, b.cap - g);
+                    s_win[r] = make_uint2(r * b.cap + g - run, run + fit);
+                }
+                run += cn;
+            }
         }
         uint32_t total = 0;
         for (uint32_t w2 = 0; w2 < kBinThreads / 32; ++w2) total += s_warp[w2];
@@ -303,6 +329,15 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                         s_reg[p] = static_cast<uint16_t>(reg);
                     }
                 }
+        if (defer) {
+#pragma unroll
+            for (int j = 0; j < kDefer; ++j)
+                if (dcn[j]) {
+                    const uint32_t r = r0 + j, g = dg[j], cn = dcn[j];
+                    const uint32_t fit = g >= b.cap ? 0u : min(cn, b.cap - g);
+                    s_win[r] = make_uint2(r * b.cap + g - dlb[j], dlb[j] + fit);
+                }
+        }
         __syncthreads();
 
         // coalesced bin writes: consecutive staging entries of a region go to
@@ -354,8 +389,8 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                 else
                     mark_word<W>(lin + (static_cast<uint64_t>(r) << b.region_shift), o);
             }
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
@@ -458,15 +493,17 @@ __device__ __forceinline__ void split_tile(uint32_t* s_sorted, uint32_t r, uint3
     const uint32_t fmask = (1u << f.shift) - 1u;
     const uint32_t per_thread = (f.per_region + T - 1) / T;
     uint32_t off[kSplitPerThread];
-    const uint32_t e0 = tid * kSplitPerThread;
-    const uint4* v = reinterpret_cast<const uint4*>(s_sorted + e0);
+    // entries 4 * (q * T + tid) .. + 3: consecutive lanes read consecutive
+    // 16-byte vectors (no bank conflicts); which thread ranks an entry is free
+    const uint4* v = reinterpret_cast<const uint4*>(s_sorted);
 #pragma unroll
     for (int q = 0; q < kSplitPerThread / 4; ++q) {
-        const uint4 x = v[q];
-        off[4 * q] = e0 + 4 * q < n ? x.x : 0xFFFFFFFFu;
-        off[4 * q + 1] = e0 + 4 * q + 1 < n ? x.y : 0xFFFFFFFFu;
-        off[4 * q + 2] = e0 + 4 * q + 2 < n ? x.z : 0xFFFFFFFFu;
-        off[4 * q + 3] = e0 + 4 * q + 3 < n ? x.w : 0xFFFFFFFFu;
+        const uint32_t e0 = 4u * (q * T + tid);
+        const uint4 x = v[q * T + tid];
+        off[4 * q] = e0 < n ? x.x : 0xFFFFFFFFu;
+        off[4 * q + 1] = e0 + 1 < n ? x.y : 0xFFFFFFFFu;
+        off[4 * q + 2] = e0 + 2 < n ? x.z : 0xFFFFFFFFu;
+        off[4 * q + 3] = e0 + 3 < n ? x.w : 0xFFFFFFFFu;
     }
     uint32_t rank[kSplitPerThread];
 #pragma unroll

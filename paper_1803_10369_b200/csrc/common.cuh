@@ -27,6 +27,9 @@ struct DevCfg {
     uint32_t wbytes;
     uint64_t sub_sample, sub_rslot, sub_ind;
     uint64_t sub_row[kMaxRows];
+    // sub_hi_term(sub) of each sub-key (hash_u32k): the high word's share of
+    // the first multiply, constant per hash function
+    uint32_t kh_sample, kh_rslot, kh_row[kMaxRows];
 };
 
 // hash.hpp:9-13 (splitmix64 finalizer)
@@ -43,11 +46,40 @@ __host__ __device__ __forceinline__ uint64_t sub_key(uint64_t seed, uint32_t ind
 __host__ __device__ __forceinline__ uint32_t hash_u32(uint64_t sub, uint32_t key) {
     return static_cast<uint32_t>(avalanche64(sub ^ static_cast<uint64_t>(key)));
 }
+// hash_u32 in 32-bit halves (the key only touches the low word): with
+// x = sub ^ key, (x ^ x >> 30).hi depends on sub alone, so its product with
+// the low word of the first multiplier is a per-function constant
+// kh = sub_hi_term(sub). Bit-identical to hash_u32 (tests/test_hash_halves.py
+// compares the two on the host); three instructions fewer per hash.
+__host__ __device__ __forceinline__ uint32_t sub_hi_term(uint64_t sub) {
+    const uint32_t hi = static_cast<uint32_t>(sub >> 32);
+    return (hi ^ (hi >> 30)) * 0x1CE4E5B9u;
+}
+__host__ __device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t s) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_r(lo, hi, s);
+#else
+    return static_cast<uint32_t>(((static_cast<uint64_t>(hi) << 32) | lo) >> s);
+#endif
+}
+__host__ __device__ __forceinline__ uint32_t hash_u32k(uint64_t sub, uint32_t kh, uint32_t key) {
+    const uint32_t xlo = static_cast<uint32_t>(sub) ^ key;
+    const uint32_t ylo = xlo ^ funnel_r(xlo, static_cast<uint32_t>(sub >> 32), 30);
+    // * 0xBF58476D1CE4E5B9 (mod 2^64)
+    const uint64_t z = static_cast<uint64_t>(ylo) * 0x1CE4E5B9u + (static_cast<uint64_t>(ylo * 0xBF58476Du + kh) << 32);
+    const uint32_t zlo = static_cast<uint32_t>(z), zhi = static_cast<uint32_t>(z >> 32);
+    const uint32_t tlo = zlo ^ funnel_r(zlo, zhi, 27), thi = zhi ^ (zhi >> 27);
+    // * 0x94D049BB133111EB (mod 2^64)
+    const uint64_t u = static_cast<uint64_t>(tlo) * 0x133111EBu +
+                       (static_cast<uint64_t>(tlo * 0x94D049BBu + thi * 0x133111EBu) << 32);
+    const uint32_t ulo = static_cast<uint32_t>(u);
+    return ulo ^ funnel_r(ulo, static_cast<uint32_t>(u >> 32), 31);
+}
 // HashFamily::reduce = (u64(h) * range) >> 32 (hash.hpp:60-62)
 __device__ __forceinline__ uint32_t reduce32(uint32_t h, uint32_t range) { return __umulhi(h, range); }
 
 __device__ __forceinline__ uint32_t column_of(const DevCfg& c, uint32_t row, uint32_t aip) {
-    return reduce32(hash_u32(c.sub_row[row], aip), c.cols);
+    return reduce32(hash_u32k(c.sub_row[row], c.kh_row[row], aip), c.cols);
 }
 __device__ __forceinline__ uint32_t indicator_bit_index(const DevCfg& c, uint32_t aip) {
     return reduce32(hash_u32(c.sub_ind, aip), kIndicatorBits);

@@ -460,6 +460,9 @@ struct Engine {
         dc.sub_rslot = sub_key(cfg.seed, kRoughSlotHash);
         dc.sub_ind = sub_key(cfg.seed, kIndicatorHash);
         for (uint32_t i = 0; i < kMaxRows; ++i) dc.sub_row[i] = sub_key(cfg.seed, kRowHashBase + i);
+        dc.kh_sample = sub_hi_term(dc.sub_sample);
+        dc.kh_rslot = sub_hi_term(dc.sub_rslot);
+        for (uint32_t i = 0; i < kMaxRows; ++i) dc.kh_row[i] = sub_hi_term(dc.sub_row[i]);
         lin_words = static_cast<uint64_t>(cfg.cols) * cfg.linear_slots;
         rough_words = static_cast<uint64_t>(cfg.cols) * cfg.rough_slots;
         const uint64_t rows = cfg.rows;
@@ -760,6 +763,7 @@ struct Engine {
         const char* dd = std::getenv("SRLA_K1_DEDUP");
         dedup_mode = dd ? (dd[0] == '1' ? 1 : 0) : -1;
         bcfg.dedup = bcfg.pack && dedup_mode == 1 ? 1u : 0u;
+        bcfg.ab_nohoist = std::getenv("SRLA_K1_HOIST") && std::getenv("SRLA_K1_HOIST")[0] == '0' ? 1u : 0u;
         bcfg.seen_ovf = nullptr;  // set where K1 runs with the ordering counters
         // forced-binned small tables (tests): tiny bins, so the overflow paths run
         uint64_t coarse_total = small ? (1ull << 16) : (1ull << 29);

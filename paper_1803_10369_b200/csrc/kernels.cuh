@@ -69,10 +69,10 @@ __global__ void __launch_bounds__(256) k_scan(const uint32_t* __restrict__ recs,
         for (uint32_t q = 0; q < 4; ++q) {
             rsl[q] = 0;
             if (q < valid) {
-                const uint32_t sample = hash_u32(c.sub_sample, dst[q]);
+                const uint32_t sample = hash_u32k(c.sub_sample, c.kh_sample, dst[q]);
                 const uint32_t lslot = c.gl_mask ? (sample & c.gl_mask) : (sample % c.gl);
                 const bool smp = (sample & c.tau_mask) == 0u;
-                const uint32_t rslot = smp ? reduce32(hash_u32(c.sub_rslot, dst[q]), c.g) : 0u;
+                const uint32_t rslot = smp ? reduce32(hash_u32k(c.sub_rslot, c.kh_rslot, dst[q]), c.g) : 0u;
 #pragma unroll
                 for (int i = 0; i < MAXR; ++i) {
                     if (i < static_cast<int>(c.rows)) {

@@ -424,7 +424,7 @@ __global__ void k_scan_serial(const uint32_t* __restrict__ recs, uint32_t n, Dev
         const uint32_t aip = recs[3ull * r + 1], bip = recs[3ull * r + 2];
         uint32_t cols[MAXR];
         for (uint32_t i = 0; i < c.rows && i < MAXR; ++i) cols[i] = column_of(c, i, aip);
-        const uint32_t sample = hash_u32(c.sub_sample, bip);
+        const uint32_t sample = hash_u32k(c.sub_sample, c.kh_sample, bip);
         const uint32_t lslot = c.gl_mask ? (sample & c.gl_mask) : (sample % c.gl);
         for (uint32_t i = 0; i < c.rows; ++i) {  // linear marks, every pair (sea.hpp:155-161)
             const uint64_t w = i * lrow + static_cast<uint64_t>(cols[i]) * c.gl + lslot;
@@ -436,7 +436,7 @@ __global__ void k_scan_serial(const uint32_t* __restrict__ recs, uint32_t n, Dev
         }
         if ((sample & c.tau_mask) != 0u) continue;  // not sampled (sea.hpp:164)
         ++ev;
-        const uint32_t rslot = reduce32(hash_u32(c.sub_rslot, bip), c.g);
+        const uint32_t rslot = reduce32(hash_u32k(c.sub_rslot, c.kh_rslot, bip), c.g);
         for (uint32_t i = 0; i < c.rows; ++i) rough[i * rrow + static_cast<uint64_t>(cols[i]) * c.g + rslot] = W(0);
         uint32_t weight = 0;  // union rough weight (sea.hpp:172-181)
         for (uint32_t j = 0; j < c.g; ++j) {

@@ -69,6 +69,7 @@ struct BinCfg {
     uint32_t pack;          // region << region_shift | offset fits 32 bits (tables of <= 2^32 words)
     uint32_t dedup;         // drop marks this block staged before (needs pack; see k_scan_bin)
     uint32_t* seen_ovf;     // set when a bin overflowed (the engine then turns dedup on)
+    uint32_t ab_nohoist;    // A/B (SRLA_K1_HOIST=0): the filter's branch inside the mark loop
 };
 
 constexpr int kBinThreads = 512;
@@ -205,13 +206,14 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
         uint32_t off[kBinPerThread][kBinRows], rr[kBinPerThread][kBinRows];
         uint32_t smask = 0, rsl[kBinPerThread];
         const uint32_t nrows = ROWS ? static_cast<uint32_t>(ROWS) : c.rows;
-        auto place = [&](auto full_tag) {
+        auto place = [&](auto full_tag, auto dedup_tag) {
             constexpr bool kFull = decltype(full_tag)::value;
+            constexpr bool kDedup = decltype(dedup_tag)::value;
 #pragma unroll
             for (uint32_t q = 0; q < kBinPerThread; ++q) {
                 rsl[q] = 0;
                 const bool live = kFull || q < valid;
-                const uint32_t sample = hash_u32(c.sub_sample, dst[q]);
+                const uint32_t sample = hash_u32k(c.sub_sample, c.kh_sample, dst[q]);
                 const uint32_t lslot = c.gl_mask ? (sample & c.gl_mask) : (sample % c.gl);
                 uint32_t cols[kBinRows];
 #pragma unroll
@@ -224,17 +226,17 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                         const uint32_t r = static_cast<uint32_t>(w >> b.region_shift);
                         off[q][i] = static_cast<uint32_t>(w) & rmask;
                         bool dup = false;
-                        if (b.dedup) {  // w < 2^32 (pack)
+                        if (kDedup && b.dedup) {  // w < 2^32 (pack)
                             const uint32_t key = static_cast<uint32_t>(w);
                             uint32_t* slot = s_seen + ((key * 0x9E3779B1u) >> (32 - kDedupBits));
                             dup = *slot == key;
                             if (!dup) *slot = key;
                         }
-                        if (!dup) rr[q][i] = (r << 16) | atomicAdd(&s_cnt[r], 1u);
+                        if (!kDedup || !dup) rr[q][i] = (r << 16) | atomicAdd(&s_cnt[r], 1u);
                     }
                 }
                 if (live && (sample & c.tau_mask) == 0u) {  // sampled (1 in 2^tau): rough stamps
-                    const uint32_t rslot = reduce32(hash_u32(c.sub_rslot, dst[q]), c.g);
+                    const uint32_t rslot = reduce32(hash_u32k(c.sub_rslot, c.kh_rslot, dst[q]), c.g);
                     for (uint32_t i = 0; i < nrows; ++i)
                         atomicMin(stamp + i * rrow + static_cast<uint64_t>(cols[i < kBinRows ? i : 0]) * c.g + rslot,
                                   base + q);
@@ -243,8 +245,14 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
                 }
             }
         };
-        if (valid == kBinPerThread) place(std::true_type{});
-        else place(std::false_type{});
+        // the filter's branch hoisted out of the mark loop (it is off unless bins overflowed)
+        if (b.dedup || b.ab_nohoist) {
+            if (valid == kBinPerThread) place(std::true_type{}, std::true_type{});
+            else place(std::false_type{}, std::true_type{});
+        } else {
+            if (valid == kBinPerThread) place(std::true_type{}, std::false_type{});
+            else place(std::false_type{}, std::false_type{});
+        }
         if (__any_sync(0xFFFFFFFFu, smask != 0)) {
             uint32_t pos = warp_append(ev_count, __popc(smask));
 #pragma unroll

@@ -323,20 +323,34 @@ __global__ void __launch_bounds__(kBinThreads, 2) k_scan_bin(const uint32_t* __r
         for (uint32_t w2 = 0; w2 < kBinThreads / 32; ++w2) total += s_warp[w2];
         __syncthreads();
 
+        // branch-free when every mark of the tile is staged (4 rows, full tile, no filter)
+        auto scatter = [&](auto all_tag, auto pack_tag) {
+            constexpr bool kAll = decltype(all_tag)::value;
+            constexpr bool kPack = decltype(pack_tag)::value;
 #pragma unroll
-        for (uint32_t q = 0; q < kBinPerThread; ++q)
+            for (uint32_t q = 0; q < kBinPerThread; ++q)
 #pragma unroll
-            for (int i = 0; i < kBinRows; ++i)
-                if (rr[q][i] != 0xFFFFFFFFu) {
-                    const uint32_t reg = rr[q][i] >> 16;
-                    const uint32_t p = s_lbase[reg] + (rr[q][i] & 0xFFFFu);
-                    if (b.pack) {  // region and offset in one word: the write pass loads one value
-                        s_off[p] = (reg << b.region_shift) | off[q][i];
-                    } else {
-                        s_off[p] = off[q][i];
-                        s_reg[p] = static_cast<uint16_t>(reg);
+                for (int i = 0; i < kBinRows; ++i)
+                    if (kAll || rr[q][i] != 0xFFFFFFFFu) {
+                        const uint32_t reg = rr[q][i] >> 16;
+                        const uint32_t p = s_lbase[reg] + (rr[q][i] & 0xFFFFu);
+                        if constexpr (kPack) {  // region and offset in one word: the write pass loads one value
+                            s_off[p] = (reg << b.region_shift) | off[q][i];
+                        } else {
+                            s_off[p] = off[q][i];
+                            s_reg[p] = static_cast<uint16_t>(reg);
+                        }
                     }
-                }
+        };
+        const bool all_marks = ROWS == kBinRows && !b.dedup && !b.ab_nohoist &&
+                               (tile + 1) * static_cast<uint64_t>(kBinTile) <= n;
+        if (b.pack) {
+            if (all_marks) scatter(std::true_type{}, std::true_type{});
+            else scatter(std::false_type{}, std::true_type{});
+        } else {
+            if (all_marks) scatter(std::true_type{}, std::false_type{});
+            else scatter(std::false_type{}, std::false_type{});
+        }
         if (defer) {
 #pragma unroll
             for (int j = 0; j < kDefer; ++j)

@@ -527,10 +527,17 @@ __device__ __forceinline__ void split_tile(uint32_t* s_sorted, uint32_t r, uint3
         off[4 * q + 2] = e0 + 2 < n ? x.z : 0xFFFFFFFFu;
         off[4 * q + 3] = e0 + 3 < n ? x.w : 0xFFFFFFFFu;
     }
+    // full tiles (all but a region's last) rank and scatter without per-entry tests
+    const bool full = n == static_cast<uint32_t>(T * kSplitPerThread);
     uint32_t rank[kSplitPerThread];
+    if (full) {
 #pragma unroll
-    for (int k = 0; k < kSplitPerThread; ++k)
-        if (off[k] != 0xFFFFFFFFu) rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
+        for (int k = 0; k < kSplitPerThread; ++k) rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kSplitPerThread; ++k)
+            if (off[k] != 0xFFFFFFFFu) rank[k] = atomicAdd(&s_cnt[off[k] >> f.shift], 1u);
+    }
     __syncthreads();
     uint32_t mine = 0;
     const uint32_t b0 = tid * per_thread;
@@ -557,12 +564,20 @@ __device__ __forceinline__ void split_tile(uint32_t* s_sorted, uint32_t r, uint3
         run += cn;
     }
     __syncthreads();
+    if (full) {
 #pragma unroll
-    for (int k = 0; k < kSplitPerThread; ++k)
-        if (off[k] != 0xFFFFFFFFu) {
+        for (int k = 0; k < kSplitPerThread; ++k) {
             const uint32_t b = off[k] >> f.shift;
             s_sorted[s_lbase[b] + rank[k]] = (b << 16) | (off[k] & fmask);
         }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kSplitPerThread; ++k)
+            if (off[k] != 0xFFFFFFFFu) {
+                const uint32_t b = off[k] >> f.shift;
+                s_sorted[s_lbase[b] + rank[k]] = (b << 16) | (off[k] & fmask);
+            }
+    }
     __syncthreads();
     bool ovf = false;
     for (uint32_t i = tid; i < n; i += T) {

@@ -40,11 +40,13 @@ def _ragged_slices(oracle, name):
     return out
 
 
-@pytest.mark.parametrize("bins", ["default", "forced"])
+@pytest.mark.parametrize("bins", ["default", "forced", "forced_nohoist"])
 @pytest.mark.parametrize("name", ["contended", "drift_evict", "pipeline_small"])
 def test_ragged_and_empty_slices(gpu, oracle, name, bins, monkeypatch):
-    if bins == "forced":
+    if bins != "default":
         monkeypatch.setenv("SRLA_FORCE_BINS", "1")  # tiny bins: the overflow paths run too
+    if bins == "forced_nohoist":  # K1's per-mark filter test and scatter tests (the A/B path)
+        monkeypatch.setenv("SRLA_K1_HOIST", "0")
     cfg, _ = S.SCENARIOS[name]
     slices = _ragged_slices(oracle, name)
     a = GF.run_flow(_oracle(oracle, cfg), cfg, slices)
